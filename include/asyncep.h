@@ -1,0 +1,196 @@
+/*
+ * asyncep.h -- C ABI of the B200-native AsyncEP MoE-layer hot path
+ * (arxiv/paper_2605_02960, "MoE-Prefill", S6.2 "Asynchronous Expert Parallelism").
+ *
+ * What the library computes (S2.2): for every local token x_t,
+ *     logits = W_r x_t  (fp32)   ->  top-k experts S_t (desc. logit, ties -> lower id)
+ *     w_tj   = softmax over the k selected logits (== softmax -> top-k -> renormalise)
+ *     y_t    = r_t + sum_j w_tj * W_down[S_tj] ( silu(W_gate[S_tj] x_t) * (W_up[S_tj] x_t) )
+ * with the four steps (1) router GEMM + softmax + top-k, (2) local permute/dispatch,
+ * (3) grouped expert GEMM gate/up -> SwiGLU -> down, (4) weighted combine, all on the
+ * caller's compute stream.  Concurrently the NEXT layer's expert
+ * weights, sharded 1/N per GPU by expert index, are AllGathered into a double-buffered
+ * slot on the caller's comm stream, ordered against compute by CUDA events.
+ * asyncep_saturation_T is Eq. 1 in the per-layer token form.
+ *
+ * Conventions
+ *  - Every pointer named "device" is a CUDA device pointer on the current device; all
+ *    device buffers and both streams are allocated and OWNED BY THE CALLER and must
+ *    outlive the context.  The library owns only the context, its CUDA events and its
+ *    TMA descriptors.  The NCCL communicator is BORROWED (never destroyed).
+ *  - All compute entry points enqueue work and return; no host synchronisation.
+ *  - Every call returns an asyncep_status; asyncep_last_error() returns a thread-local
+ *    message for the last failure.  Degenerate inputs (num_tokens == 0) are no-ops.
+ *  - Not thread-safe per context; one context per GPU per process.
+ *  - Data types: bf16 = IEEE bfloat16 (2 B); e4m3 = OCP FP8 E4M3FN (1 B); fp32.
+ */
+#ifndef ASYNCEP_H
+#define ASYNCEP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASYNCEP_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ASYNCEP_API __attribute__((visibility("default")))
+#else
+#define ASYNCEP_API
+#endif
+
+typedef struct asyncep_ctx asyncep_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  ASYNCEP_OK = 0,
+  ASYNCEP_ERR_INVALID_ARG = 1,   /* bad shape / alignment / null / range              */
+  ASYNCEP_ERR_UNSUPPORTED = 2,   /* valid but not implemented (e.g. dtype, no GPU)      */
+  ASYNCEP_ERR_CUDA = 3,          /* a CUDA runtime/driver call failed                    */
+  ASYNCEP_ERR_NCCL = 4,          /* NCCL missing or a collective failed                  */
+  ASYNCEP_ERR_NOT_PREFETCHED = 5,/* forward(l) without prefetch(l) (gathered layers)     */
+  ASYNCEP_ERR_WORKSPACE = 6      /* num_tokens > max_tokens                              */
+} asyncep_status;
+
+typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
+
+/* Debug / test flags (asyncep_config.flags).  Default 0 = the production path. */
+#define ASYNCEP_FLAG_IDENTITY_EXPERTS 0x1 /* skip the grouped GEMM: Y_perm = X_perm (plumbing pin)      */
+#define ASYNCEP_FLAG_SIMT_GEMM        0x2 /* CUDA-core grouped GEMM instead of tcgen05 (sanitizer runs) */
+#define ASYNCEP_FLAG_STAGE_TIMING     0x4 /* record CUDA events around each stage (asyncep_stage_times) */
+#define ASYNCEP_FLAG_SIMT_ROUTER      0x8 /* CUDA-core router logits instead of tcgen05                */
+
+typedef struct {
+  int32_t num_layers;      /* L                                                         */
+  int32_t num_experts;     /* E (E % world_size == 0)                                   */
+  int32_t top_k;           /* k, 1 <= k <= min(E, 16)                                   */
+  int32_t hidden;          /* H, multiple of 64                                         */
+  int32_t ffn;             /* h (expert FFN width), multiple of 128                     */
+  int32_t expert_dtype;    /* asyncep_dtype of the expert weights                       */
+  int32_t world_size;      /* N ranks sharing the expert shards                         */
+  int32_t rank;            /* r, 0 <= r < N                                             */
+  int32_t replicate_layer0;/* 1: layer 0 is fully resident on every rank */
+  int32_t norm_topk;       /* 1: renormalise the k weights (reading R1); 0: raw softmax */
+  int64_t max_tokens;      /* upper bound on num_tokens per forward (workspace sizing)  */
+  float   gamma;           /* Eq. 1 jitter margin, >= 1 (PAPER.md:319 default 1.2)      */
+  int32_t flags;           /* ASYNCEP_FLAG_*                                            */
+} asyncep_config;
+
+/*
+ * Packed expert layout (the shard / slot format).  One expert is one contiguous blob:
+ *   BF16:  [ W_gu : 2h x H bf16 | W_down : H x h bf16 ]
+ *   FP8 :  [ W_gu : 2h x H e4m3 | W_down : H x h e4m3 | s_gu : 2h fp32 | s_down : H fp32 ]
+ * both matrices row-major with the contraction dim (K) contiguous ("K-major").  W_gu rows
+ * are gate/up interleaved per 128-row block: rows [256b, 256b+128) are gate rows
+ * [128b, 128b+128), rows [256b+128, 256b+256) are the matching up rows, so one
+ * 256-wide GEMM N-tile holds matching gate and up columns (SwiGLU fuses into its
+ * epilogue).  FP8 scales are per output row (dequantised weight = code * scale).
+ * A layer is E blobs in expert order; rank r's shard is experts [r*E/N, (r+1)*E/N),
+ * so the rank-major AllGather of shards IS the layer.
+ */
+ASYNCEP_API size_t asyncep_expert_bytes(const asyncep_config* cfg);   /* bytes of one packed expert    */
+ASYNCEP_API size_t asyncep_slot_bytes(const asyncep_config* cfg);     /* E * expert_bytes (one layer)  */
+ASYNCEP_API size_t asyncep_shard_bytes(const asyncep_config* cfg);    /* (E/N) * expert_bytes          */
+ASYNCEP_API size_t asyncep_workspace_size(const asyncep_config* cfg); /* device scratch for forward    */
+
+/*
+ * Pack natural-layout weights of `count` experts into packed blobs at `out` (device).
+ *   BF16: gate, up : [count, h, H] bf16; down : [count, H, h] bf16 (device, contiguous);
+ *         scales must be NULL.
+ *   FP8 : gate, up, down are e4m3 codes in the same shapes; gate_scale, up_scale :
+ *         [count, h] fp32, down_scale : [count, H] fp32.
+ * Enqueued on `stream` (cudaStream_t, may be NULL = legacy default stream).
+ */
+ASYNCEP_API asyncep_status asyncep_pack_experts(const asyncep_config* cfg, int32_t count,
+                                    const void* gate, const void* up, const void* down,
+                                    const float* gate_scale, const float* up_scale,
+                                    const float* down_scale, void* out, void* stream);
+
+/*
+ * Create a context.
+ *  nccl_comm     : ncclComm_t borrowed from the caller (torch ProcessGroupNCCL._comm_ptr());
+ *                  may be NULL when world_size == 1.
+ *  compute_stream, comm_stream : cudaStream_t, caller-owned (comm_stream may be NULL when
+ *                  world_size == 1).
+ *  router_w      : [L] device pointers, each [E, H] bf16 (replicated on every rank).
+ *  expert_shard  : [L] device pointers to this rank's packed shard of layer l
+ *                  (asyncep_shard_bytes each), except layer 0 when replicate_layer0 == 1,
+ *                  where it is the full packed layer (asyncep_slot_bytes).  When
+ *                  world_size == 1 every entry is the full packed layer.
+ *  slot0, slot1  : 2 device buffers of asyncep_slot_bytes (NULL allowed if world_size==1).
+ *  workspace     : asyncep_workspace_size bytes of device memory, 256-B aligned.
+ * Errors: INVALID_ARG on any shape/alignment violation, NCCL if world_size > 1 and NCCL
+ * symbols cannot be resolved in the process, CUDA on runtime failures.
+ */
+ASYNCEP_API asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* compute_stream,
+                            void* comm_stream, const void* const* router_w,
+                            const void* const* expert_shard, void* slot0, void* slot1,
+                            void* workspace, asyncep_ctx** out);
+
+/*
+ * Issue the background AllGather of layer `layer`'s expert shards into slot[layer % 2]
+ * on the comm stream ("MoE gatherer").  Waits (on the device) until the
+ * slot's previous occupant (layer - 2) has finished its GEMMs; records ag_done[layer%2].
+ * No-op (returns OK) when world_size == 1 or (layer == 0 and replicate_layer0).
+ */
+ASYNCEP_API asyncep_status asyncep_prefetch_layer(asyncep_ctx* ctx, int32_t layer);
+
+/*
+ * Test hook: like asyncep_prefetch_layer but without NCCL -- copies the N shards given in
+ * `shards` ([N] device pointers, each asyncep_shard_bytes) rank-major into the slot with
+ * device-to-device copies on the comm stream, under the same event ordering.  Lets the
+ * double-buffer / event machinery run on one GPU.  Requires world_size > 1.
+ */
+ASYNCEP_API asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* ctx, int32_t layer,
+                                            const void* const* shards);
+
+/*
+ * The MoE FFN forward of layer `layer` on the compute stream.
+ *  x         : [num_tokens, H] bf16 device, 16-B aligned rows.
+ *  residual  : nullable [num_tokens, H] bf16 device; added to the output (reading R9).
+ *  y         : [num_tokens, H] bf16 device output; may alias residual but not x.
+ *  topk_ids_out [num_tokens, k] int32, topk_w_out [num_tokens, k] fp32,
+ *  expert_counts_out [E] int32 : nullable device outputs (router decisions, in the
+ *                  canonical order: descending logit, ties -> lower expert id).
+ * Gathered layers require a prior asyncep_prefetch_layer(layer) (else NOT_PREFETCHED).
+ * num_tokens == 0 is a successful no-op; num_tokens > max_tokens -> WORKSPACE.
+ */
+ASYNCEP_API asyncep_status asyncep_moe_forward(asyncep_ctx* ctx, int32_t layer, const void* x,
+                                   int64_t num_tokens, const void* residual, void* y,
+                                   int32_t* topk_ids_out, float* topk_w_out,
+                                   int32_t* expert_counts_out);
+
+/*
+ * Saturation threshold, Eq. 1 in per-layer form (readings R11, R12):
+ *   t_AG = (N-1)/N * E*3*H*h*b / ag_bytes_per_s;  T_FLOPs = gamma * t_AG * flops_per_s;
+ *   T_tok = T_FLOPs / (6*k*H*h)  [tokens per GPU per layer].
+ * Pure function (no context); N == 1 gives 0.  Outputs may be NULL.
+ */
+ASYNCEP_API asyncep_status asyncep_saturation_T(const asyncep_config* cfg, double flops_per_s,
+                                    double ag_bytes_per_s, double* tokens_per_gpu_out,
+                                    double* flops_out);
+
+/*
+ * Stage timing (ASYNCEP_FLAG_STAGE_TIMING, cf. the paper's gated per-layer CUDA-event
+ * hooks).  Synchronises on the recorded events and returns, summed
+ * over all forwards since the last reset, the milliseconds of each stage:
+ *   [0] router  [1] permute  [2] exposed gather wait  [3] GEMM1 gate/up+SwiGLU
+ *   [4] GEMM2 down  [5] combine   (n_stages <= 6), and the number of forwards counted.
+ */
+ASYNCEP_API asyncep_status asyncep_stage_times(asyncep_ctx* ctx, double* ms_out, int32_t n_stages,
+                                   int64_t* forwards_out);
+ASYNCEP_API asyncep_status asyncep_reset_stage_times(asyncep_ctx* ctx);
+
+/* Number of kernels the library launched since context creation (host-side counter). */
+ASYNCEP_API int64_t asyncep_kernel_launches(const asyncep_ctx* ctx);
+
+ASYNCEP_API asyncep_status asyncep_destroy(asyncep_ctx* ctx);
+ASYNCEP_API const char* asyncep_last_error(void);
+ASYNCEP_API int32_t asyncep_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASYNCEP_H */

@@ -1,0 +1,218 @@
+"""Thin Python binding of the C ABI in ``include/asyncep.h`` (libasyncep.so).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA
+kernels.  The functions carry the C names.  There is no CPU fallback: if the
+extension is missing the import of this module fails loudly.
+
+PyTorch supplies device memory (tensors), streams (``torch.cuda.Stream``) and the NCCL
+communicator (``ProcessGroupNCCL._comm_ptr()``); the library borrows all of them.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libasyncep.so")
+
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_NOT_PREFETCHED, ERR_WORKSPACE = range(7)
+BF16, FP8_E4M3 = 0, 1
+FLAG_IDENTITY_EXPERTS = 0x1
+FLAG_SIMT_GEMM = 0x2
+FLAG_STAGE_TIMING = 0x4
+FLAG_SIMT_ROUTER = 0x8
+STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
+
+
+class AsyncEPError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"asyncep status {status}: {msg}")
+        self.status = status
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("num_layers", ctypes.c_int32), ("num_experts", ctypes.c_int32),
+                ("top_k", ctypes.c_int32), ("hidden", ctypes.c_int32), ("ffn", ctypes.c_int32),
+                ("expert_dtype", ctypes.c_int32), ("world_size", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("replicate_layer0", ctypes.c_int32),
+                ("norm_topk", ctypes.c_int32), ("max_tokens", ctypes.c_int64),
+                ("gamma", ctypes.c_float), ("flags", ctypes.c_int32)]
+
+
+def make_config(num_layers, num_experts, top_k, hidden, ffn, *, expert_dtype=BF16, world_size=1,
+                rank=0, replicate_layer0=1, norm_topk=1, max_tokens=1, gamma=1.2, flags=0) -> Config:
+    return Config(num_layers, num_experts, top_k, hidden, ffn, expert_dtype, world_size, rank,
+                  replicate_layer0, norm_topk, max_tokens, gamma, flags)
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, D, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+        CP = ctypes.POINTER(Config)
+        sig = {
+            "asyncep_abi_version": ([], I32),
+            "asyncep_last_error": ([], ctypes.c_char_p),
+            "asyncep_expert_bytes": ([CP], SZ),
+            "asyncep_slot_bytes": ([CP], SZ),
+            "asyncep_shard_bytes": ([CP], SZ),
+            "asyncep_workspace_size": ([CP], SZ),
+            "asyncep_pack_experts": ([CP, I32, P, P, P, P, P, P, P, P], I32),
+            "asyncep_init": ([CP, P, P, P, P, P, P, P, P, ctypes.POINTER(P)], I32),
+            "asyncep_prefetch_layer": ([P, I32], I32),
+            "asyncep_prefetch_layer_local": ([P, I32, P], I32),
+            "asyncep_moe_forward": ([P, I32, P, I64, P, P, P, P, P], I32),
+            "asyncep_saturation_T": ([CP, D, D, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
+            "asyncep_stage_times": ([P, ctypes.POINTER(D), I32, ctypes.POINTER(I64)], I32),
+            "asyncep_reset_stage_times": ([P], I32),
+            "asyncep_kernel_launches": ([P], I64),
+            "asyncep_destroy": ([P], I32),
+        }
+        for name, (args, res) in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != OK:
+        raise AsyncEPError(status, lib().asyncep_last_error().decode(errors="replace"))
+
+
+def _p(t) -> int | None:
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return t.data_ptr()
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+# ------------------------------------------------------------------------------ sizes
+def asyncep_expert_bytes(cfg: Config) -> int:
+    return lib().asyncep_expert_bytes(ctypes.byref(cfg))
+
+
+def asyncep_slot_bytes(cfg: Config) -> int:
+    return lib().asyncep_slot_bytes(ctypes.byref(cfg))
+
+
+def asyncep_shard_bytes(cfg: Config) -> int:
+    return lib().asyncep_shard_bytes(ctypes.byref(cfg))
+
+
+def asyncep_workspace_size(cfg: Config) -> int:
+    n = lib().asyncep_workspace_size(ctypes.byref(cfg))
+    if n == 0:
+        _check(ERR_INVALID_ARG)
+    return n
+
+
+def asyncep_pack_experts(cfg: Config, gate, up, down, out, stream=None, gate_scale=None,
+                         up_scale=None, down_scale=None) -> None:
+    _check(lib().asyncep_pack_experts(ctypes.byref(cfg), gate.shape[0], _p(gate), _p(up), _p(down),
+                                      _p(gate_scale), _p(up_scale), _p(down_scale), _p(out),
+                                      _stream(stream)))
+
+
+# ------------------------------------------------------------------------------ context
+@dataclass
+class Context:
+    handle: ctypes.c_void_p
+    cfg: Config
+    keep: list = field(default_factory=list)  # tensors that must outlive the context
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.asyncep_destroy(self.handle)
+            self.handle = None
+
+
+def asyncep_init(cfg: Config, nccl_comm, compute_stream, comm_stream, router_w, expert_shard,
+                 slot0, slot1, workspace) -> Context:
+    L = cfg.num_layers
+    assert len(router_w) == L and len(expert_shard) == L
+    rw = (ctypes.c_void_p * L)(*[_p(t) for t in router_w])
+    sh = (ctypes.c_void_p * L)(*[_p(t) for t in expert_shard])
+    h = ctypes.c_void_p()
+    _check(lib().asyncep_init(ctypes.byref(cfg), nccl_comm, _stream(compute_stream), _stream(comm_stream),
+                              rw, sh, _p(slot0), _p(slot1), _p(workspace), ctypes.byref(h)))
+    return Context(h, cfg, [list(router_w), list(expert_shard), slot0, slot1, workspace,
+                            compute_stream, comm_stream])
+
+
+def asyncep_prefetch_layer(ctx: Context, layer: int) -> None:
+    _check(lib().asyncep_prefetch_layer(ctx.handle, layer))
+
+
+def asyncep_prefetch_layer_local(ctx: Context, layer: int, shards) -> None:
+    arr = (ctypes.c_void_p * len(shards))(*[_p(t) for t in shards])
+    _check(lib().asyncep_prefetch_layer_local(ctx.handle, layer, arr))
+
+
+def asyncep_moe_forward(ctx: Context, layer: int, x: torch.Tensor, residual=None, y=None,
+                        topk_ids_out=None, topk_w_out=None, expert_counts_out=None) -> torch.Tensor:
+    T = x.shape[0]
+    if y is None:
+        y = torch.empty_like(x)
+    _check(lib().asyncep_moe_forward(ctx.handle, layer, _p(x), T, _p(residual), _p(y),
+                                     _p(topk_ids_out), _p(topk_w_out), _p(expert_counts_out)))
+    return y
+
+
+def asyncep_saturation_T(cfg: Config, flops_per_s: float, ag_bytes_per_s: float):
+    t = ctypes.c_double()
+    f = ctypes.c_double()
+    _check(lib().asyncep_saturation_T(ctypes.byref(cfg), flops_per_s, ag_bytes_per_s, ctypes.byref(t),
+                                      ctypes.byref(f)))
+    return t.value, f.value
+
+
+def asyncep_stage_times(ctx: Context):
+    ms = (ctypes.c_double * len(STAGES))()
+    n = ctypes.c_int64()
+    _check(lib().asyncep_stage_times(ctx.handle, ms, len(STAGES), ctypes.byref(n)))
+    return dict(zip(STAGES, list(ms))), n.value
+
+
+def asyncep_reset_stage_times(ctx: Context) -> None:
+    _check(lib().asyncep_reset_stage_times(ctx.handle))
+
+
+def asyncep_kernel_launches(ctx: Context) -> int:
+    return lib().asyncep_kernel_launches(ctx.handle)
+
+
+def asyncep_destroy(ctx: Context) -> None:
+    if ctx.handle:
+        _check(lib().asyncep_destroy(ctx.handle))
+        ctx.handle = None
+
+
+def asyncep_abi_version() -> int:
+    return lib().asyncep_abi_version()
+
+
+def nccl_comm_ptr(pg=None) -> int:
+    """The ncclComm_t of torch's NCCL process group (must be eagerly initialised)."""
+    import torch.distributed as dist
+    pg = pg or dist.group.WORLD
+    return pg._get_backend(torch.device("cuda"))._comm_ptr()

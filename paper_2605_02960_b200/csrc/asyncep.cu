@@ -1,0 +1,472 @@
+// asyncep.cu -- the C ABI (include/asyncep.h): context, workspace carving, the
+// double-buffered expert slot with its CUDA-event ordering, the NCCL AllGather
+// ("MoE gatherer") and the four-step forward.
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "asyncep.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using aep::bf16;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+asyncep_status fail(asyncep_status st, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess)                                                                          \
+      return fail(ASYNCEP_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                  __LINE__);                                                                        \
+  } while (0)
+
+// NCCL entry points, resolved in the running process (the caller's torch already loaded
+// libnccl.so.2; we never link a second copy).
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+typedef int (*nccl_async_err_fn)(void*, int*);
+struct NcclApi {
+  nccl_allgather_fn allgather = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  nccl_async_err_fn async_err = nullptr;
+};
+bool resolve_nccl(NcclApi& api) {
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = RTLD_DEFAULT;
+  api.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
+  api.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+  api.async_err = (nccl_async_err_fn)dlsym(h, "ncclCommGetAsyncError");
+  return api.allgather != nullptr;
+}
+constexpr int kNcclUint8 = 1;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, xperm, act, total;
+};
+WsLayout ws_layout(const asyncep_config& c) {
+  WsLayout L{};
+  const size_t Tm = (size_t)c.max_tokens, k = (size_t)c.top_k, E = (size_t)c.num_experts;
+  const size_t R = Tm * k;
+  const size_t nblk = (Tm + aep::kPermTokensPerBlock - 1) / aep::kPermTokensPerBlock;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.ids = take(R * 4);
+  L.w = take(R * 4);
+  L.dest = take(R * 4);
+  L.src_tok = take(R * 4);
+  L.blk = take(nblk * E * 4);
+  L.offsets = take((E + 1) * 4);
+  L.tile_start = take((E + 1) * 4);
+  L.counts = take(E * 4);
+  L.xperm = take(R * (size_t)c.hidden * 2);  // X_perm, reused as Y_perm after GEMM1
+  L.act = take(R * (size_t)c.ffn * 2);
+  L.total = o;
+  return L;
+}
+
+asyncep_status check_config(const asyncep_config* c) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "config is NULL");
+  if (c->num_layers <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "num_layers must be > 0");
+  if (c->num_experts <= 0 || c->num_experts > aep::kMaxExperts)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "num_experts must be in [1, %d]", aep::kMaxExperts);
+  if (c->top_k <= 0 || c->top_k > c->num_experts || c->top_k > aep::kMaxTopK)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "top_k must be in [1, min(E, %d)]", aep::kMaxTopK);
+  if (c->hidden <= 0 || c->hidden % 64) return fail(ASYNCEP_ERR_INVALID_ARG, "hidden must be a multiple of 64");
+  if (c->hidden >= 256 && c->hidden % 256)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "hidden >= 256 must be a multiple of 256");
+  if (c->ffn <= 0 || c->ffn % 128) return fail(ASYNCEP_ERR_INVALID_ARG, "ffn must be a multiple of 128");
+  if (c->expert_dtype != ASYNCEP_BF16)
+    return fail(ASYNCEP_ERR_UNSUPPORTED, "expert_dtype %d not supported by this build", c->expert_dtype);
+  if (c->world_size <= 0 || c->rank < 0 || c->rank >= c->world_size)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "bad world_size/rank");
+  if (c->num_experts % c->world_size)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "num_experts (%d) %% world_size (%d) != 0", c->num_experts,
+                c->world_size);
+  if (c->max_tokens <= 0 || (int64_t)c->max_tokens * c->top_k >= (int64_t)1 << 31)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "max_tokens out of range");
+  if (!(c->gamma >= 1.0f)) return fail(ASYNCEP_ERR_INVALID_ARG, "gamma must be >= 1");
+  return ASYNCEP_OK;
+}
+
+constexpr int kStages = 6;
+constexpr int kEventsPerFwd = kStages + 1;
+constexpr int kMaxPendingFwd = 512;
+
+}  // namespace
+
+struct asyncep_ctx {
+  asyncep_config cfg;
+  void* comm = nullptr;
+  NcclApi nccl;
+  cudaStream_t cs = nullptr, ms = nullptr;
+  std::vector<const void*> router_w, shard;
+  void* slot[2] = {nullptr, nullptr};
+  uint8_t* ws = nullptr;
+  WsLayout L;
+  size_t expert_bytes = 0, slot_bytes = 0, shard_bytes = 0;
+  int num_sms = 148;
+  // slot bookkeeping (host side): layer held / being gathered, and whether its forward ran
+  int slot_layer[2] = {-1, -1};
+  bool slot_consumed[2] = {true, true};
+  cudaEvent_t ag_done[2] = {nullptr, nullptr}, slot_free[2] = {nullptr, nullptr};
+  // tcgen05 tensor maps
+  aep::ActMaps act_maps;
+  std::vector<aep::GemmMaps> layer_maps;  // per resident layer (index l), valid if resident[l]
+  std::vector<char> resident;
+  aep::GemmMaps slot_maps[2];
+  // stage timing
+  std::vector<cudaEvent_t> ev_pool;
+  int ev_used = 0;  // forwards recorded since the last flush
+  double stage_ms[kStages] = {0};
+  int64_t fwd_count = 0;
+  int64_t launches = 0;
+};
+
+namespace {
+
+bool layer_resident(const asyncep_ctx* c, int l) {
+  return c->cfg.world_size == 1 || (l == 0 && c->cfg.replicate_layer0);
+}
+
+asyncep_status flush_timing(asyncep_ctx* c) {
+  if (c->ev_used == 0) return ASYNCEP_OK;
+  CUDA_TRY(cudaEventSynchronize(c->ev_pool[(size_t)c->ev_used * kEventsPerFwd - 1]));
+  for (int f = 0; f < c->ev_used; ++f) {
+    cudaEvent_t* e = &c->ev_pool[(size_t)f * kEventsPerFwd];
+    for (int s = 0; s < kStages; ++s) {
+      float ms = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e[s], e[s + 1]));
+      c->stage_ms[s] += ms;
+    }
+  }
+  c->fwd_count += c->ev_used;
+  c->ev_used = 0;
+  return ASYNCEP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t asyncep_abi_version(void) { return ASYNCEP_ABI_VERSION; }
+const char* asyncep_last_error(void) { return g_last_error.c_str(); }
+
+size_t asyncep_expert_bytes(const asyncep_config* c) {
+  if (!c) return 0;
+  return (size_t)3 * c->hidden * c->ffn * 2;
+}
+size_t asyncep_slot_bytes(const asyncep_config* c) {
+  return c ? asyncep_expert_bytes(c) * (size_t)c->num_experts : 0;
+}
+size_t asyncep_shard_bytes(const asyncep_config* c) {
+  return (c && c->world_size > 0) ? asyncep_expert_bytes(c) * (size_t)(c->num_experts / c->world_size) : 0;
+}
+size_t asyncep_workspace_size(const asyncep_config* c) {
+  if (check_config(c) != ASYNCEP_OK) return 0;
+  return ws_layout(*c).total;
+}
+
+asyncep_status asyncep_pack_experts(const asyncep_config* cfg, int32_t count, const void* gate, const void* up,
+                                    const void* down, const float* gs, const float* us, const float* ds, void* out,
+                                    void* stream) {
+  asyncep_status st = check_config(cfg);
+  if (st) return st;
+  if (count < 0 || count > cfg->num_experts) return fail(ASYNCEP_ERR_INVALID_ARG, "bad expert count");
+  if (count == 0) return ASYNCEP_OK;
+  if (!gate || !up || !down || !out) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
+  if (gs || us || ds) return fail(ASYNCEP_ERR_INVALID_ARG, "scales must be NULL for BF16");
+  if (((uintptr_t)gate | (uintptr_t)up | (uintptr_t)down | (uintptr_t)out) & 15)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "pointers must be 16-B aligned");
+  aep::launch_pack_bf16((const bf16*)gate, (const bf16*)up, (const bf16*)down, count, cfg->hidden, cfg->ffn,
+                        asyncep_expert_bytes(cfg), (uint8_t*)out, (cudaStream_t)stream);
+  CUDA_TRY(cudaGetLastError());
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* compute_stream, void* comm_stream,
+                            const void* const* router_w, const void* const* expert_shard, void* slot0,
+                            void* slot1, void* workspace, asyncep_ctx** out) {
+  asyncep_status st = check_config(cfg);
+  if (st) return st;
+  if (!out || !router_w || !expert_shard || !workspace) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
+  *out = nullptr;
+  if ((uintptr_t)workspace & 255) return fail(ASYNCEP_ERR_INVALID_ARG, "workspace must be 256-B aligned");
+  const int L = cfg->num_layers;
+  for (int l = 0; l < L; ++l) {
+    if (!router_w[l] || !expert_shard[l]) return fail(ASYNCEP_ERR_INVALID_ARG, "null weight pointer (layer %d)", l);
+    if (((uintptr_t)router_w[l] | (uintptr_t)expert_shard[l]) & 15)
+      return fail(ASYNCEP_ERR_INVALID_ARG, "weights must be 16-B aligned (layer %d)", l);
+  }
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10) return fail(ASYNCEP_ERR_UNSUPPORTED, "device is sm_%d%d; this library is sm_100a", prop.major, prop.minor);
+
+  asyncep_ctx* c = new asyncep_ctx();
+  c->cfg = *cfg;
+  c->cs = (cudaStream_t)compute_stream;
+  c->ms = (cudaStream_t)comm_stream;
+  c->num_sms = prop.multiProcessorCount;
+  c->router_w.assign(router_w, router_w + L);
+  c->shard.assign(expert_shard, expert_shard + L);
+  c->ws = (uint8_t*)workspace;
+  c->L = ws_layout(*cfg);
+  c->expert_bytes = asyncep_expert_bytes(cfg);
+  c->slot_bytes = asyncep_slot_bytes(cfg);
+  c->shard_bytes = asyncep_shard_bytes(cfg);
+  auto bail = [&](asyncep_status s) {
+    asyncep_destroy(c);
+    return s;
+  };
+  if (cfg->world_size > 1) {
+    if (!slot0 || !slot1 || ((uintptr_t)slot0 | (uintptr_t)slot1) & 15)
+      return bail(fail(ASYNCEP_ERR_INVALID_ARG, "world_size > 1 needs two 16-B aligned slots"));
+    if (!c->ms) return bail(fail(ASYNCEP_ERR_INVALID_ARG, "world_size > 1 needs a comm stream"));
+    c->slot[0] = slot0;
+    c->slot[1] = slot1;
+    c->comm = nccl_comm;
+    if (nccl_comm && !resolve_nccl(c->nccl))
+      return bail(fail(ASYNCEP_ERR_NCCL, "ncclAllGather not found in the process (load torch's NCCL first)"));
+  } else if (nccl_comm) {
+    c->comm = nccl_comm;
+    if (!resolve_nccl(c->nccl)) return bail(fail(ASYNCEP_ERR_NCCL, "ncclAllGather not found in the process"));
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (cudaEventCreateWithFlags(&c->ag_done[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(ASYNCEP_ERR_CUDA, "cudaEventCreate failed"));
+  }
+  // TMA descriptors: activations (fixed workspace addresses), each resident layer, both slots.
+  const int64_t R = (int64_t)cfg->max_tokens * cfg->top_k;
+  if (!aep::make_act_maps(c->act_maps, (const bf16*)(c->ws + c->L.xperm), (const bf16*)(c->ws + c->L.act), R,
+                          cfg->hidden, cfg->ffn))
+    return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
+  c->layer_maps.resize(L);
+  c->resident.assign(L, 0);
+  for (int l = 0; l < L; ++l) {
+    if (!layer_resident(c, l)) continue;
+    c->resident[l] = 1;
+    if (!aep::make_weight_maps(c->layer_maps[l], c->shard[l], c->expert_bytes, cfg->num_experts, cfg->hidden,
+                               cfg->ffn, c->act_maps.bn2))
+      return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l));
+  }
+  for (int i = 0; i < 2; ++i)
+    if (c->slot[i] && !aep::make_weight_maps(c->slot_maps[i], c->slot[i], c->expert_bytes, cfg->num_experts,
+                                             cfg->hidden, cfg->ffn, c->act_maps.bn2))
+      return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (slot %d)", i));
+  *out = c;
+  return ASYNCEP_OK;
+}
+
+static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void* const* shards) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
+  if (layer_resident(c, layer)) return ASYNCEP_OK;
+  const int s = layer % 2;
+  if (!c->slot_consumed[s] && c->slot_layer[s] != layer)
+    return fail(ASYNCEP_ERR_INVALID_ARG,
+                "slot %d still holds layer %d whose forward has not been issued (at most 2 layers in flight)", s,
+                c->slot_layer[s]);
+  // WAR: the slot's previous occupant must have finished its GEMMs.
+  CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
+  if (shards) {
+    for (int r = 0; r < c->cfg.world_size; ++r) {
+      if (!shards[r]) return fail(ASYNCEP_ERR_INVALID_ARG, "null shard %d", r);
+      CUDA_TRY(cudaMemcpyAsync((uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes, shards[r], c->shard_bytes,
+                               cudaMemcpyDeviceToDevice, c->ms));
+    }
+  } else {
+    if (!c->comm) return fail(ASYNCEP_ERR_NCCL, "no NCCL communicator (use asyncep_prefetch_layer_local)");
+    const int r = c->nccl.allgather(c->shard[layer], c->slot[s], c->shard_bytes, kNcclUint8, c->comm, c->ms);
+    if (r != 0)
+      return fail(ASYNCEP_ERR_NCCL, "ncclAllGather: %s", c->nccl.errstr ? c->nccl.errstr(r) : "error");
+  }
+  CUDA_TRY(cudaEventRecord(c->ag_done[s], c->ms));
+  c->slot_layer[s] = layer;
+  c->slot_consumed[s] = false;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_prefetch_layer(asyncep_ctx* c, int32_t layer) { return prefetch_common(c, layer, nullptr); }
+
+asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* c, int32_t layer, const void* const* shards) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (c->cfg.world_size < 2) return fail(ASYNCEP_ERR_INVALID_ARG, "prefetch_layer_local needs world_size > 1");
+  if (!shards) return fail(ASYNCEP_ERR_INVALID_ARG, "shards is NULL");
+  return prefetch_common(c, layer, shards);
+}
+
+asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x, int64_t T, const void* residual,
+                                   void* y, int32_t* ids_out, float* w_out, int32_t* counts_out) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  const asyncep_config& cf = c->cfg;
+  if (layer < 0 || layer >= cf.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
+  if (T < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "num_tokens < 0");
+  if (T > cf.max_tokens) return fail(ASYNCEP_ERR_WORKSPACE, "num_tokens %lld > max_tokens %lld", (long long)T,
+                                     (long long)cf.max_tokens);
+  if (T == 0) return ASYNCEP_OK;
+  if (!x || !y) return fail(ASYNCEP_ERR_INVALID_ARG, "x / y is NULL");
+  if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual) & 15)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "x / y / residual must be 16-B aligned");
+  if (x == y) return fail(ASYNCEP_ERR_INVALID_ARG, "y must not alias x");
+  const bool res = layer_resident(c, layer);
+  const int s = layer % 2;
+  if (!res && (c->slot_layer[s] != layer || c->slot_consumed[s]))
+    return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not prefetched", layer);
+
+  const int E = cf.num_experts, k = cf.top_k, H = cf.hidden, h = cf.ffn;
+  cudaStream_t st = c->cs;
+  uint8_t* ws = c->ws;
+  int32_t* ids = (int32_t*)(ws + c->L.ids);
+  float* w = (float*)(ws + c->L.w);
+  int32_t* dest = (int32_t*)(ws + c->L.dest);
+  int32_t* src_tok = (int32_t*)(ws + c->L.src_tok);
+  int32_t* blk = (int32_t*)(ws + c->L.blk);
+  int32_t* offsets = (int32_t*)(ws + c->L.offsets);
+  int32_t* tile_start = (int32_t*)(ws + c->L.tile_start);
+  int32_t* counts = (int32_t*)(ws + c->L.counts);
+  bf16* xperm = (bf16*)(ws + c->L.xperm);
+  bf16* act = (bf16*)(ws + c->L.act);
+  const int nblk = (int)((T + aep::kPermTokensPerBlock - 1) / aep::kPermTokensPerBlock);
+
+  const bool timing = (cf.flags & ASYNCEP_FLAG_STAGE_TIMING) != 0;
+  cudaEvent_t* ev = nullptr;
+  if (timing) {
+    if (c->ev_used == kMaxPendingFwd) {
+      asyncep_status fs = flush_timing(c);
+      if (fs) return fs;
+    }
+    if (c->ev_pool.empty()) {
+      c->ev_pool.resize((size_t)kMaxPendingFwd * kEventsPerFwd);
+      for (auto& e : c->ev_pool) CUDA_TRY(cudaEventCreate(&e));
+    }
+    ev = &c->ev_pool[(size_t)c->ev_used * kEventsPerFwd];
+    ++c->ev_used;
+    CUDA_TRY(cudaEventRecord(ev[0], st));
+  }
+  // (1) router GEMM + softmax + top-k
+  aep::launch_router_simt((const bf16*)x, (const bf16*)c->router_w[layer], T, H, E, k, cf.norm_topk, ids, w, st);
+  c->launches += 1;
+  if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
+  // (2) permute / dispatch
+  aep::launch_perm_hist(ids, T, k, E, blk, st);
+  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, st);
+  aep::launch_perm_scatter((const bf16*)x, ids, blk, T, H, k, E, dest, src_tok, xperm, st);
+  c->launches += 3;
+  if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
+  // wait for this layer's gathered experts (placed just before GEMM1 so router and
+  // permute also overlap the gather tail)
+  if (!res) CUDA_TRY(cudaStreamWaitEvent(st, c->ag_done[s], 0));
+  if (timing) CUDA_TRY(cudaEventRecord(ev[3], st));
+  // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
+  const uint8_t* wl = (const uint8_t*)(res ? c->shard[layer] : c->slot[s]);
+  const aep::GemmMaps& wm = res ? c->layer_maps[layer] : c->slot_maps[s];
+  aep::GroupedArgs g{offsets, tile_start, E,
+                     (int)(((int64_t)T * k + aep::kTileM - 1) / aep::kTileM + E)};
+  bf16* yperm = xperm;
+  if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
+    // Y_perm = X_perm (already in place)
+  } else if (cf.flags & ASYNCEP_FLAG_SIMT_GEMM) {
+    aep::launch_gemm1_simt(g, xperm, wl, c->expert_bytes, H, h, act, st);
+    if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
+    aep::launch_gemm2_simt(g, act, wl, c->expert_bytes, H, h, yperm, st);
+    c->launches += 2;
+  } else {
+    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, c->num_sms, st);
+    if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
+    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st);
+    c->launches += 2;
+  }
+  if (timing && (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS)) CUDA_TRY(cudaEventRecord(ev[4], st));
+  if (timing) CUDA_TRY(cudaEventRecord(ev[5], st));
+  if (!res) {
+    CUDA_TRY(cudaEventRecord(c->slot_free[s], st));
+    c->slot_consumed[s] = true;
+  }
+  // (4) weighted combine (+ residual)
+  aep::launch_combine(yperm, dest, w, (const bf16*)residual, (bf16*)y, T, H, k, st);
+  c->launches += 1;
+  if (timing) CUDA_TRY(cudaEventRecord(ev[6], st));
+  if (ids_out) CUDA_TRY(cudaMemcpyAsync(ids_out, ids, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, st));
+  if (w_out) CUDA_TRY(cudaMemcpyAsync(w_out, w, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, st));
+  if (counts_out) CUDA_TRY(cudaMemcpyAsync(counts_out, counts, (size_t)E * 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaGetLastError());
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_saturation_T(const asyncep_config* cfg, double flops_per_s, double ag_bytes_per_s,
+                                    double* tokens_out, double* flops_out) {
+  if (!cfg) return fail(ASYNCEP_ERR_INVALID_ARG, "config is NULL");
+  if (cfg->num_experts <= 0 || cfg->top_k <= 0 || cfg->hidden <= 0 || cfg->ffn <= 0 || cfg->world_size <= 0)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "bad shape");
+  if (!(flops_per_s > 0) || !(ag_bytes_per_s > 0)) return fail(ASYNCEP_ERR_INVALID_ARG, "rates must be > 0");
+  if (!(cfg->gamma >= 1.0f)) return fail(ASYNCEP_ERR_INVALID_ARG, "gamma must be >= 1");
+  const double b = cfg->expert_dtype == ASYNCEP_FP8_E4M3 ? 1.0 : 2.0;
+  const double n = (double)cfg->world_size;
+  const double per_tok_flops = 6.0 * cfg->top_k * (double)cfg->hidden * (double)cfg->ffn;
+  // t_AG = (N-1)/N * E*3*H*h*b / BW ; T_FLOPs = gamma * t_AG * F ; T_tok = T_FLOPs / (6 k H h)
+  const double t_ag = (n - 1.0) / n * (double)cfg->num_experts * 3.0 * cfg->hidden * (double)cfg->ffn * b /
+                      ag_bytes_per_s;
+  const double tf = (double)cfg->gamma * t_ag * flops_per_s;
+  if (flops_out) *flops_out = tf;
+  if (tokens_out) *tokens_out = tf / per_tok_flops;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_stage_times(asyncep_ctx* c, double* ms_out, int32_t n, int64_t* fwd_out) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  for (int i = 0; i < n && i < kStages; ++i) ms_out[i] = c->stage_ms[i];
+  if (fwd_out) *fwd_out = c->fwd_count;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_reset_stage_times(asyncep_ctx* c) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  for (double& v : c->stage_ms) v = 0.0;
+  c->fwd_count = 0;
+  return ASYNCEP_OK;
+}
+
+int64_t asyncep_kernel_launches(const asyncep_ctx* c) { return c ? c->launches : 0; }
+
+asyncep_status asyncep_destroy(asyncep_ctx* c) {
+  if (!c) return ASYNCEP_OK;
+  for (int i = 0; i < 2; ++i) {
+    if (c->ag_done[i]) cudaEventDestroy(c->ag_done[i]);
+    if (c->slot_free[i]) cudaEventDestroy(c->slot_free[i]);
+  }
+  for (auto& e : c->ev_pool)
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return ASYNCEP_OK;
+}
+
+}  // extern "C"

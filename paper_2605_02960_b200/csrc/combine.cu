@@ -1,0 +1,73 @@
+// combine.cu -- step (4): weighted combine / unpermute ("... and sums their
+// outputs"; reading R9 for the residual):
+//     y_t = r_t + sum_{j=0..k-1} w_tj * Y_perm[dest(t, j)]     (fp32 accumulate, j order)
+// One warp per token, 16-B vectors (8 bf16 per lane per step); HBM-bound.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace aep {
+
+namespace {
+__global__ void __launch_bounds__(256) combine_kernel(const bf16* __restrict__ yperm,
+                                                      const int32_t* __restrict__ dest,
+                                                      const float* __restrict__ w, const bf16* residual,
+                                                      bf16* y, int64_t T, int H, int k) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  int32_t d[kMaxTopK];
+  float wj[kMaxTopK];
+#pragma unroll
+  for (int j = 0; j < kMaxTopK; ++j) {
+    d[j] = (j < k) ? dest[t * k + j] : 0;
+    wj[j] = (j < k) ? w[t * k + j] : 0.f;
+  }
+  const int nv = H / 8;
+#pragma unroll 2
+  for (int v = lane; v < nv; v += 32) {
+    float acc[8];
+    if (residual) {
+      const uint4 r = reinterpret_cast<const uint4*>(residual + t * H)[v];
+      const uint32_t u[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { acc[2 * q] = bf16_lo(u[q]); acc[2 * q + 1] = bf16_hi(u[q]); }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    }
+    uint4 vals[kMaxTopK];
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j)
+      if (j < k)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(vals[j].x), "=r"(vals[j].y), "=r"(vals[j].z), "=r"(vals[j].w)
+                     : "l"(reinterpret_cast<const uint4*>(yperm + (int64_t)d[j] * H) + v));
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) {
+      if (j < k) {
+        const uint32_t u[4] = {vals[j].x, vals[j].y, vals[j].z, vals[j].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = fmaf(wj[j], bf16_lo(u[q]), acc[2 * q]);
+          acc[2 * q + 1] = fmaf(wj[j], bf16_hi(u[q]), acc[2 * q + 1]);
+        }
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16x2(acc[0], acc[1]);
+    o.y = pack_bf16x2(acc[2], acc[3]);
+    o.z = pack_bf16x2(acc[4], acc[5]);
+    o.w = pack_bf16x2(acc[6], acc[7]);
+    reinterpret_cast<uint4*>(y + t * H)[v] = o;
+  }
+}
+}  // namespace
+
+void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
+                    int64_t T, int H, int k, cudaStream_t s) {
+  if (T <= 0) return;
+  const unsigned grid = (unsigned)((T + 7) / 8);
+  combine_kernel<<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
+}
+
+}  // namespace aep

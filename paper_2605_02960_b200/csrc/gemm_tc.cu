@@ -1,0 +1,313 @@
+// gemm_tc.cu -- step (3): the grouped expert GEMM on 5th-gen tensor cores (sm_100a).
+//
+//   GEMM1 (per expert e, rows R_e of X_perm):  G = X_perm[R_e] . W_gu[e]^T  -> SwiGLU epilogue
+//          act = bf16( silu(G_gate) * G_up )                     (R4, R5)
+//   GEMM2:  Y_perm[R_e] = bf16( act[R_e] . W_down[e]^T )
+//
+// Persistent, warp-specialised CTA (one per SM, 256 threads):
+//   warp 0      TMA producer: A tile {64 x 128 rows} (2-D map over X_perm / act) and
+//               B tile {64 x BN rows x 1 expert} (3-D map over the packed layer) into a
+//               4-stage shared-memory ring (128-B swizzle), mbarrier full/empty pairs.
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (M=128, N=BN, K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit
+//               frees the smem stage / publishes the accumulator.
+//   warp 2      TMEM allocator (512 columns = 2 accumulators x 256).
+//   warps 4-7   epilogue: tcgen05.ld 32x32b (thread = accumulator row), SwiGLU or plain
+//               bf16 pack, masked 16-B stores of rows that belong to the expert.
+// Tiles: t -> (m-tile, n-tile), m-tile -> expert via the device-side prefix tile_start
+// (built by the permute scan), so the host never learns the per-expert counts.  Every
+// output tile is produced by exactly one CTA with a fixed K order: results are
+// bitwise-deterministic and independent of the grid size.
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace aep {
+
+namespace {
+constexpr int BM = kTileM;          // 128 rows per tile (UMMA M)
+constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
+constexpr int STAGES = 4;
+constexpr int NTHREADS = 256;
+constexpr int A_BYTES = BM * BK * 2;           // 16 KB
+constexpr int B_BYTES_MAX = 256 * BK * 2;      // 32 KB
+constexpr int TMEM_COLS = 512;
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 256 +
+                              2 * (kMaxExperts + 1) * sizeof(int32_t);
+
+struct TcArgs {
+  const int32_t* offsets;
+  const int32_t* tile_start;
+  int E;
+  int K;        // contraction length (multiple of 64)
+  int BN;       // N tile = rows of B per tile (multiple of 16, <= 256)
+  int n_tiles;  // N tiles per m-tile
+  int swiglu;   // 1: GEMM1 SwiGLU epilogue; 0: plain store
+  int n_out;    // output columns = output row stride
+  bf16* out;
+};
+
+__device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
+  int lo = 0, hi = E - 1;  // largest e with ts[e] <= mt (skips empty experts)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ts[mid] <= mt) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                   const TcArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES_MAX);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int32_t* s_ts = reinterpret_cast<int32_t*>(smem + STAGES * (A_BYTES + B_BYTES_MAX) + 256);
+  int32_t* s_off = s_ts + (kMaxExperts + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  for (int i = threadIdx.x; i <= p.E; i += NTHREADS) {
+    s_ts[i] = p.tile_start[i];
+    s_off[i] = p.offsets[i];
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = s_ts[p.E] * p.n_tiles;
+  const int nkb = p.K / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_b = policy_evict_last();
+      const uint32_t tx = (uint32_t)A_BYTES + (uint32_t)p.BN * BK * 2;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        const int e = find_expert(s_ts, p.E, mt);
+        const int row0 = s_off[e] + (mt - s_ts[e]) * BM;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], tx);
+          tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
+          tma_load_3d(sB + stage * B_BYTES_MAX, &map_b, &full[stage], kb * BK, nt * p.BN, e, pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(BM, p.BN, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * 256);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * B_BYTES_MAX);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            mma_bf16(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
+                     (kb | k) != 0 ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+      const int e = find_expert(s_ts, p.E, mt);
+      const int row = s_off[e] + (mt - s_ts[e]) * BM + ew * 32 + lane;
+      const bool valid = row < s_off[e + 1];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
+      if (p.swiglu) {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.n_out + nt * 128);
+#pragma unroll 1
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tb + c0, g);
+          tmem_ld32(tb + 128 + c0, u);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float a0 = silu_f(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
+              const float a1 = silu_f(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
+              o[i] = pack_bf16x2(a0, a1);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[c0 / 8 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          }
+        }
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.n_out + nt * p.BN);
+#pragma unroll 1
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          if (nt * p.BN + c0 >= p.n_out) break;
+          uint32_t r[32];
+          tmem_ld32(tb + c0, r);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              dst[c0 / 8 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+void launch_tc(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, int K, int BN, int n_tiles,
+               int swiglu, int n_out, bf16* out, int num_sms, cudaStream_t s) {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+  });
+  TcArgs a{g.offsets, g.tile_start, g.E, K, BN, n_tiles, swiglu, n_out, out};
+  const int upper = g.max_m_tiles * n_tiles;
+  const int grid = upper < num_sms ? (upper > 0 ? upper : 1) : num_sms;
+  gemm_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(ma, mb, a);
+}
+}  // namespace
+
+int gemm2_bn(int H) { return H >= 256 ? 256 : H; }
+
+bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h) {
+  const uint32_t box[2] = {BK, BM};
+  {
+    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)R_max};
+    const uint64_t strides[1] = {(uint64_t)H * 2};
+    if (!encode_tmap(&m.xperm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xperm, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)h, (uint64_t)R_max};
+    const uint64_t strides[1] = {(uint64_t)h * 2};
+    if (!encode_tmap(&m.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  m.bn2 = gemm2_bn(H);
+  return true;
+}
+
+bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2) {
+  {
+    const uint64_t dims[3] = {(uint64_t)H, (uint64_t)(2 * h), (uint64_t)E};
+    const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)expert_bytes};
+    const uint32_t box[3] = {BK, 256, 1};
+    if (!encode_tmap(&m.wgu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, layer, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  {
+    const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * 2;
+    const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};
+    const uint64_t strides[2] = {(uint64_t)h * 2, (uint64_t)expert_bytes};
+    const uint32_t box[3] = {BK, (uint32_t)bn2, 1};
+    if (!encode_tmap(&m.wd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wd, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  return true;
+}
+
+void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
+                     int num_sms, cudaStream_t s) {
+  // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
+  launch_tc(g, am.xperm, wm.wgu, H, 256, (2 * h) / 256, 1, h, act, num_sms, s);
+}
+
+void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
+                     int num_sms, cudaStream_t s) {
+  const int bn = am.bn2;
+  launch_tc(g, am.act, wm.wd, h, bn, (H + bn - 1) / bn, 0, H, yperm, num_sms, s);
+}
+
+// ------------------------------------------------------------------ tensor-map encoding
+bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const void* base, const uint64_t* dims,
+                 const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  typedef CUresult (*encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static encode_fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<encode_fn>(p);
+  });
+  if (!fn) return false;
+  cuuint64_t d[5];
+  cuuint64_t st[4];
+  cuuint32_t b[5], es[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    es[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  const CUresult r = fn(map, dtype, (cuuint32_t)rank, const_cast<void*>(base), d, st, b, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace aep

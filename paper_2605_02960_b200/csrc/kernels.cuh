@@ -1,0 +1,84 @@
+// kernels.cuh -- internal launcher interface between the C ABI (asyncep.cu) and the
+// kernels.  Not part of the public ABI.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace aep {
+
+typedef __nv_bfloat16 bf16;
+
+constexpr int kPermTokensPerBlock = 64;  // permute/dispatch granularity (tokens per CTA)
+constexpr int kTileM = 128;              // grouped-GEMM M tile (rows of one expert)
+constexpr int kMaxExperts = 256;
+constexpr int kMaxTopK = 16;
+
+// Step (1): router GEMM (fp32 logits) + softmax + top-k, CUDA cores.
+// x [T,H] bf16, wr [E,H] bf16 -> ids [T,k] int32, w [T,k] fp32.
+void launch_router_simt(const bf16* x, const bf16* wr, int64_t T, int H, int E, int k, int norm_topk,
+                        int32_t* ids, float* w, cudaStream_t s);
+
+// Step (1) on tensor cores: tcgen05 logits tile (128 tokens x E) + top-k epilogue.
+struct RouterTc {
+  CUtensorMap map_x;  // [T_max, H] bf16, box {64, 128}, SW128
+  CUtensorMap map_wr; // [E, H] bf16, box {64, E_pad}
+  int E_pad;          // E rounded up to a multiple of 16 (MMA N)
+};
+bool make_router_maps(RouterTc& rt, const bf16* x, int64_t T_max, const bf16* wr, int H, int E);
+void launch_router_tc(const RouterTc& rt, int64_t T, int H, int E, int k, int norm_topk, int32_t* ids,
+                      float* w, int num_sms, cudaStream_t s);
+
+// Step (2): permute / dispatch.
+void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s);
+void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
+                      int32_t* counts, cudaStream_t s);
+void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, int64_t T, int H,
+                         int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm, cudaStream_t s);
+
+// Step (3): grouped expert GEMM.  Weights come from a packed layer (see asyncep.h):
+// per expert blob of expert_bytes; W_gu at blob offset 0 ([2h, H]), W_down at 2h*H*2.
+struct GroupedArgs {
+  const int32_t* offsets;    // [E+1] rows of each expert in X_perm
+  const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kTileM)
+  int E;
+  int max_m_tiles;           // host upper bound on tile_start[E]
+};
+// CUDA-core reference path (debug / sanitizer): SwiGLU GEMM1 and plain GEMM2.
+void launch_gemm1_simt(const GroupedArgs& g, const bf16* xperm, const uint8_t* layer, size_t expert_bytes,
+                       int H, int h, bf16* act, cudaStream_t s);
+void launch_gemm2_simt(const GroupedArgs& g, const bf16* act, const uint8_t* layer, size_t expert_bytes,
+                       int H, int h, bf16* yperm, cudaStream_t s);
+
+// tcgen05 path.  One set of TMA maps per weight source (resident layer or slot).
+struct GemmMaps {
+  CUtensorMap wgu;   // 3D {H, 2h, E} bf16, box {64, 256, 1}
+  CUtensorMap wd;    // 3D {h, H, E} bf16, box {64, BN2, 1}
+};
+struct ActMaps {
+  CUtensorMap xperm; // 2D {H, R_max}, box {64, 128}
+  CUtensorMap act;   // 2D {h, R_max}, box {64, 128}
+  int bn2;           // GEMM2 N tile
+};
+bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2);
+bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h);
+int gemm2_bn(int H);
+void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
+                     int num_sms, cudaStream_t s);
+void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
+                     int num_sms, cudaStream_t s);
+
+// Step (4): weighted combine (+ residual).
+void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
+                    int64_t T, int H, int k, cudaStream_t s);
+
+// Weight packing (natural layout -> packed expert blobs), BF16.
+void launch_pack_bf16(const bf16* gate, const bf16* up, const bf16* down, int count, int H, int h,
+                      size_t expert_bytes, uint8_t* out, cudaStream_t s);
+
+// Driver entry point for cuTensorMapEncodeTiled (resolved once through the runtime).
+bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const void* base, const uint64_t* dims,
+                 const uint64_t* strides_bytes /* rank-1 entries */, const uint32_t* box, CUtensorMapSwizzle sw);
+
+}  // namespace aep

@@ -1,0 +1,44 @@
+// pack.cu -- natural-layout expert weights -> packed expert blobs (layout in asyncep.h):
+//   W_gu [2h, H]: rows [256b, 256b+128) = gate rows [128b, 128b+128),
+//                 rows [256b+128, 256b+256) = up rows [128b, 128b+128);
+//   W_down [H, h] as given.   One CTA per (expert, packed row); 16-B vector copies.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace aep {
+
+namespace {
+__global__ void pack_bf16_kernel(const bf16* __restrict__ gate, const bf16* __restrict__ up,
+                                 const bf16* __restrict__ down, int H, int h, size_t expert_bytes,
+                                 uint8_t* __restrict__ out) {
+  const int e = blockIdx.y;
+  const int r = blockIdx.x;  // 0 .. 2h + H - 1
+  uint8_t* blob = out + (size_t)e * expert_bytes;
+  const uint4* src;
+  uint4* dst;
+  int nv;
+  if (r < 2 * h) {
+    const int b = r / 256, q = r % 256;
+    const int srow = b * 128 + (q % 128);
+    const bf16* m = (q < 128) ? gate : up;
+    src = reinterpret_cast<const uint4*>(m + ((size_t)e * h + srow) * H);
+    dst = reinterpret_cast<uint4*>(blob + (size_t)r * H * 2);
+    nv = H / 8;
+  } else {
+    const int rr = r - 2 * h;
+    src = reinterpret_cast<const uint4*>(down + ((size_t)e * H + rr) * h);
+    dst = reinterpret_cast<uint4*>(blob + (size_t)2 * h * H * 2 + (size_t)rr * h * 2);
+    nv = h / 8;
+  }
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) dst[v] = src[v];
+}
+}  // namespace
+
+void launch_pack_bf16(const bf16* gate, const bf16* up, const bf16* down, int count, int H, int h,
+                      size_t expert_bytes, uint8_t* out, cudaStream_t s) {
+  if (count <= 0) return;
+  dim3 grid(2 * h + H, count);
+  pack_bf16_kernel<<<grid, 128, 0, s>>>(gate, up, down, H, h, expert_bytes, out);
+}
+
+}  // namespace aep

@@ -1,0 +1,146 @@
+// permute.cu -- step (2): local permute / dispatch ("all top-k dispatch
+// is local"; "auxiliary kernels (reshaping, token permutation/alignment)").
+//
+//   hist    : per-CTA (64-token chunk) expert histogram          -> blk_counts[nblk][E]
+//   scan    : per-expert exclusive scan over chunks + over experts -> row base of every
+//             (chunk, expert), offsets[E+1], GEMM m-tile prefix tile_start[E+1], counts[E]
+//   scatter : stable rank of every (t, j) inside its expert in (t, j) order (warp
+//             __match_any_sync + popc), then one warp per token copies x_t (16-B vectors)
+//             to its k destination rows of X_perm.
+// Pure integer work + data movement: the result is bit-exact and deterministic.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace aep {
+
+namespace {
+
+__global__ void perm_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E,
+                                 int32_t* __restrict__ blk_counts) {
+  extern __shared__ int32_t hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int64_t t0 = (int64_t)blockIdx.x * kPermTokensPerBlock;
+  const int64_t tn = min((int64_t)kPermTokensPerBlock, T - t0);
+  const int n = (int)tn * k;
+  const int32_t* p = ids + t0 * k;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[p[i]], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) blk_counts[(int64_t)blockIdx.x * E + e] = hist[e];
+}
+
+// One CTA, one thread per expert.
+__global__ void perm_scan_kernel(int32_t* __restrict__ bc, int nblk, int E, int32_t* __restrict__ offsets,
+                                 int32_t* __restrict__ tile_start, int32_t* __restrict__ counts) {
+  __shared__ int32_t tot[kMaxExperts];
+  __shared__ int32_t off[kMaxExperts + 1];
+  const int e = threadIdx.x;
+  if (e < E) {
+    int32_t run = 0;
+#pragma unroll 8
+    for (int b = 0; b < nblk; ++b) {
+      const int32_t c = bc[(int64_t)b * E + e];
+      bc[(int64_t)b * E + e] = run;
+      run += c;
+    }
+    tot[e] = run;
+    if (counts) counts[e] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t o = 0, ts = 0;
+    for (int i = 0; i < E; ++i) {
+      off[i] = o;
+      offsets[i] = o;
+      tile_start[i] = ts;
+      o += tot[i];
+      ts += (tot[i] + kTileM - 1) / kTileM;
+    }
+    off[E] = o;
+    offsets[E] = o;
+    tile_start[E] = ts;
+  }
+  __syncthreads();
+  if (e < E) {
+    const int32_t base = off[e];
+#pragma unroll 8
+    for (int b = 0; b < nblk; ++b) bc[(int64_t)b * E + e] += base;
+  }
+}
+
+__global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restrict__ x,
+                                                           const int32_t* __restrict__ ids,
+                                                           const int32_t* __restrict__ blk_base, int64_t T,
+                                                           int H, int k, int E, int32_t* __restrict__ dest,
+                                                           int32_t* __restrict__ src_tok,
+                                                           bf16* __restrict__ xperm) {
+  __shared__ int32_t cnt[kMaxExperts];
+  __shared__ int32_t dst[kPermTokensPerBlock * kMaxTopK];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kPermTokensPerBlock;
+  const int tn = (int)min((int64_t)kPermTokensPerBlock, T - t0);
+  const int n = tn * k;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  if (warp == 0) {
+    // entries in (t, j) order, 32 at a time; stable rank inside each expert
+    const int32_t* bb = blk_base + (int64_t)blockIdx.x * E;
+    for (int c = 0; c < n; c += 32) {
+      const int i = c + lane;
+      const bool valid = i < n;
+      const int e = valid ? ids[t0 * k + i] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const unsigned lt = (1u << lane) - 1u;
+      const int rank = __popc(peers & lt);
+      int d = 0;
+      if (valid) d = bb[e] + cnt[e] + rank;
+      __syncwarp();
+      if (valid && (peers & lt) == 0) cnt[e] += __popc(peers);
+      __syncwarp();
+      if (valid) {
+        dst[i] = d;
+        dest[t0 * k + i] = d;
+        src_tok[d] = (int32_t)(t0 + i / k);
+      }
+    }
+  }
+  __syncthreads();
+  // copy: one warp per token, 16-B vectors, each x row read once and written k times
+  for (int tl = warp; tl < tn; tl += blockDim.x / 32) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + (t0 + tl) * (int64_t)H);
+    const int nv = H / 8;
+    int32_t d[kMaxTopK];
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j) d[j] = (j < k) ? dst[tl * k + j] : 0;
+#pragma unroll 4
+    for (int v = lane; v < nv; v += 32) {
+      uint4 val;
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                   : "l"(src + v));
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j)
+        if (j < k) reinterpret_cast<uint4*>(xperm + (int64_t)d[j] * H)[v] = val;
+    }
+  }
+}
+}  // namespace
+
+void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s) {
+  const int nblk = (int)((T + kPermTokensPerBlock - 1) / kPermTokensPerBlock);
+  perm_hist_kernel<<<nblk, 256, sizeof(int32_t) * E, s>>>(ids, T, k, E, blk_counts);
+}
+
+void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
+                      int32_t* counts, cudaStream_t s) {
+  const int threads = ((E + 31) / 32) * 32;
+  perm_scan_kernel<<<1, threads, 0, s>>>(blk_counts, nblk, E, offsets, tile_start, counts);
+}
+
+void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, int64_t T, int H, int k,
+                         int E, int32_t* dest, int32_t* src_tok, bf16* xperm, cudaStream_t s) {
+  const int nblk = (int)((T + kPermTokensPerBlock - 1) / kPermTokensPerBlock);
+  perm_scatter_kernel<<<nblk, 256, 0, s>>>(x, ids, blk_base, T, H, k, E, dest, src_tok, xperm);
+}
+
+}  // namespace aep

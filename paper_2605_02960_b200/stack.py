@@ -1,0 +1,93 @@
+"""Host-side driver for an L-layer AsyncEP MoE stack on one GPU (one rank).
+
+Allocates (with torch) the replicated router weights, this rank's packed expert shards
+(layer 0 fully replicated), the two gather slots and the workspace, creates
+the library context, and runs the per-layer schedule of the "MoE gatherer"
+(PAPER.md:630): issue the AllGather of layer l+1, then compute layer l.
+
+Weights are supplied by callables so this module holds no generator:
+  router_fn(l)             -> [E, H] bf16 tensor
+  expert_fn(l, experts)    -> (gate [n,h,H], up [n,h,H], down [n,H,h]) bf16 tensors
+"""
+from __future__ import annotations
+
+import torch
+
+from . import asyncep as A
+
+
+class MoEStack:
+    def __init__(self, L, E, k, H, h, max_tokens, router_fn, expert_fn, *, world_size=1, rank=0,
+                 replicate_layer0=True, norm_topk=True, flags=0, gamma=1.2, device="cuda",
+                 nccl_comm=None, compute_stream=None, comm_stream=None, pack_chunk=8):
+        self.device = torch.device(device)
+        self.cfg = A.make_config(L, E, k, H, h, world_size=world_size, rank=rank,
+                                 replicate_layer0=int(replicate_layer0), norm_topk=int(norm_topk),
+                                 max_tokens=max_tokens, gamma=gamma, flags=flags)
+        self.L, self.E, self.k, self.H, self.h = L, E, k, H, h
+        self.N, self.rank = world_size, rank
+        self.compute_stream = compute_stream or torch.cuda.current_stream(self.device)
+        self.comm_stream = comm_stream if comm_stream is not None else (
+            torch.cuda.Stream(self.device) if world_size > 1 else None)
+        ebytes = A.asyncep_expert_bytes(self.cfg)
+        self.expert_bytes = ebytes
+        self.router_w = [router_fn(l).to(self.device, torch.bfloat16).contiguous() for l in range(L)]
+        self.shards = []
+        per = E // world_size
+        for l in range(L):
+            full = world_size == 1 or (l == 0 and replicate_layer0)
+            ex = range(E) if full else range(rank * per, (rank + 1) * per)
+            buf = torch.empty(len(ex) * ebytes, dtype=torch.uint8, device=self.device)
+            for c0 in range(0, len(ex), pack_chunk):
+                sub = ex[c0:c0 + pack_chunk]
+                g, u, d = expert_fn(l, sub)
+                g, u, d = (t.to(self.device, torch.bfloat16).contiguous() for t in (g, u, d))
+                A.asyncep_pack_experts(self.cfg, g, u, d, buf[c0 * ebytes:(c0 + len(sub)) * ebytes],
+                                       stream=torch.cuda.current_stream(self.device))
+                del g, u, d
+            self.shards.append(buf)
+        if world_size > 1:
+            sb = A.asyncep_slot_bytes(self.cfg)
+            self.slots = [torch.empty(sb, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        else:
+            self.slots = [None, None]
+        self.workspace = torch.empty(A.asyncep_workspace_size(self.cfg), dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        self.ctx = A.asyncep_init(self.cfg, nccl_comm, self.compute_stream, self.comm_stream, self.router_w,
+                                  self.shards, self.slots[0], self.slots[1], self.workspace)
+        self._bufs = None
+
+    def layer_resident(self, l: int) -> bool:
+        return self.N == 1 or (l == 0 and bool(self.cfg.replicate_layer0))
+
+    def prefetch(self, l: int, local_shards=None) -> None:
+        if local_shards is not None:
+            if not self.layer_resident(l):
+                A.asyncep_prefetch_layer_local(self.ctx, l, local_shards(l))
+        else:
+            A.asyncep_prefetch_layer(self.ctx, l)
+
+    def forward(self, l, x, residual=None, y=None, ids=None, w=None, counts=None):
+        return A.asyncep_moe_forward(self.ctx, l, x, residual=residual, y=y, topk_ids_out=ids,
+                                     topk_w_out=w, expert_counts_out=counts)
+
+    def run(self, x, residual=True, out=None, local_shards=None, record=None):
+        """One pass of the whole stack: x_{l+1} = x_l + MoE_l(x_l) (reading R9).
+        Returns the final activations (a ping-pong buffer unless ``out`` is given).
+        ``record(l, x_l)`` (optional) sees each layer's input before it runs."""
+        T = x.shape[0]
+        if self._bufs is None or self._bufs[0].shape[0] < T:
+            self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
+                          for _ in range(2)]
+        cur = x
+        if not self.layer_resident(0):
+            self.prefetch(0, local_shards)
+        for l in range(self.L):
+            if l + 1 < self.L:
+                self.prefetch(l + 1, local_shards)  # gather of layer l+1 overlaps layer l
+            if record is not None:
+                record(l, cur)
+            dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
+            self.forward(l, cur, residual=cur if residual else None, y=dst)
+            cur = dst
+        return cur

@@ -1,0 +1,39 @@
+"""Shared builders for the GPU tests: seeded synthetic stacks (synth) run through the
+library (paper_2605_02960_b200), plus host copies of the same weights for the oracle."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import synth
+
+
+def f32(t) -> np.ndarray:
+    return t.detach().to("cpu", torch.float32).numpy()
+
+
+class Workload:
+    """Natural-layout weights of an L-layer stack, generated on demand on any device."""
+
+    def __init__(self, L, E, k, H, h, seed=0, zipf_s=0.0):
+        self.L, self.E, self.k, self.H, self.h, self.seed, self.zipf_s = L, E, k, H, h, seed, zipf_s
+
+    def router(self, l, device="cuda"):
+        return synth.router_weight(self.E, self.H, self.seed, l, device=device, zipf_s=self.zipf_s)
+
+    def experts(self, l, experts=None, device="cuda"):
+        return synth.expert_weights(self.E, self.H, self.h, self.seed, l, device=device, experts=experts)
+
+    def tokens(self, T, device="cuda"):
+        return synth.tokens(T, self.H, self.seed, device=device, zipf_s=self.zipf_s)
+
+    def host_layer(self, l):
+        """fp32 numpy copies for the oracle (drawn on the GPU: synth is bit-identical)."""
+        wr = f32(self.router(l))
+        g, u, d = self.experts(l)
+        return wr, f32(g), f32(u), f32(d)
+
+    def stack(self, max_tokens, **kw):
+        from paper_2605_02960_b200.stack import MoEStack
+        return MoEStack(self.L, self.E, self.k, self.H, self.h, max_tokens,
+                        lambda l: self.router(l), lambda l, ex: self.experts(l, ex), **kw)

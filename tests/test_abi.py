@@ -1,0 +1,80 @@
+"""CPU-side checks of the C-ABI boundary: the library builds for sm_100a, loads without a
+GPU, exports every symbol include/asyncep.h declares, and its pure host functions
+(sizes, config validation, Eq. 1) agree with the oracle.  No device compute here."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def A():
+    from paper_2605_02960_b200 import build
+    build.build()
+    from paper_2605_02960_b200 import asyncep
+    return asyncep
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "asyncep.h")).read()
+    return sorted(set(re.findall(r"ASYNCEP_API\s+[\w\s\*]+?\b(asyncep_\w+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = declared_symbols()
+    for required in ("asyncep_init", "asyncep_prefetch_layer", "asyncep_moe_forward", "asyncep_saturation_T"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(A):
+    lib = ctypes.CDLL(A.LIB_PATH)
+    for name in declared_symbols():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", A.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (asyncep_\w+)", out))
+    assert set(declared_symbols()) <= exported
+    assert A.asyncep_abi_version() == 1
+
+
+def test_library_is_sm100a_code(A):
+    out = subprocess.run(["cuobjdump", "--list-elf", A.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    sass = subprocess.run(["cuobjdump", "-sass", A.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCQMMA" in sass, "no tcgen05 MMA in the binary"
+    assert "UTMALDG" in sass, "no TMA loads in the binary"
+    assert "LDTM" in sass, "no TMEM loads in the binary"
+
+
+def test_sizes_and_config_validation(A):
+    cfg = A.make_config(8, 128, 8, 4096, 1536, world_size=8, max_tokens=32768)
+    assert A.asyncep_expert_bytes(cfg) == 3 * 4096 * 1536 * 2
+    assert A.asyncep_slot_bytes(cfg) == 4_831_838_208  # SURVEY.md appendix (BF16 layer)
+    assert A.asyncep_shard_bytes(cfg) == 4_831_838_208 // 8
+    assert A.asyncep_workspace_size(cfg) > 32768 * 8 * (4096 + 1536) * 2
+    bad = [dict(num_experts=100, world_size=8),  # E % N != 0
+           dict(hidden=4000), dict(ffn=1000), dict(top_k=0), dict(top_k=17), dict(gamma=0.5),
+           dict(max_tokens=0)]
+    for b in bad:
+        kw = dict(num_layers=8, num_experts=128, top_k=8, hidden=4096, ffn=1536, world_size=8, max_tokens=1024)
+        kw.update(b)
+        c = A.make_config(kw.pop("num_layers"), kw.pop("num_experts"), kw.pop("top_k"), kw.pop("hidden"),
+                          kw.pop("ffn"), **kw)
+        with pytest.raises(A.AsyncEPError):
+            A.asyncep_workspace_size(c)
+
+
+@pytest.mark.parametrize("N", [1, 2, 4, 8])
+@pytest.mark.parametrize("dtype,b,F", [(0, 2, 1.42e15), (1, 1, 2.84e15)])
+def test_saturation_T_matches_oracle(A, N, dtype, b, F):
+    cfg = A.make_config(8, 128, 8, 4096, 1536, expert_dtype=dtype, world_size=N, max_tokens=1, gamma=1.2)
+    t, f = A.asyncep_saturation_T(cfg, F, 7.5e11)
+    t0, f0 = oracle.saturation_T(128, 8, 4096, 1536, b, N, float(ctypes.c_float(1.2).value), F, 7.5e11)
+    assert t == pytest.approx(t0, rel=1e-12) and f == pytest.approx(f0, rel=1e-12)
+    if N == 1:
+        assert t == 0.0
