@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: AsyncEP MoE-layer stack forward on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the metric's config): Qwen3-235B-A22B MoE-layer
+shape -- E=128 experts, top-8, H=4096, expert FFN h=1536 -- BF16, an 8-layer stack with
+residual chaining (reading R9), 32,768 tokens per GPU (weak scaling: per-GPU work fixed).
+One "step" = one pass of the whole hot path (router -> permute -> grouped GEMM with
+SwiGLU -> combine) through all 8 layers over one batch of synthetic tokens.
+
+  N = 1  : all layers resident (world_size 1, no gather).
+  N > 1  : one process per GPU (torchrun), experts of layers >= 1 sharded 1/N by expert
+           index, layer 0 replicated, NCCL AllGather of layer l+1 on a side stream while
+           layer l computes.  No data-path collective.
+
+Timing: W warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
+events on the compute stream, max over ranks.  Inputs are larger than L2 (38.7 GB of
+weights, 268 MB of activations per layer), so no explicit L2 flush.
+
+--impl reference: the CPU oracle (oracle/, plain fp64 C) on the host cores, on a bounded
+sample of the same workload (see cpu_baseline.sample in the JSON line).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "tokens/s and MFU per B200, Qwen3-235B MoE layers, 1/2/4/8 GPUs; exposed AG time"
+L_, E_, K_, H_, h_ = 8, 128, 8, 4096, 1536
+T_LOC = 32768
+FLOPS_TOK_LAYER = 2 * H_ * E_ + 6 * K_ * H_ * h_          # 303,038,464 (router + experts)
+GEMM1_FLOPS_TOK = 4 * K_ * H_ * h_                        # gate/up: 2 * k * H * 2h
+GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
+SPEC_BF16 = 2.25e15
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, dev_index: int, period=0.1):
+        self.dev_index, self.period = dev_index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            names = {
+                "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+                "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+                "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for n, b in names.items():
+                            if r & b and n != "gpu_idle":
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._t = None
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=2)
+        s = sorted(self.samples)
+        med = s[len(s) // 2] if s else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(s)}
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    import glob
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "gemm1_ncu_full.json")))
+    if not cands:
+        return None
+    try:
+        d = json.load(open(cands[-1]))
+        d = d[0] if isinstance(d, list) else d
+        return {"bytes_per_launch": d.get("dram_bytes_per_launch"),
+                "source": os.path.relpath(cands[-1], ROOT)}
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ oracle arm
+class OracleSample:
+    """The CPU oracle on a bounded sample of the workload: n_tokens through one of the
+    Qwen3-235B-shape layers (the per-layer cost is identical for every layer)."""
+
+    def __init__(self, layer: int = 0, seed: int = 0):
+        import torch
+
+        import oracle
+        import synth
+        dev = "cuda" if torch.cuda.is_available() else "cpu"  # synth is bit-identical on both
+        self.dev, self.seed = dev, seed
+        self.wr = synth.router_weight(E_, H_, seed, layer, device=dev).float().cpu().numpy()
+        g, u, d = synth.expert_weights(E_, H_, h_, seed, layer, device=dev)
+        self.g, self.u, self.d = (t.float().cpu().numpy() for t in (g, u, d))
+        del g, u, d
+        oracle.build()
+        self.threads = oracle.num_threads()
+
+    def run(self, n_tokens: int, sample: int = 0):
+        import oracle
+        import synth
+        x = synth.tokens(n_tokens, H_, self.seed + 1000 + sample, device=self.dev).float().cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.moe_layer(x, self.wr, self.g, self.u, self.d, K_)
+        dt = time.perf_counter() - t0
+        desc = (f"{n_tokens} tokens through 1 of the {L_} Qwen3-235B-shape layers (fp64 C oracle, "
+                f"{self.threads} threads); stack tokens/s = layer tokens/s / {L_}")
+        return n_tokens / dt / L_, dt, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n_tok = int(os.environ.get("ASYNCEP_REF_TOKENS", "256"))
+    orc = OracleSample()
+    vals = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        v, dt, desc = orc.run(n_tok, sample=i)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    dt_tot = sum(b for _, b in vals)
+    v = n_tok * len(vals) / dt_tot / L_
+    ms = dt_tot / len(vals) * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "qwen3-235b-a22b moe-layer stack (E=128,k=8,H=4096,h=1536), 8 layers, "
+                               f"bounded sample of {n_tok} tokens per step",
+                   "tokens_per_gpu": T_LOC, "layers": L_},
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": orc.threads, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tokens", type=int, default=T_LOC, help="tokens per GPU")
+    ap.add_argument("--layers", type=int, default=L_)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import synth
+    from paper_2605_02960_b200 import asyncep as A
+    from paper_2605_02960_b200.stack import MoEStack
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.all_reduce(torch.ones(1, device=dev))  # eager comm init
+        comm = A.nccl_comm_ptr()
+    L, T = args.layers, args.tokens
+    seed = 0
+    flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0)
+    stack = MoEStack(L, E_, K_, H_, h_, T,
+                     lambda l: synth.router_weight(E_, H_, seed, l, device=dev),
+                     lambda l, ex: synth.expert_weights(E_, H_, h_, seed, l, device=dev, experts=ex),
+                     world_size=world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
+                     nccl_comm=comm)
+    # tokens: DP -- every rank its own batch
+    x = synth.tokens(T, H_, seed + 17 + rank, device=dev)
+    out = torch.empty_like(x)
+    cs = stack.compute_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        stack.run(x, out=out)
+    barrier()
+    A.asyncep_reset_stage_times(stack.ctx)
+    launches0 = A.asyncep_kernel_launches(stack.ctx)
+    clocks = ClockSampler(local).start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(cs)
+    for _ in range(args.steps):
+        stack.run(x, out=out)
+    e1.record(cs)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = A.asyncep_kernel_launches(stack.ctx) - launches0
+    stages, nfwd = A.asyncep_stage_times(stack.ctx)
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = t.item()
+    ms_step = ms_max / args.steps
+    value = world * T * args.steps / (ms_max / 1e3)     # whole-job tokens/s
+    per_gpu = value / world
+    mfu_flops = per_gpu * L * FLOPS_TOK_LAYER
+
+    # ---------------- e2e: public API with host buffers (pinned), copies in the timed region
+    xh = x.cpu().pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xd = torch.empty_like(x)
+    for _ in range(1):
+        xd.copy_(xh, non_blocking=True)
+        stack.run(xd, out=out)
+        yh.copy_(out, non_blocking=True)
+    barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(cs)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        stack.run(xd, out=out)
+        yh.copy_(out, non_blocking=True)
+    f1.record(cs)
+    barrier()
+    t2 = torch.tensor([f0.elapsed_time(f1)], device=dev)
+    if world > 1:
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    e2e_value = world * T * args.steps / (t2.item() / 1e3)
+
+    peaks, peak_src = load_peaks()
+    # dominant kernel: GEMM1 (gate/up + SwiGLU), stage-timed with CUDA events on the
+    # compute stream around each launch inside the timed region
+    g1_ms = stages["gemm1_gateup_swiglu"] / max(nfwd, 1)
+    g1_flops = GEMM1_FLOPS_TOK * T
+    g1_tflops = g1_flops / (g1_ms / 1e3) / 1e12
+    peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = ncu_traffic()
+    per_layer_ms = {k: v / max(nfwd, 1) for k, v in stages.items()}
+    step_layer_ms = ms_step / L
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"qwen3-235b-a22b moe-layer stack, {L} layers, E=128 k=8 H=4096 h=1536, "
+                               f"{T} tokens/GPU, BF16, random-init weights",
+                   "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
+                   "parallelism": f"dp{world}+asyncep{world}" if world > 1 else "dp1 (all experts resident)",
+                   "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
+        "tokens_per_s_per_gpu": per_gpu,
+        "layer_tokens_per_s_per_gpu": per_gpu * L,
+        "mfu": {"vs_spec_2.25PF": mfu_flops / SPEC_BF16,
+                "vs_measured_sustained": mfu_flops / (peak_tf * 1e12),
+                "flops_per_token_layer": FLOPS_TOK_LAYER},
+        "stage_ms_per_layer": per_layer_ms,
+        "layer_ms": step_layer_ms,
+        "exposed_ag": {"ms_per_layer": per_layer_ms["gather_wait"],
+                       "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms else None,
+                       "note": "event gap before GEMM1 on gathered layers (0 when N=1)"},
+        "roofline": {"kernel": "grouped GEMM1 gate/up + SwiGLU (tcgen05)", "bound": "tensor",
+                     "achieved": g1_tflops, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": g1_tflops / peak_tf,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)",
+                     "algorithmic_flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
+                     "traffic": traffic},
+        "clocks": clk,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": xh.numel() * 2,
+                "d2h_bytes_per_step": yh.numel() * 2,
+                "note": "public API (MoEStack.run over the C ABI) with pinned host input/output copied each step"},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_tok = int(os.environ.get("ASYNCEP_CPU_TOKENS", "2048"))
+        del stack
+        torch.cuda.empty_cache()
+        orc = OracleSample()
+        v, dt, desc = orc.run(n_tok)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": orc.threads, "kind": "oracle",
+                                "sample": desc + f"; {dt:.1f} s of CPU work"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
