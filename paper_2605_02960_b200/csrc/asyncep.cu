@@ -60,12 +60,13 @@ constexpr int kNcclUint8 = 1;
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, xperm, act, total;
+  size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, xperm, act, total;
 };
 WsLayout ws_layout(const asyncep_config& c) {
   WsLayout L{};
   const size_t Tm = (size_t)c.max_tokens, k = (size_t)c.top_k, E = (size_t)c.num_experts;
   const size_t R = Tm * k;
+  const size_t Rp = (size_t)aep::perm_rows((int64_t)Tm, (int)k, (int)E);  // padded permuted rows
   const size_t nblk = (Tm + aep::kPermTokensPerBlock - 1) / aep::kPermTokensPerBlock;
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -76,13 +77,14 @@ WsLayout ws_layout(const asyncep_config& c) {
   L.ids = take(R * 4);
   L.w = take(R * 4);
   L.dest = take(R * 4);
-  L.src_tok = take(R * 4);
+  L.src_tok = take(Rp * 4);  // indexed by padded permuted row
   L.blk = take(nblk * E * 4);
   L.offsets = take((E + 1) * 4);
   L.tile_start = take((E + 1) * 4);
   L.counts = take(E * 4);
-  L.xperm = take(R * (size_t)c.hidden * 2);  // X_perm, reused as Y_perm after GEMM1
-  L.act = take(R * (size_t)c.ffn * 2);
+  L.done = take(4);
+  L.xperm = take(Rp * (size_t)c.hidden * 2);  // X_perm, reused as Y_perm after GEMM1
+  L.act = take(Rp * (size_t)c.ffn * 2);
   L.total = o;
   return L;
 }
@@ -137,6 +139,7 @@ struct asyncep_ctx {
   std::vector<aep::GemmMaps> layer_maps;  // per resident layer (index l), valid if resident[l]
   std::vector<char> resident;
   aep::GemmMaps slot_maps[2];
+  std::vector<aep::RouterTc> router_maps;  // per layer
   // stage timing
   std::vector<cudaEvent_t> ev_pool;
   int ev_used = 0;  // forwards recorded since the last flush
@@ -260,8 +263,10 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
         cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(ASYNCEP_ERR_CUDA, "cudaEventCreate failed"));
   }
+  if (cudaMemsetAsync(c->ws + c->L.done, 0, 4, c->cs) != cudaSuccess)
+    return bail(fail(ASYNCEP_ERR_CUDA, "cudaMemsetAsync failed"));
   // TMA descriptors: activations (fixed workspace addresses), each resident layer, both slots.
-  const int64_t R = (int64_t)cfg->max_tokens * cfg->top_k;
+  const int64_t R = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
   if (!aep::make_act_maps(c->act_maps, (const bf16*)(c->ws + c->L.xperm), (const bf16*)(c->ws + c->L.act), R,
                           cfg->hidden, cfg->ffn))
     return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
@@ -274,6 +279,10 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
                                cfg->ffn, c->act_maps.bn2))
       return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l));
   }
+  c->router_maps.resize(L);
+  for (int l = 0; l < L; ++l)
+    if (!aep::make_router_wmap(c->router_maps[l], (const bf16*)c->router_w[l], cfg->hidden, cfg->num_experts))
+      return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router %d)", l));
   for (int i = 0; i < 2; ++i)
     if (c->slot[i] && !aep::make_weight_maps(c->slot_maps[i], c->slot[i], c->expert_bytes, cfg->num_experts,
                                              cfg->hidden, cfg->ffn, c->act_maps.bn2))
@@ -369,13 +378,17 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     CUDA_TRY(cudaEventRecord(ev[0], st));
   }
   // (1) router GEMM + softmax + top-k
-  aep::launch_router_simt((const bf16*)x, (const bf16*)c->router_w[layer], T, H, E, k, cf.norm_topk, ids, w, st);
+  if (cf.flags & ASYNCEP_FLAG_SIMT_ROUTER)
+    aep::launch_router_simt((const bf16*)x, (const bf16*)c->router_w[layer], T, H, E, k, cf.norm_topk, ids, w, st);
+  else if (!aep::launch_router_tc(c->router_maps[layer], (const bf16*)x, T, H, E, k, cf.norm_topk, ids, w,
+                                  c->num_sms, st))
+    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router x map)");
   c->launches += 1;
   if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
   // (2) permute / dispatch
   aep::launch_perm_hist(ids, T, k, E, blk, st);
-  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, st);
-  aep::launch_perm_scatter((const bf16*)x, ids, blk, T, H, k, E, dest, src_tok, xperm, st);
+  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), st);
+  aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok, xperm, st);
   c->launches += 3;
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
   // wait for this layer's gathered experts (placed just before GEMM1 so router and
@@ -385,8 +398,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
   const uint8_t* wl = (const uint8_t*)(res ? c->shard[layer] : c->slot[s]);
   const aep::GemmMaps& wm = res ? c->layer_maps[layer] : c->slot_maps[s];
-  aep::GroupedArgs g{offsets, tile_start, E,
-                     (int)(((int64_t)T * k + aep::kTileM - 1) / aep::kTileM + E)};
+  aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kTileM)};
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

@@ -8,6 +8,7 @@
 namespace aep {
 
 namespace {
+template <int KMAX>
 __global__ void __launch_bounds__(256) combine_kernel(const bf16* __restrict__ yperm,
                                                       const int32_t* __restrict__ dest,
                                                       const float* __restrict__ w, const bf16* residual,
@@ -15,15 +16,14 @@ __global__ void __launch_bounds__(256) combine_kernel(const bf16* __restrict__ y
   const int lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (t >= T) return;
-  int32_t d[kMaxTopK];
-  float wj[kMaxTopK];
+  int32_t d[KMAX];
+  float wj[KMAX];
 #pragma unroll
-  for (int j = 0; j < kMaxTopK; ++j) {
+  for (int j = 0; j < KMAX; ++j) {
     d[j] = (j < k) ? dest[t * k + j] : 0;
     wj[j] = (j < k) ? w[t * k + j] : 0.f;
   }
   const int nv = H / 8;
-#pragma unroll 2
   for (int v = lane; v < nv; v += 32) {
     float acc[8];
     if (residual) {
@@ -35,15 +35,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const bf16* __restrict__ y
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.f;
     }
-    uint4 vals[kMaxTopK];
+    uint4 vals[KMAX];
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j)
+    for (int j = 0; j < KMAX; ++j)
       if (j < k)
         asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(vals[j].x), "=r"(vals[j].y), "=r"(vals[j].z), "=r"(vals[j].w)
                      : "l"(reinterpret_cast<const uint4*>(yperm + (int64_t)d[j] * H) + v));
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j) {
+    for (int j = 0; j < KMAX; ++j) {
       if (j < k) {
         const uint32_t u[4] = {vals[j].x, vals[j].y, vals[j].z, vals[j].w};
 #pragma unroll
@@ -67,7 +67,10 @@ void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, cons
                     int64_t T, int H, int k, cudaStream_t s) {
   if (T <= 0) return;
   const unsigned grid = (unsigned)((T + 7) / 8);
-  combine_kernel<<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
+  if (k <= 2) combine_kernel<2><<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
+  else if (k <= 4) combine_kernel<4><<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
+  else if (k <= 8) combine_kernel<8><<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
+  else combine_kernel<16><<<grid, 256, 0, s>>>(yperm, dest, w, residual, y, T, H, k);
 }
 
 }  // namespace aep

@@ -12,8 +12,8 @@ namespace {
 constexpr int SN = 64;   // output columns per CTA
 constexpr int SK = 16;   // K chunk
 
-__device__ __forceinline__ void decode_mtile(int mt, const int32_t* ts, const int32_t* off, int E, int& e,
-                                             int& row0, int& row_end) {
+__device__ __forceinline__ void decode_mtile(int mt, const int32_t* ts, const int32_t* off, const int32_t* cnt,
+                                             int E, int& e, int& row0, int& row_end) {
   int lo = 0, hi = E - 1;  // largest e with ts[e] <= mt
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -21,7 +21,7 @@ __device__ __forceinline__ void decode_mtile(int mt, const int32_t* ts, const in
   }
   e = lo;
   row0 = off[e] + (mt - ts[e]) * kTileM;
-  row_end = off[e + 1];
+  row_end = off[e] + cnt[e];
 }
 
 template <bool SWIGLU>
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GroupedArgs g, const bf1
   const int total = g.tile_start[g.E];
   for (int mt = blockIdx.y; mt < total; mt += gridDim.y) {
     int e, row0, row_end;
-    decode_mtile(mt, g.tile_start, g.offsets, g.E, e, row0, row_end);
+    decode_mtile(mt, g.tile_start, g.offsets, g.counts, g.E, e, row0, row_end);
     const bf16* W = reinterpret_cast<const bf16*>(layer + (size_t)e * expert_bytes + b_off);
     // B rows for this CTA's output columns
     int rg, ru = 0;

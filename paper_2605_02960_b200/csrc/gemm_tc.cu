@@ -32,20 +32,25 @@ constexpr int STAGES = 4;
 constexpr int NTHREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int B_BYTES_MAX = 256 * BK * 2;      // 32 KB
+constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 256 +
-                              2 * (kMaxExperts + 1) * sizeof(int32_t);
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES +
+                              256 + (kMaxExperts + 1) * sizeof(int32_t);
+
+enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2 };
 
 struct TcArgs {
-  const int32_t* offsets;
-  const int32_t* tile_start;
-  int E;
+  const int32_t* tile_start;  // grouped mode: [E+1] m-tile prefix (expert rows padded to BM)
+  int E;                      // groups (experts); router mode: number of experts (columns)
+  int dense_rows;             // > 0: dense mode, one group of dense_rows rows (router)
   int K;        // contraction length (multiple of 64)
-  int BN;       // N tile = rows of B per tile (multiple of 16, <= 256)
+  int BN;       // N tile = rows of B per tile (multiple of 64, <= 256)
   int n_tiles;  // N tiles per m-tile
-  int swiglu;   // 1: GEMM1 SwiGLU epilogue; 0: plain store
-  int n_out;    // output columns = output row stride
-  bf16* out;
+  int n_out;    // output columns
+  // router epilogue
+  int top_k, norm_topk;
+  int32_t* ids;
+  float* w;
 };
 
 __device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
@@ -57,29 +62,109 @@ __device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
   return lo;
 }
 
+// Router epilogue, one thread = one token row of the logits tile (E <= 256 columns in
+// TMEM): running top-k in registers (descending logit, ties -> lower expert id, R2), then
+// w_j = softmax over the k selected logits (norm_topk, R1) or the full-E softmax entry.
+__device__ __forceinline__ void router_epilogue(uint32_t tb, int E, int k, int norm_topk, bool valid,
+                                                int32_t* ids, float* w) {
+  float tv[kMaxTopK];
+  int ti[kMaxTopK];
+#pragma unroll
+  for (int j = 0; j < kMaxTopK; ++j) { tv[j] = -INFINITY; ti[j] = 0x7fffffff; }
+  for (int c0 = 0; c0 < E; c0 += 32) {
+    uint32_t r[32];
+    tmem_ld32(tb + c0, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      float v = __uint_as_float(r[i]);
+      int e = c0 + i;
+      if (e >= E) break;
+#pragma unroll
+      for (int j = 0; j < kMaxTopK; ++j) {
+        if (j < k && (v > tv[j] || (v == tv[j] && e < ti[j]))) {
+          const float sv = tv[j];
+          const int se = ti[j];
+          tv[j] = v; ti[j] = e; v = sv; e = se;
+        }
+      }
+    }
+  }
+  float denom = 0.f;
+  const float ref = tv[0];
+  if (norm_topk) {
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j)
+      if (j < k) denom += expf(tv[j] - ref);
+  } else {
+    for (int c0 = 0; c0 < E; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tb + c0, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c0 + i < E) denom += expf(__uint_as_float(r[i]) - ref);
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j)
+      if (j < k) {
+        ids[j] = ti[j];
+        w[j] = expf(tv[j] - ref) / denom;
+      }
+  }
+}
+
+// Epilogue store of 64 bf16 columns (32 packed words) of this thread's row through the
+// warp's 32 x 128 B staging buffer (128-B swizzle: 16-B chunk j of row r at chunk
+// j ^ (r & 7), conflict-free) and one TMA bulk tensor store of the {64 x 32} box.
+__device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t* stg, int lane,
+                                                const CUtensorMap* map_out, int col0, int row0) {
+  if (lane == 0) bulk_wait_read0();  // previous store has finished reading the buffer
+  __syncwarp();
+  const uint32_t base = smem_u32(stg) + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(base + ((j ^ (lane & 7)) << 4), o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_2d(map_out, stg, col0, row0);
+    bulk_commit();
+  }
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const TcArgs p) {
+                   const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES_MAX);
+  uint8_t* sStg = sB + STAGES * B_BYTES_MAX;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  int32_t* s_ts = reinterpret_cast<int32_t*>(smem + STAGES * (A_BYTES + B_BYTES_MAX) + 256);
-  int32_t* s_off = s_ts + (kMaxExperts + 1);
+  int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = warp_id(), lane = lane_id();
-  for (int i = threadIdx.x; i <= p.E; i += NTHREADS) {
-    s_ts[i] = p.tile_start[i];
-    s_off[i] = p.offsets[i];
+  const int G = p.dense_rows > 0 ? 1 : p.E;  // number of groups
+  if (p.dense_rows > 0) {
+    if (threadIdx.x == 0) {
+      s_ts[0] = 0;
+      s_ts[1] = (p.dense_rows + BM - 1) / BM;
+    }
+  } else {
+    for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i];
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (MODE != EPI_ROUTER) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -95,7 +180,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total = s_ts[p.E] * p.n_tiles;
+  const int total = s_ts[G] * p.n_tiles;
   const int nkb = p.K / BK;
 
   if (warp == 0) {
@@ -106,8 +191,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-        const int e = find_expert(s_ts, p.E, mt);
-        const int row0 = s_off[e] + (mt - s_ts[e]) * BM;
+        const int e = find_expert(s_ts, G, mt);
+        const int row0 = mt * BM;  // expert row ranges are padded to BM multiples
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], tx);
@@ -149,53 +234,54 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
   } else if (warp >= 4) {
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
+    uint8_t* stg = sStg + ew * STG_BYTES;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-      const int e = find_expert(s_ts, p.E, mt);
-      const int row = s_off[e] + (mt - s_ts[e]) * BM + ew * 32 + lane;
-      const bool valid = row < s_off[e + 1];
+      const int wrow0 = mt * BM + ew * 32;  // first row of this warp's 32-row slice
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
-      if (p.swiglu) {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.n_out + nt * 128);
+      if (MODE == EPI_ROUTER) {
+        const int row = wrow0 + lane;
+        router_epilogue(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows, p.ids + (int64_t)row * p.top_k,
+                        p.w + (int64_t)row * p.top_k);
+      } else if (MODE == EPI_SWIGLU) {
+        // accumulator columns [0,128) = gate, [128,256) = up of act columns nt*128 + [0,128)
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 32) {
-          uint32_t g[32], u[32];
-          tmem_ld32(tb + c0, g);
-          tmem_ld32(tb + 128 + c0, u);
-          tmem_ld_wait();
-          if (valid) {
-            uint32_t o[16];
+        for (int c0 = 0; c0 < 128; c0 += 64) {
+          uint32_t o[32];
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            uint32_t g[32], u[32];
+            tmem_ld32(tb + c0 + 32 * half, g);
+            tmem_ld32(tb + 128 + c0 + 32 * half, u);
+            tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const float a0 = silu_f(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
               const float a1 = silu_f(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
-              o[i] = pack_bf16x2(a0, a1);
+              o[16 * half + i] = pack_bf16x2(a0, a1);
             }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[c0 / 8 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
           }
+          stage_and_store(o, stg, lane, &map_out, nt * 128 + c0, wrow0);
         }
       } else {
-        uint4* dst = reinterpret_cast<uint4*>(p.out + (int64_t)row * p.n_out + nt * p.BN);
 #pragma unroll 1
-        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        for (int c0 = 0; c0 < p.BN; c0 += 64) {
           if (nt * p.BN + c0 >= p.n_out) break;
-          uint32_t r[32];
-          tmem_ld32(tb + c0, r);
-          tmem_ld_wait();
-          if (valid) {
-            uint32_t o[16];
+          uint32_t o[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+          for (int half = 0; half < 2; ++half) {
+            uint32_t r[32];
+            tmem_ld32(tb + c0 + 32 * half, r);
+            tmem_ld_wait();
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              dst[c0 / 8 + q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+            for (int i = 0; i < 16; ++i)
+              o[16 * half + i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
           }
+          stage_and_store(o, stg, lane, &map_out, nt * p.BN + c0, wrow0);
         }
       }
       tc_fence_before();
@@ -203,6 +289,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (MODE != EPI_ROUTER && lane == 0) bulk_wait0();  // all stores of this warp complete
+    __syncwarp();
   }
   __syncthreads();
   if (warp == 2) {
@@ -211,16 +299,29 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-void launch_tc(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, int K, int BN, int n_tiles,
-               int swiglu, int n_out, bf16* out, int num_sms, cudaStream_t s) {
+template <int MODE>
+void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
+                 cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
   });
-  TcArgs a{g.offsets, g.tile_start, g.E, K, BN, n_tiles, swiglu, n_out, out};
+  gemm_tc_kernel<MODE><<<grid, NTHREADS, SMEM_BYTES, s>>>(ma, mb, mo, a);
+}
+
+void launch_tc(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int K,
+               int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s) {
+  TcArgs a{};
+  a.tile_start = g.tile_start;
+  a.E = g.E;
+  a.K = K;
+  a.BN = BN;
+  a.n_tiles = n_tiles;
+  a.n_out = n_out;
   const int upper = g.max_m_tiles * n_tiles;
   const int grid = upper < num_sms ? (upper > 0 ? upper : 1) : num_sms;
-  gemm_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(ma, mb, a);
+  if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU>(a, ma, mb, mo, grid, s);
+  else launch_mode<EPI_PLAIN>(a, ma, mb, mo, grid, s);
 }
 }  // namespace
 
@@ -239,6 +340,19 @@ bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max
     const uint64_t dims[2] = {(uint64_t)h, (uint64_t)R_max};
     const uint64_t strides[1] = {(uint64_t)h * 2};
     if (!encode_tmap(&m.act, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  {  // epilogue TMA-store maps: box {64 cols, 32 rows}
+    const uint32_t sbox[2] = {64, 32};
+    const uint64_t d1[2] = {(uint64_t)h, (uint64_t)R_max};
+    const uint64_t s1[1] = {(uint64_t)h * 2};
+    if (!encode_tmap(&m.act_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, act, d1, s1, sbox,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const uint64_t d2[2] = {(uint64_t)H, (uint64_t)R_max};
+    const uint64_t s2[1] = {(uint64_t)H * 2};
+    if (!encode_tmap(&m.yperm_out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, xperm, d2, s2, sbox,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
   }
@@ -270,13 +384,56 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
                      int num_sms, cudaStream_t s) {
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
-  launch_tc(g, am.xperm, wm.wgu, H, 256, (2 * h) / 256, 1, h, act, num_sms, s);
+  launch_tc(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
 }
 
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
                      int num_sms, cudaStream_t s) {
   const int bn = am.bn2;
-  launch_tc(g, am.act, wm.wd, h, bn, (H + bn - 1) / bn, 0, H, yperm, num_sms, s);
+  launch_tc(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
+}
+
+// ------------------------------------------------------------------ router on tcgen05
+// Logits tile = 128 tokens x E_pad experts (M=128, N=E_pad, K=H) in TMEM, fp32; the
+// epilogue threads (one per token) do the top-k straight out of TMEM.
+bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E) {
+  rt.E_pad = (E + 15) / 16 * 16;
+  {
+    const uint64_t dims[3] = {(uint64_t)H, (uint64_t)E, 1};
+    const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)H * 2 * E};
+    const uint32_t box[3] = {BK, (uint32_t)rt.E_pad, 1};
+    if (!encode_tmap(&rt.map_wr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  return true;
+}
+
+bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
+                      int32_t* ids, float* w, int num_sms, cudaStream_t s) {
+  if (T <= 0) return true;
+  CUtensorMap map_x;
+  {
+    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
+    const uint64_t strides[1] = {(uint64_t)H * 2};
+    const uint32_t box[2] = {BK, BM};
+    if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  TcArgs a{};
+  a.E = E;
+  a.dense_rows = (int)T;
+  a.K = H;
+  a.BN = rt.E_pad;
+  a.n_tiles = 1;
+  a.top_k = k;
+  a.norm_topk = norm_topk;
+  a.ids = ids;
+  a.w = w;
+  const int tiles = (int)((T + BM - 1) / BM);
+  launch_mode<EPI_ROUTER>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
+  return true;
 }
 
 // ------------------------------------------------------------------ tensor-map encoding

@@ -22,29 +22,39 @@ void launch_router_simt(const bf16* x, const bf16* wr, int64_t T, int H, int E, 
 
 // Step (1) on tensor cores: tcgen05 logits tile (128 tokens x E) + top-k epilogue.
 struct RouterTc {
-  CUtensorMap map_x;  // [T_max, H] bf16, box {64, 128}, SW128
-  CUtensorMap map_wr; // [E, H] bf16, box {64, E_pad}
+  CUtensorMap map_wr; // [E, H] bf16 (3-D {H, E, 1}), box {64, E_pad, 1}, SW128 -- per layer
   int E_pad;          // E rounded up to a multiple of 16 (MMA N)
 };
-bool make_router_maps(RouterTc& rt, const bf16* x, int64_t T_max, const bf16* wr, int H, int E);
-void launch_router_tc(const RouterTc& rt, int64_t T, int H, int E, int k, int norm_topk, int32_t* ids,
-                      float* w, int num_sms, cudaStream_t s);
+bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E);
+// x map is built per call (x is the caller's buffer): [T, H] bf16, box {64, 128}
+bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
+                      int32_t* ids, float* w, int num_sms, cudaStream_t s);
 
 // Step (2): permute / dispatch.
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s);
+// blk_counts is [E][nblk]; `done` is a zero-initialised device counter (re-armed by the kernel).
 void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
-                      int32_t* counts, cudaStream_t s);
-void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, int64_t T, int H,
-                         int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm, cudaStream_t s);
+                      int32_t* counts, unsigned int* done, cudaStream_t s);
+void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, const int32_t* offsets,
+                         int64_t T, int H, int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm,
+                         cudaStream_t s);
 
 // Step (3): grouped expert GEMM.  Weights come from a packed layer (see asyncep.h):
 // per expert blob of expert_bytes; W_gu at blob offset 0 ([2h, H]), W_down at 2h*H*2.
+// Expert e's rows of X_perm / act / Y_perm are [offsets[e], offsets[e] + counts[e]);
+// offsets are padded to kTileM multiples (offsets[e] = kTileM * tile_start[e]) so every
+// GEMM m-tile belongs to exactly one expert.
 struct GroupedArgs {
-  const int32_t* offsets;    // [E+1] rows of each expert in X_perm
+  const int32_t* offsets;    // [E+1] padded row offsets
   const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kTileM)
+  const int32_t* counts;     // [E] rows per expert
   int E;
   int max_m_tiles;           // host upper bound on tile_start[E]
 };
+// rows of the permuted buffers for T tokens: T*k + E*(kTileM-1), rounded up to kTileM
+inline int64_t perm_rows(int64_t T, int k, int E) {
+  return ((T * k + (int64_t)E * (kTileM - 1)) + kTileM - 1) / kTileM * kTileM;
+}
 // CUDA-core reference path (debug / sanitizer): SwiGLU GEMM1 and plain GEMM2.
 void launch_gemm1_simt(const GroupedArgs& g, const bf16* xperm, const uint8_t* layer, size_t expert_bytes,
                        int H, int h, bf16* act, cudaStream_t s);
@@ -57,9 +67,11 @@ struct GemmMaps {
   CUtensorMap wd;    // 3D {h, H, E} bf16, box {64, BN2, 1}
 };
 struct ActMaps {
-  CUtensorMap xperm; // 2D {H, R_max}, box {64, 128}
-  CUtensorMap act;   // 2D {h, R_max}, box {64, 128}
-  int bn2;           // GEMM2 N tile
+  CUtensorMap xperm;     // 2D {H, R_max}, box {64, 128}  (GEMM1 A)
+  CUtensorMap act;       // 2D {h, R_max}, box {64, 128}  (GEMM2 A)
+  CUtensorMap act_out;   // 2D {h, R_max}, box {64, 32}   (GEMM1 epilogue TMA store)
+  CUtensorMap yperm_out; // 2D {H, R_max}, box {64, 32}   (GEMM2 epilogue TMA store)
+  int bn2;               // GEMM2 N tile
 };
 bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2);
 bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h);

@@ -3,7 +3,8 @@
 //
 //   hist    : per-CTA (64-token chunk) expert histogram          -> blk_counts[nblk][E]
 //   scan    : per-expert exclusive scan over chunks + over experts -> row base of every
-//             (chunk, expert), offsets[E+1], GEMM m-tile prefix tile_start[E+1], counts[E]
+//             (chunk, expert), offsets[E+1] (padded to the GEMM M tile), m-tile prefix
+//             tile_start[E+1], counts[E]
 //   scatter : stable rank of every (t, j) inside its expert in (t, j) order (warp
 //             __match_any_sync + popc), then one warp per token copies x_t (16-B vectors)
 //             to its k destination rows of X_perm.
@@ -15,7 +16,7 @@ namespace aep {
 
 namespace {
 
-__global__ void perm_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E,
+__global__ void perm_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int k, int E, int nblk,
                                  int32_t* __restrict__ blk_counts) {
   extern __shared__ int32_t hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
@@ -26,52 +27,75 @@ __global__ void perm_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int
   const int32_t* p = ids + t0 * k;
   for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[p[i]], 1);
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) blk_counts[(int64_t)blockIdx.x * E + e] = hist[e];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) blk_counts[(int64_t)e * nblk + blockIdx.x] = hist[e];
 }
 
-// One CTA, one thread per expert.
-__global__ void perm_scan_kernel(int32_t* __restrict__ bc, int nblk, int E, int32_t* __restrict__ offsets,
-                                 int32_t* __restrict__ tile_start, int32_t* __restrict__ counts) {
+// One CTA per expert: exclusive scan of that expert's per-chunk counts (row e of the
+// [E][nblk] matrix) -> chunk base inside the expert; the last CTA to finish scans the
+// expert totals -> offsets[E+1], tile_start[E+1], counts[E].
+constexpr int SCAN_THREADS = 256;
+__global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __restrict__ bc, int nblk, int E,
+                                                                 int32_t* __restrict__ offsets,
+                                                                 int32_t* __restrict__ tile_start,
+                                                                 int32_t* __restrict__ counts,
+                                                                 unsigned int* __restrict__ done) {
+  __shared__ int32_t warp_tot[SCAN_THREADS / 32];
   __shared__ int32_t tot[kMaxExperts];
-  __shared__ int32_t off[kMaxExperts + 1];
-  const int e = threadIdx.x;
-  if (e < E) {
-    int32_t run = 0;
-#pragma unroll 8
-    for (int b = 0; b < nblk; ++b) {
-      const int32_t c = bc[(int64_t)b * E + e];
-      bc[(int64_t)b * E + e] = run;
+  __shared__ bool last;
+  const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  int32_t* row = bc + (int64_t)e * nblk;
+  const int per = (nblk + SCAN_THREADS - 1) / SCAN_THREADS;  // consecutive chunks per thread
+  const int b0 = tid * per;
+  int32_t local = 0;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < nblk) local += row[b0 + i];
+  // block exclusive scan of `local`
+  int32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[wid] = incl;
+  __syncthreads();
+  int32_t wbase = 0;
+  for (int w = 0; w < wid; ++w) wbase += warp_tot[w];
+  int32_t run = wbase + incl - local;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < nblk) {
+      const int32_t c = row[b0 + i];
+      row[b0 + i] = run;
       run += c;
     }
-    tot[e] = run;
-    if (counts) counts[e] = run;
+  if (tid == SCAN_THREADS - 1) {
+    counts[e] = run;  // expert total (thread holding the last chunk ends at the total)
+    __threadfence();
+    last = (atomicAdd(done, 1u) == (unsigned)(gridDim.x - 1));
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int32_t o = 0, ts = 0;
+  if (!last) return;
+  __threadfence();
+  for (int i = tid; i < E; i += SCAN_THREADS) tot[i] = ((volatile int32_t*)counts)[i];
+  __syncthreads();
+  if (tid == 0) {
+    int32_t ts = 0;  // expert row ranges padded to kTileM: offsets[e] = kTileM * tile_start[e]
     for (int i = 0; i < E; ++i) {
-      off[i] = o;
-      offsets[i] = o;
+      offsets[i] = ts * kTileM;
       tile_start[i] = ts;
-      o += tot[i];
       ts += (tot[i] + kTileM - 1) / kTileM;
     }
-    off[E] = o;
-    offsets[E] = o;
+    offsets[E] = ts * kTileM;
     tile_start[E] = ts;
-  }
-  __syncthreads();
-  if (e < E) {
-    const int32_t base = off[e];
-#pragma unroll 8
-    for (int b = 0; b < nblk; ++b) bc[(int64_t)b * E + e] += base;
+    *done = 0;  // re-arm for the next forward (stream-ordered)
   }
 }
 
 __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restrict__ x,
                                                            const int32_t* __restrict__ ids,
-                                                           const int32_t* __restrict__ blk_base, int64_t T,
-                                                           int H, int k, int E, int32_t* __restrict__ dest,
+                                                           const int32_t* __restrict__ blk_base,
+                                                           const int32_t* __restrict__ offsets, int nblk,
+                                                           int64_t T, int H, int k, int E,
+                                                           int32_t* __restrict__ dest,
                                                            int32_t* __restrict__ src_tok,
                                                            bf16* __restrict__ xperm) {
   __shared__ int32_t cnt[kMaxExperts];
@@ -80,11 +104,11 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
   const int64_t t0 = (int64_t)blockIdx.x * kPermTokensPerBlock;
   const int tn = (int)min((int64_t)kPermTokensPerBlock, T - t0);
   const int n = tn * k;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) cnt[e] = 0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    cnt[e] = offsets[e] + blk_base[(int64_t)e * nblk + blockIdx.x];  // first row of this chunk in e
   __syncthreads();
   if (warp == 0) {
     // entries in (t, j) order, 32 at a time; stable rank inside each expert
-    const int32_t* bb = blk_base + (int64_t)blockIdx.x * E;
     for (int c = 0; c < n; c += 32) {
       const int i = c + lane;
       const bool valid = i < n;
@@ -93,7 +117,7 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
       const unsigned lt = (1u << lane) - 1u;
       const int rank = __popc(peers & lt);
       int d = 0;
-      if (valid) d = bb[e] + cnt[e] + rank;
+      if (valid) d = cnt[e] + rank;
       __syncwarp();
       if (valid && (peers & lt) == 0) cnt[e] += __popc(peers);
       __syncwarp();
@@ -128,19 +152,19 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
 
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s) {
   const int nblk = (int)((T + kPermTokensPerBlock - 1) / kPermTokensPerBlock);
-  perm_hist_kernel<<<nblk, 256, sizeof(int32_t) * E, s>>>(ids, T, k, E, blk_counts);
+  perm_hist_kernel<<<nblk, 256, sizeof(int32_t) * E, s>>>(ids, T, k, E, nblk, blk_counts);
 }
 
 void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
-                      int32_t* counts, cudaStream_t s) {
-  const int threads = ((E + 31) / 32) * 32;
-  perm_scan_kernel<<<1, threads, 0, s>>>(blk_counts, nblk, E, offsets, tile_start, counts);
+                      int32_t* counts, unsigned int* done, cudaStream_t s) {
+  perm_scan_kernel<<<E, SCAN_THREADS, 0, s>>>(blk_counts, nblk, E, offsets, tile_start, counts, done);
 }
 
-void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, int64_t T, int H, int k,
-                         int E, int32_t* dest, int32_t* src_tok, bf16* xperm, cudaStream_t s) {
+void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, const int32_t* offsets,
+                         int64_t T, int H, int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm,
+                         cudaStream_t s) {
   const int nblk = (int)((T + kPermTokensPerBlock - 1) / kPermTokensPerBlock);
-  perm_scatter_kernel<<<nblk, 256, 0, s>>>(x, ids, blk_base, T, H, k, E, dest, src_tok, xperm);
+  perm_scatter_kernel<<<nblk, 256, 0, s>>>(x, ids, blk_base, offsets, nblk, T, H, k, E, dest, src_tok, xperm);
 }
 
 }  // namespace aep

@@ -1,0 +1,125 @@
+"""AsyncEP weight streaming on one GPU (Tier 1 at PAPER.md:544).
+
+N ranks are emulated in one process: every "rank" r holds only experts [rE/N,(r+1)E/N) of
+layers >= 1 (layer 0 replicated); rank 0 runs the stack with the double-buffered slot and
+the same event ordering as the NCCL path, filling the slot by device-to-device copies of
+the N shards (asyncep_prefetch_layer_local).  The output must be BITWISE equal to the
+resident 1-GPU stack (the gather is a memcpy and the kernels are deterministic)."""
+import pytest
+import torch
+
+from gpu_helpers import Workload
+
+pytestmark = pytest.mark.gpu
+
+
+def _bits(t):
+    return t.contiguous().view(torch.int16)
+
+
+@pytest.mark.parametrize("N", [2, 4, 8])
+def test_sharded_stack_bitwise_equals_resident(N):
+    wl = Workload(L=5, E=16, k=4, H=256, h=256, seed=11)
+    T = 1500
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    ranks = [wl.stack(max_tokens=T, world_size=N, rank=r) for r in range(N)]
+    s0 = ranks[0]
+
+    def shards(l):
+        return [ranks[r].shards[l] for r in range(N)]
+
+    out = s0.run(x, local_shards=shards).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
+    # a second pass reuses both slots (WAR ordering through slot_free events)
+    out2 = s0.run(x, local_shards=shards).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out2), _bits(ref))
+
+
+def test_slot_holds_the_unsharded_layer_bytes():
+    wl = Workload(L=3, E=8, k=2, H=64, h=128, seed=12)
+    full = wl.stack(max_tokens=64)
+    N = 4
+    ranks = [wl.stack(max_tokens=64, world_size=N, rank=r) for r in range(N)]
+    s0 = ranks[0]
+    from paper_2605_02960_b200 import asyncep as A
+    A.asyncep_prefetch_layer_local(s0.ctx, 1, [ranks[r].shards[1] for r in range(N)])
+    torch.cuda.synchronize()
+    assert torch.equal(s0.slots[1], full.shards[1])
+
+
+def test_prefetch_ordering_errors():
+    from paper_2605_02960_b200 import asyncep as A
+    wl = Workload(L=4, E=8, k=2, H=64, h=128, seed=13)
+    N = 2
+    ranks = [wl.stack(max_tokens=64, world_size=N, rank=r) for r in range(N)]
+    s0 = ranks[0]
+    sh = lambda l: [ranks[r].shards[l] for r in range(N)]
+    x = wl.tokens(64)
+    y = torch.empty_like(x)
+    s0.forward(0, x, y=y)  # layer 0 is replicated: no prefetch needed
+    with pytest.raises(A.AsyncEPError) as ei:
+        s0.forward(1, x, y=y)
+    assert ei.value.status == A.ERR_NOT_PREFETCHED
+    A.asyncep_prefetch_layer_local(s0.ctx, 1, sh(1))
+    with pytest.raises(A.AsyncEPError) as ei:   # layer 3 would overwrite slot 1 before forward(1)
+        A.asyncep_prefetch_layer_local(s0.ctx, 3, sh(3))
+    assert ei.value.status == A.ERR_INVALID_ARG
+    s0.forward(1, x, y=y)
+    A.asyncep_prefetch_layer_local(s0.ctx, 3, sh(3))   # now legal
+    with pytest.raises(A.AsyncEPError):
+        A.asyncep_prefetch_layer(s0.ctx, 2)  # no NCCL communicator given
+    torch.cuda.synchronize()
+
+
+def test_delayed_gather_only_slows_down():
+    """Fault injection: a long spin kernel on the comm stream before the
+    gather must not change the output (catches a missing ag_done wait)."""
+    wl = Workload(L=3, E=16, k=4, H=256, h=256, seed=14)
+    T = 512
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    N = 2
+    ranks = [wl.stack(max_tokens=T, world_size=N, rank=r) for r in range(N)]
+    s0 = ranks[0]
+    sh = lambda l: [ranks[r].shards[l] for r in range(N)]
+    with torch.cuda.stream(s0.comm_stream):
+        torch.cuda._sleep(200_000_000)  # ~0.1 s of spinning on the comm stream
+    out = s0.run(x, local_shards=sh).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
+
+
+def test_poisoned_slot_after_use_is_never_read():
+    """Poison a slot right after its layer's GEMMs (ordered after slot_free on the comm
+    stream); a later layer reading it too early would produce NaN (catches WAR bugs)."""
+    from paper_2605_02960_b200 import asyncep as A
+    wl = Workload(L=4, E=8, k=2, H=64, h=128, seed=15)
+    T = 256
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    N = 2
+    ranks = [wl.stack(max_tokens=T, world_size=N, rank=r) for r in range(N)]
+    s0 = ranks[0]
+    sh = lambda l: [ranks[r].shards[l] for r in range(N)]
+    bufs = [torch.empty_like(x) for _ in range(2)]
+    cur = x
+    A.asyncep_prefetch_layer_local(s0.ctx, 1, sh(1))
+    for l in range(4):
+        if l + 1 < 4:
+            A.asyncep_prefetch_layer_local(s0.ctx, l + 1, sh(l + 1))
+        dst = bufs[l % 2]
+        s0.forward(l, cur, residual=cur, y=dst)
+        if l >= 1:
+            # poison on the comm stream after the event that frees the slot: the next
+            # prefetch into this slot is ordered after the poison, so results stay exact
+            ev = torch.cuda.Event()
+            ev.record(s0.compute_stream)
+            s0.comm_stream.wait_event(ev)
+            with torch.cuda.stream(s0.comm_stream):
+                s0.slots[l % 2].view(torch.int16).fill_(0x7FC0)  # bf16 NaN pattern
+        cur = dst
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(cur), _bits(ref))

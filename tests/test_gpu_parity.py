@@ -38,7 +38,7 @@ def test_synth_generator_is_bit_identical_on_cpu_and_gpu():
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
-@pytest.mark.parametrize("flags", [0, 2], ids=["tcgen05", "simt"])
+@pytest.mark.parametrize("flags", [0, 2, 8, 10], ids=["tcgen05", "simt_gemm", "simt_router", "simt_all"])
 @pytest.mark.parametrize("T", [256, 1, 63, 1000])
 def test_tiny_layer_parity(flags, T):
     wl = Workload(**TINY, seed=1)
@@ -110,6 +110,26 @@ def test_edge_cases_and_errors():
     y, ids, w, counts = run_layer(wl, st, 0, x[:128])
     wr, g, u, d = wl.host_layer(0)
     check_layer(f32(x[:128]), wr, g, u, d, 2, y, ids, w, counts)
+
+
+def test_router_tcgen05_vs_simt_ids():
+    """The tcgen05 router and the CUDA-core router pick the same experts (outside near
+    ties) and agree on weights; both are fp32-accumulated logits (R3)."""
+    wl = Workload(L=1, E=128, k=8, H=2048, h=128, seed=9)
+    T = 5000
+    x = wl.tokens(T)
+    outs = []
+    for flags in (0, 8):
+        st = wl.stack(max_tokens=T, flags=flags | 1)
+        ids = torch.empty((T, 8), dtype=torch.int32, device="cuda")
+        w = torch.empty((T, 8), dtype=torch.float32, device="cuda")
+        st.forward(0, x, y=torch.empty_like(x), ids=ids, w=w)
+        torch.cuda.synchronize()
+        outs.append((ids.cpu().numpy(), w.cpu().numpy()))
+    orc = oracle.router(f32(x), f32(wl.router(0)), 8)
+    far = orc["gap"] >= 1e-4
+    assert np.array_equal(np.sort(outs[0][0], 1)[far], np.sort(outs[1][0], 1)[far])
+    assert np.abs(np.sort(outs[0][1], 1) - np.sort(outs[1][1], 1))[far].max() <= 1e-5
 
 
 def test_deterministic_bitwise():
