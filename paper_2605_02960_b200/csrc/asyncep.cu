@@ -398,7 +398,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
   const uint8_t* wl = (const uint8_t*)(res ? c->shard[layer] : c->slot[s]);
   const aep::GemmMaps& wm = res ? c->layer_maps[layer] : c->slot_maps[s];
-  aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kTileM)};
+  aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign)};
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

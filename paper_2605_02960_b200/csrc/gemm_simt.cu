@@ -14,13 +14,15 @@ constexpr int SK = 16;   // K chunk
 
 __device__ __forceinline__ void decode_mtile(int mt, const int32_t* ts, const int32_t* off, const int32_t* cnt,
                                              int E, int& e, int& row0, int& row_end) {
-  int lo = 0, hi = E - 1;  // largest e with ts[e] <= mt
+  constexpr int per = kRowAlign / kTileM;  // 128-row tiles per padded row tile
+  const int pt = mt / per;
+  int lo = 0, hi = E - 1;  // largest e with ts[e] <= pt
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (ts[mid] <= mt) lo = mid; else hi = mid - 1;
+    if (ts[mid] <= pt) lo = mid; else hi = mid - 1;
   }
   e = lo;
-  row0 = off[e] + (mt - ts[e]) * kTileM;
+  row0 = mt * kTileM;
   row_end = off[e] + cnt[e];
 }
 
@@ -35,7 +37,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GroupedArgs g, const bf1
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int n0 = blockIdx.x * SN;
-  const int total = g.tile_start[g.E];
+  const int total = g.tile_start[g.E] * (kRowAlign / kTileM);
   for (int mt = blockIdx.y; mt < total; mt += gridDim.y) {
     int e, row0, row_end;
     decode_mtile(mt, g.tile_start, g.offsets, g.counts, g.E, e, row0, row_end);
@@ -131,13 +133,13 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GroupedArgs g, const bf1
 
 void launch_gemm1_simt(const GroupedArgs& g, const bf16* xperm, const uint8_t* layer, size_t expert_bytes,
                        int H, int h, bf16* act, cudaStream_t s) {
-  dim3 grid(h / SN, (unsigned)min(g.max_m_tiles, 4096));
+  dim3 grid(h / SN, (unsigned)min(g.max_m_tiles * (kRowAlign / kTileM), 4096));
   gemm_simt_kernel<true><<<grid, 256, 0, s>>>(g, xperm, layer, expert_bytes, 0, H, H, h, act);
 }
 
 void launch_gemm2_simt(const GroupedArgs& g, const bf16* act, const uint8_t* layer, size_t expert_bytes,
                        int H, int h, bf16* yperm, cudaStream_t s) {
-  dim3 grid((H + SN - 1) / SN, (unsigned)min(g.max_m_tiles, 4096));
+  dim3 grid((H + SN - 1) / SN, (unsigned)min(g.max_m_tiles * (kRowAlign / kTileM), 4096));
   gemm_simt_kernel<false><<<grid, 256, 0, s>>>(g, act, layer, expert_bytes, (size_t)2 * h * H * 2, h, h, H,
                                                yperm);
 }

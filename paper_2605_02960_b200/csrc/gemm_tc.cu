@@ -1,23 +1,31 @@
-// gemm_tc.cu -- step (3): the grouped expert GEMM on 5th-gen tensor cores (sm_100a).
+// gemm_tc.cu -- step (3): the grouped expert GEMM on 5th-gen tensor cores (sm_100a),
+// and the router logits GEMM of step (1) with its top-k fused into the epilogue.
 //
 //   GEMM1 (per expert e, rows R_e of X_perm):  G = X_perm[R_e] . W_gu[e]^T  -> SwiGLU epilogue
 //          act = bf16( silu(G_gate) * G_up )                     (R4, R5)
 //   GEMM2:  Y_perm[R_e] = bf16( act[R_e] . W_down[e]^T )
+//   router: logits = x . W_r^T (fp32, R3) -> top-k -> weights    (R1, R2)
 //
-// Persistent, warp-specialised CTA (one per SM, 256 threads):
-//   warp 0      TMA producer: A tile {64 x 128 rows} (2-D map over X_perm / act) and
-//               B tile {64 x BN rows x 1 expert} (3-D map over the packed layer) into a
-//               4-stage shared-memory ring (128-B swizzle), mbarrier full/empty pairs.
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
-//               (M=128, N=BN, K=16) x 4 per stage into a TMEM accumulator; tcgen05.commit
-//               frees the smem stage / publishes the accumulator.
+// Persistent, warp-specialised kernel, 256 threads per CTA, one CTA per SM:
+//   warp 0      TMA producer: A tile {64 x 128 rows} (2-D map over X_perm / act / x) and
+//               B tile {64 x BN/NCTA rows x 1 expert} (3-D map over the packed layer) into
+//               an S-stage shared-memory ring (128-B swizzle); mbarrier full/empty pairs.
+//   warp 1      MMA issuer (leader CTA only): one thread issues tcgen05.mma kind::f16
+//               (M = 128*NCTA, N = BN, K = 16) x 4 per stage into a TMEM accumulator;
+//               tcgen05.commit frees the smem stage / publishes the accumulator.
 //   warp 2      TMEM allocator (512 columns = 2 accumulators x 256).
-//   warps 4-7   epilogue: tcgen05.ld 32x32b (thread = accumulator row), SwiGLU or plain
-//               bf16 pack, masked 16-B stores of rows that belong to the expert.
-// Tiles: t -> (m-tile, n-tile), m-tile -> expert via the device-side prefix tile_start
-// (built by the permute scan), so the host never learns the per-expert counts.  Every
-// output tile is produced by exactly one CTA with a fixed K order: results are
-// bitwise-deterministic and independent of the grid size.
+//   warps 4-7   epilogue: tcgen05.ld 32x32b (thread = accumulator row) -> SwiGLU / plain
+//               bf16 pack -> swizzled smem staging -> TMA bulk tensor store; or top-k.
+// NCTA = 2 (the grouped GEMMs): a CTA pair (cluster of 2) runs cta_group::2 MMAs with
+// M = 256: each CTA loads its own 128 rows of A and HALF of the BN rows of B, so every
+// SM reads 8 KB of operands per 256x256x16 MMA instead of 12 KB per 128x256x16 (the
+// 1-CTA kernel was shared-memory-read bound, ncu: 90 % sm__mem_tensor).  For GEMM1 the
+// CTA0 half of a 256-row W_gu tile is exactly the gate rows and the CTA1 half the
+// matching up rows, so each CTA's accumulator holds [gate | up] and SwiGLU stays local.
+// Tiles: t -> (row tile, n-tile); row tile -> expert via the device-side prefix
+// tile_start (permute scan; expert rows padded to 256), no host sync.  Every output tile
+// is produced by one CTA (pair) in a fixed K order: bitwise deterministic results that do
+// not depend on the grid size.
 #include <mutex>
 
 #include "common.cuh"
@@ -26,26 +34,30 @@
 namespace aep {
 
 namespace {
-constexpr int BM = kTileM;          // 128 rows per tile (UMMA M)
+constexpr int BM = kTileM;          // 128 rows per CTA (per-CTA UMMA M slice)
 constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
-constexpr int STAGES = 4;
 constexpr int NTHREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
-constexpr int B_BYTES_MAX = 256 * BK * 2;      // 32 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int TMEM_COLS = 512;
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES +
-                              256 + (kMaxExperts + 1) * sizeof(int32_t);
+
+template <int NCTA>
+struct Cfg {
+  static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
+  static constexpr int STAGES = NCTA == 2 ? 6 : 4;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES + 256 +
+                                 (kMaxExperts + 1) * sizeof(int32_t);
+};
 
 enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2 };
 
 struct TcArgs {
-  const int32_t* tile_start;  // grouped mode: [E+1] m-tile prefix (expert rows padded to BM)
+  const int32_t* tile_start;  // grouped mode: [E+1] prefix of row tiles (rows padded to 128*NCTA)
   int E;                      // groups (experts); router mode: number of experts (columns)
   int dense_rows;             // > 0: dense mode, one group of dense_rows rows (router)
   int K;        // contraction length (multiple of 64)
-  int BN;       // N tile = rows of B per tile (multiple of 64, <= 256)
-  int n_tiles;  // N tiles per m-tile
+  int BN;       // N tile (multiple of 16*NCTA, <= 256); each CTA loads BN/NCTA rows of B
+  int n_tiles;  // N tiles per row tile
   int n_out;    // output columns
   // router epilogue
   int top_k, norm_topk;
@@ -135,15 +147,17 @@ __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t
   }
 }
 
-template <int MODE>
+template <int MODE, int NCTA>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
+  using C = Cfg<NCTA>;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
-  uint8_t* sStg = sB + STAGES * B_BYTES_MAX;
+  uint8_t* sStg = sB + STAGES * C::B_BYTES_MAX;
   uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -152,11 +166,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = warp_id(), lane = lane_id();
+  const uint32_t rank = NCTA == 2 ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int unit = NCTA == 2 ? (int)cluster_id_x() : (int)blockIdx.x;  // CTA pair (or CTA) index
+  const int nunits = NCTA == 2 ? (int)nclusters_x() : (int)gridDim.x;
+  constexpr int TM = BM * NCTA;  // rows per tile (per CTA pair)
   const int G = p.dense_rows > 0 ? 1 : p.E;  // number of groups
   if (p.dense_rows > 0) {
     if (threadIdx.x == 0) {
       s_ts[0] = 0;
-      s_ts[1] = (p.dense_rows + BM - 1) / BM;
+      s_ts[1] = (p.dense_rows + TM - 1) / TM;
     }
   } else {
     for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i];
@@ -166,51 +185,63 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tma_prefetch_desc(&map_b);
     if (MODE != EPI_ROUTER) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], NCTA);  // leader: own expect_tx arrive + peer's arrive
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], 4 * NCTA);  // one arrive per epilogue warp of each CTA
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) {
+    if (NCTA == 2) tmem_alloc2(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (NCTA == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total = s_ts[G] * p.n_tiles;
   const int nkb = p.K / BK;
+  const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
 
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol_b = policy_evict_last();
-      const uint32_t tx = (uint32_t)A_BYTES + (uint32_t)p.BN * BK * 2;
+      const uint32_t tx = (uint32_t)NCTA * ((uint32_t)A_BYTES + (uint32_t)bn_cta * BK * 2);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = unit; t < total; t += nunits) {
         const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
         const int e = find_expert(s_ts, G, mt);
-        const int row0 = mt * BM;  // expert row ranges are padded to BM multiples
+        const int row0 = mt * TM + (int)rank * BM;
+        const int brow = nt * p.BN + (int)rank * bn_cta;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], tx);
-          tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
-          tma_load_3d(sB + stage * B_BYTES_MAX, &map_b, &full[stage], kb * BK, nt * p.BN, e, pol_b);
+          if (NCTA == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+            else mbar_arrive_cluster_relaxed(&full[stage], 0);
+            tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
+            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], tx);
+            tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
+            tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(BM, p.BN, true);
+    if (lane == 0 && leader) {
+      const uint32_t idesc = make_idesc(TM, p.BN, true);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      for (int t = unit; t < total; t += nunits) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -218,15 +249,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * B_BYTES_MAX);
+          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES_MAX);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            mma_bf16(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
-                     (kb | k) != 0 ? 1u : 0u);
-          tc_commit(&empty[stage]);
+          for (int k = 0; k < BK / 16; ++k) {
+            if (NCTA == 2)
+              mma_bf16_2(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
+                         (kb | k) != 0 ? 1u : 0u);
+            else
+              mma_bf16(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
+                       (kb | k) != 0 ? 1u : 0u);
+          }
+          if (NCTA == 2) tc_commit2_mc(&empty[stage], 0x3);
+          else tc_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[acc]);
+        if (NCTA == 2) tc_commit2_mc(&tfull[acc], 0x3);
+        else tc_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -237,9 +275,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint8_t* stg = sStg + ew * STG_BYTES;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = unit; t < total; t += nunits) {
       const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
-      const int wrow0 = mt * BM + ew * 32;  // first row of this warp's 32-row slice
+      const int wrow0 = mt * TM + (int)rank * BM + ew * 32;  // first row of this warp's slice
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
@@ -285,32 +323,54 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (NCTA == 2) mbar_arrive_cluster(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
     if (MODE != EPI_ROUTER && lane == 0) bulk_wait0();  // all stores of this warp complete
     __syncwarp();
   }
-  __syncthreads();
+  tc_fence_before();
+  if (NCTA == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (NCTA == 2) tmem_dealloc2(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
-template <int MODE>
+template <int MODE, int NCTA>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
                  cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES);
+    cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)Cfg<NCTA>::SMEM);
   });
-  gemm_tc_kernel<MODE><<<grid, NTHREADS, SMEM_BYTES, s>>>(ma, mb, mo, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = Cfg<NCTA>::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = NCTA;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA>, ma, mb, mo, a);
 }
 
-void launch_tc(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int K,
-               int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s) {
+// grouped GEMMs run as CTA pairs
+constexpr int kGroupedNCTA = kRowAlign / kTileM;
+
+void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
+                    int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s) {
   TcArgs a{};
   a.tile_start = g.tile_start;
   a.E = g.E;
@@ -318,10 +378,11 @@ void launch_tc(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& m
   a.BN = BN;
   a.n_tiles = n_tiles;
   a.n_out = n_out;
-  const int upper = g.max_m_tiles * n_tiles;
-  const int grid = upper < num_sms ? (upper > 0 ? upper : 1) : num_sms;
-  if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU>(a, ma, mb, mo, grid, s);
-  else launch_mode<EPI_PLAIN>(a, ma, mb, mo, grid, s);
+  const int units = num_sms / kGroupedNCTA;
+  const int upper = g.max_m_tiles * n_tiles;  // row tiles (of kRowAlign rows) x n tiles
+  const int grid = kGroupedNCTA * (upper < units ? (upper > 0 ? upper : 1) : units);
+  if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, kGroupedNCTA>(a, ma, mb, mo, grid, s);
+  else launch_mode<EPI_PLAIN, kGroupedNCTA>(a, ma, mb, mo, grid, s);
 }
 }  // namespace
 
@@ -364,7 +425,7 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
   {
     const uint64_t dims[3] = {(uint64_t)H, (uint64_t)(2 * h), (uint64_t)E};
     const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, 256, 1};
+    const uint32_t box[3] = {BK, (uint32_t)(256 / kGroupedNCTA), 1};
     if (!encode_tmap(&m.wgu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, layer, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -373,7 +434,7 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
     const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * 2;
     const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};
     const uint64_t strides[2] = {(uint64_t)h * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, (uint32_t)bn2, 1};
+    const uint32_t box[3] = {BK, (uint32_t)(bn2 / kGroupedNCTA), 1};
     if (!encode_tmap(&m.wd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wd, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -384,43 +445,36 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
                      int num_sms, cudaStream_t s) {
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
-  launch_tc(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
+  launch_grouped(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
 }
 
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
                      int num_sms, cudaStream_t s) {
   const int bn = am.bn2;
-  launch_tc(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
+  launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
 }
 
 // ------------------------------------------------------------------ router on tcgen05
-// Logits tile = 128 tokens x E_pad experts (M=128, N=E_pad, K=H) in TMEM, fp32; the
-// epilogue threads (one per token) do the top-k straight out of TMEM.
+// Logits tile = 128 tokens x E_pad experts (M=128, N=E_pad, K=H, 1-CTA) in TMEM, fp32;
+// the epilogue threads (one per token) do the top-k straight out of TMEM.
 bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E) {
   rt.E_pad = (E + 15) / 16 * 16;
-  {
-    const uint64_t dims[3] = {(uint64_t)H, (uint64_t)E, 1};
-    const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)H * 2 * E};
-    const uint32_t box[3] = {BK, (uint32_t)rt.E_pad, 1};
-    if (!encode_tmap(&rt.map_wr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
-  }
-  return true;
+  const uint64_t dims[3] = {(uint64_t)H, (uint64_t)E, 1};
+  const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)H * 2 * E};
+  const uint32_t box[3] = {BK, (uint32_t)rt.E_pad, 1};
+  return encode_tmap(&rt.map_wr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
                       int32_t* ids, float* w, int num_sms, cudaStream_t s) {
   if (T <= 0) return true;
   CUtensorMap map_x;
-  {
-    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
-    const uint64_t strides[1] = {(uint64_t)H * 2};
-    const uint32_t box[2] = {BK, BM};
-    if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
-  }
+  const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
+  const uint64_t strides[1] = {(uint64_t)H * 2};
+  const uint32_t box[2] = {BK, BM};
+  if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   TcArgs a{};
   a.E = E;
   a.dense_rows = (int)T;
@@ -432,7 +486,7 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
   a.ids = ids;
   a.w = w;
   const int tiles = (int)((T + BM - 1) / BM);
-  launch_mode<EPI_ROUTER>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
+  launch_mode<EPI_ROUTER, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
   return true;
 }
 

@@ -11,7 +11,8 @@ namespace aep {
 typedef __nv_bfloat16 bf16;
 
 constexpr int kPermTokensPerBlock = 64;  // permute/dispatch granularity (tokens per CTA)
-constexpr int kTileM = 128;              // grouped-GEMM M tile (rows of one expert)
+constexpr int kTileM = 128;              // grouped-GEMM M rows per CTA (UMMA M slice)
+constexpr int kRowAlign = 256;           // expert row ranges are padded to this (one CTA-pair tile)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxTopK = 16;
 
@@ -42,18 +43,18 @@ void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_b
 // Step (3): grouped expert GEMM.  Weights come from a packed layer (see asyncep.h):
 // per expert blob of expert_bytes; W_gu at blob offset 0 ([2h, H]), W_down at 2h*H*2.
 // Expert e's rows of X_perm / act / Y_perm are [offsets[e], offsets[e] + counts[e]);
-// offsets are padded to kTileM multiples (offsets[e] = kTileM * tile_start[e]) so every
-// GEMM m-tile belongs to exactly one expert.
+// offsets are padded to kRowAlign multiples (offsets[e] = kRowAlign * tile_start[e]) so
+// every GEMM row tile belongs to exactly one expert.
 struct GroupedArgs {
   const int32_t* offsets;    // [E+1] padded row offsets
-  const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kTileM)
+  const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kRowAlign)
   const int32_t* counts;     // [E] rows per expert
   int E;
-  int max_m_tiles;           // host upper bound on tile_start[E]
+  int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
 };
-// rows of the permuted buffers for T tokens: T*k + E*(kTileM-1), rounded up to kTileM
+// rows of the permuted buffers for T tokens: T*k + E*(kRowAlign-1), rounded up to kRowAlign
 inline int64_t perm_rows(int64_t T, int k, int E) {
-  return ((T * k + (int64_t)E * (kTileM - 1)) + kTileM - 1) / kTileM * kTileM;
+  return ((T * k + (int64_t)E * (kRowAlign - 1)) + kRowAlign - 1) / kRowAlign * kRowAlign;
 }
 // CUDA-core reference path (debug / sanitizer): SwiGLU GEMM1 and plain GEMM2.
 void launch_gemm1_simt(const GroupedArgs& g, const bf16* xperm, const uint8_t* layer, size_t expert_bytes,

@@ -78,13 +78,13 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
   for (int i = tid; i < E; i += SCAN_THREADS) tot[i] = ((volatile int32_t*)counts)[i];
   __syncthreads();
   if (tid == 0) {
-    int32_t ts = 0;  // expert row ranges padded to kTileM: offsets[e] = kTileM * tile_start[e]
+    int32_t ts = 0;  // expert row ranges padded to kRowAlign: offsets[e] = kRowAlign * tile_start[e]
     for (int i = 0; i < E; ++i) {
-      offsets[i] = ts * kTileM;
+      offsets[i] = ts * kRowAlign;
       tile_start[i] = ts;
-      ts += (tot[i] + kTileM - 1) / kTileM;
+      ts += (tot[i] + kRowAlign - 1) / kRowAlign;
     }
-    offsets[E] = ts * kTileM;
+    offsets[E] = ts * kRowAlign;
     tile_start[E] = ts;
     *done = 0;  // re-arm for the next forward (stream-ordered)
   }
