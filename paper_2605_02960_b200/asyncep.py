@@ -24,6 +24,7 @@ FLAG_IDENTITY_EXPERTS = 0x1
 FLAG_SIMT_GEMM = 0x2
 FLAG_STAGE_TIMING = 0x4
 FLAG_SIMT_ROUTER = 0x8
+FLAG_GATHER_A = 0x10
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 
 

@@ -387,8 +387,15 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
   // (2) permute / dispatch
   aep::launch_perm_hist(ids, T, k, E, blk, st);
-  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), st);
-  aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok, xperm, st);
+  // X_perm is materialised unless GEMM1 gathers the token rows itself (ASYNCEP_FLAG_GATHER_A:
+  // TMA gather4 through src_tok -- correct, but measured 2.5x slower than the tiled loads
+  // because gather4 issue throughput caps at ~512 B per ~70 cycles per SM).
+  const bool gather_a = (cf.flags & ASYNCEP_FLAG_GATHER_A) &&
+                        !(cf.flags & (ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM));
+  const bool materialise = !gather_a;
+  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
+  aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok,
+                           materialise ? xperm : nullptr, st);
   c->launches += 3;
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
   // wait for this layer's gathered experts (placed just before GEMM1 so router and
@@ -408,7 +415,9 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     aep::launch_gemm2_simt(g, act, wl, c->expert_bytes, H, h, yperm, st);
     c->launches += 2;
   } else {
-    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, c->num_sms, st);
+    if (!aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const bf16*)x : nullptr, T, src_tok,
+                              c->num_sms, st))
+      return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (gather map)");
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st);
     c->launches += 2;

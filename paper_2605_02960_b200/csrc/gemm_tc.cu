@@ -26,6 +26,7 @@
 // tile_start (permute scan; expert rows padded to 256), no host sync.  Every output tile
 // is produced by one CTA (pair) in a fixed K order: bitwise deterministic results that do
 // not depend on the grid size.
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -34,6 +35,10 @@
 namespace aep {
 
 namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
 constexpr int BM = kTileM;          // 128 rows per CTA (per-CTA UMMA M slice)
 constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
 constexpr int NTHREADS = 256;
@@ -59,11 +64,30 @@ struct TcArgs {
   int BN;       // N tile (multiple of 16*NCTA, <= 256); each CTA loads BN/NCTA rows of B
   int n_tiles;  // N tiles per row tile
   int n_out;    // output columns
+  int ts_scale; // row tiles (of 128*NCTA rows) per tile_start unit (kRowAlign rows)
+  int raster;   // 0: row-tile-major order; G > 0: groups of G row tiles walked row-first
+  int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first
+  const int32_t* gather_rows;  // non-null: A rows are gathered from the token matrix (map_a is a
+                               // {H, T} gather4 map) with row ids gather_rows[permuted row]
   // router epilogue
   int top_k, norm_topk;
   int32_t* ids;
   float* w;
 };
+
+// linear tile index -> (row tile, n tile)
+__device__ __forceinline__ void decode_tile(int t, int n_tiles, int total_rt, int raster, int& mt, int& nt) {
+  if (raster <= 0) {
+    mt = t / n_tiles;
+    nt = t - mt * n_tiles;
+  } else {
+    const int gsz = raster * n_tiles;
+    const int g = t / gsz, r = t - g * gsz;
+    const int rows = min(raster, total_rt - g * raster);
+    mt = g * raster + r % rows;
+    nt = r / rows;
+  }
+}
 
 __device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
   int lo = 0, hi = E - 1;  // largest e with ts[e] <= mt (skips empty experts)
@@ -178,7 +202,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       s_ts[1] = (p.dense_rows + TM - 1) / TM;
     }
   } else {
-    for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i];
+    for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i] * p.ts_scale;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
@@ -202,32 +226,47 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (NCTA == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int total = s_ts[G] * p.n_tiles;
+  const int total_rt = s_ts[G];
+  const int total = total_rt * p.n_tiles;
   const int nkb = p.K / BK;
   const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
 
   if (warp == 0) {
-    if (lane == 0) {
-      const uint64_t pol_b = policy_evict_last();
+    // Producer warp.  Lane 0 arms the barriers and loads B (and A when it is a dense 2-D
+    // tile); with a gathered A every lane issues one gather4 of 4 of the tile's 128 rows.
+    const bool gather = p.gather_rows != nullptr;
+    if (gather || lane == 0) {
       const uint32_t tx = (uint32_t)NCTA * ((uint32_t)A_BYTES + (uint32_t)bn_cta * BK * 2);
+      const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit; t < total; t += nunits) {
-        const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+        int mt, nt;
+        decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
         const int e = find_expert(s_ts, G, mt);
         const int row0 = mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
+        int4 rows = make_int4(0, 0, 0, 0);
+        if (gather) rows = reinterpret_cast<const int4*>(p.gather_rows + row0)[lane];  // rows 4*lane..+3
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (NCTA == 2) {
-            if (leader) mbar_arrive_expect_tx(&full[stage], tx);
-            else mbar_arrive_cluster_relaxed(&full[stage], 0);
-            tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
-            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], tx);
-            tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0);
-            tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (NCTA == 2) {
+              if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+              else mbar_arrive_cluster_relaxed(&full[stage], 0);
+              if (!gather) tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0, pol_a);
+              tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+            } else {
+              mbar_arrive_expect_tx(&full[stage], tx);
+              if (!gather) tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0, pol_a);
+              tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+            }
+          }
+          if (gather) {
+            __syncwarp();  // the stage is free and armed
+            uint8_t* dst = sA + stage * A_BYTES + lane * 4 * 128;
+            if (NCTA == 2) tma_gather4_pair(dst, &map_a, &full[stage], kb * BK, rows);
+            else tma_gather4(dst, &map_a, &full[stage], kb * BK, rows);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -276,7 +315,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = unit; t < total; t += nunits) {
-      const int mt = t / p.n_tiles, nt = t - mt * p.n_tiles;
+      int mt, nt;
+      decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
       const int wrow0 = mt * TM + (int)rank * BM + ew * 32;  // first row of this warp's slice
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -366,11 +406,21 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA>, ma, mb, mo, a);
 }
 
-// grouped GEMMs run as CTA pairs
-constexpr int kGroupedNCTA = kRowAlign / kTileM;
+// Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
+// kernel and ASYNCEP_GEMM_RASTER=G a grouped rasterisation (A/B experiments only).
+int grouped_ncta() {
+  static const int n = env_int("ASYNCEP_GEMM_NCTA", 2) == 1 ? 1 : 2;
+  return n;
+}
+int grouped_raster() {
+  static const int r = env_int("ASYNCEP_GEMM_RASTER", 0);
+  return r;
+}
 
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
-                    int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s) {
+                    int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
+                    const int32_t* gather_rows = nullptr) {
+  const int ncta = grouped_ncta();
   TcArgs a{};
   a.tile_start = g.tile_start;
   a.E = g.E;
@@ -378,11 +428,21 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.BN = BN;
   a.n_tiles = n_tiles;
   a.n_out = n_out;
-  const int units = num_sms / kGroupedNCTA;
-  const int upper = g.max_m_tiles * n_tiles;  // row tiles (of kRowAlign rows) x n tiles
-  const int grid = kGroupedNCTA * (upper < units ? (upper > 0 ? upper : 1) : units);
-  if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, kGroupedNCTA>(a, ma, mb, mo, grid, s);
-  else launch_mode<EPI_PLAIN, kGroupedNCTA>(a, ma, mb, mo, grid, s);
+  a.ts_scale = kRowAlign / (kTileM * ncta);
+  a.raster = grouped_raster();
+  a.pol_a = env_int("ASYNCEP_POL_A", 0);
+  a.pol_b = env_int("ASYNCEP_POL_B", 1);
+  a.gather_rows = gather_rows;
+  const int units = num_sms / ncta;
+  const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
+  const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
+  if (ncta == 2) {
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s);
+    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s);
+  } else {
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 1>(a, ma, mb, mo, grid, s);
+    else launch_mode<EPI_PLAIN, 1>(a, ma, mb, mo, grid, s);
+  }
 }
 }  // namespace
 
@@ -425,7 +485,7 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
   {
     const uint64_t dims[3] = {(uint64_t)H, (uint64_t)(2 * h), (uint64_t)E};
     const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, (uint32_t)(256 / kGroupedNCTA), 1};
+    const uint32_t box[3] = {BK, (uint32_t)(256 / grouped_ncta()), 1};
     if (!encode_tmap(&m.wgu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, layer, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -434,7 +494,7 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
     const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * 2;
     const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};
     const uint64_t strides[2] = {(uint64_t)h * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, (uint32_t)(bn2 / kGroupedNCTA), 1};
+    const uint32_t box[3] = {BK, (uint32_t)(bn2 / grouped_ncta()), 1};
     if (!encode_tmap(&m.wd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wd, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
@@ -442,10 +502,22 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
   return true;
 }
 
-void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     int num_sms, cudaStream_t s) {
+bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
+                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s) {
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
-  launch_grouped(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
+  if (x_gather) {  // dispatch fused into the A load: gather token rows of x by src_tok
+    CUtensorMap map_x;
+    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
+    const uint64_t strides[1] = {(uint64_t)H * 2};
+    const uint32_t box[2] = {BK, 1};
+    if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x_gather, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    launch_grouped(g, map_x, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, src_tok);
+  } else {
+    launch_grouped(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
+  }
+  return true;
 }
 
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
@@ -481,6 +553,7 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
   a.K = H;
   a.BN = rt.E_pad;
   a.n_tiles = 1;
+  a.ts_scale = 1;
   a.top_k = k;
   a.norm_topk = norm_topk;
   a.ids = ids;
@@ -515,9 +588,13 @@ bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const vo
     es[i] = 1;
     if (i + 1 < rank) st[i] = strides_bytes[i];
   }
+  static const int promo = env_int("ASYNCEP_L2_PROMO", 256);
+  const CUtensorMapL2promotion pr = promo == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                    : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                    : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   const CUresult r = fn(map, dtype, (cuuint32_t)rank, const_cast<void*>(base), d, st, b, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 

@@ -35,7 +35,8 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s);
 // blk_counts is [E][nblk]; `done` is a zero-initialised device counter (re-armed by the kernel).
 void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
-                      int32_t* counts, unsigned int* done, cudaStream_t s);
+                      int32_t* counts, unsigned int* done, int32_t* src_tok, cudaStream_t s);
+// xperm == nullptr: ranks / dest / src_tok only (the GEMM gathers the rows itself)
 void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, const int32_t* offsets,
                          int64_t T, int H, int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm,
                          cudaStream_t s);
@@ -77,8 +78,10 @@ struct ActMaps {
 bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2);
 bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h);
 int gemm2_bn(int H);
-void launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     int num_sms, cudaStream_t s);
+// x_gather != nullptr: A rows are gathered from x [T, H] through src_tok (TMA gather4),
+// i.e. the dispatch is fused into the GEMM and X_perm is never written.
+bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
+                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s);
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
                      int num_sms, cudaStream_t s);
 

@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
                                                                  int32_t* __restrict__ offsets,
                                                                  int32_t* __restrict__ tile_start,
                                                                  int32_t* __restrict__ counts,
-                                                                 unsigned int* __restrict__ done) {
+                                                                 unsigned int* __restrict__ done,
+                                                                 int32_t* __restrict__ src_tok) {
   __shared__ int32_t warp_tot[SCAN_THREADS / 32];
   __shared__ int32_t tot[kMaxExperts];
   __shared__ bool last;
@@ -88,6 +89,12 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
     tile_start[E] = ts;
     *done = 0;  // re-arm for the next forward (stream-ordered)
   }
+  __syncthreads();
+  // padding rows of every expert gather token 0 (their GEMM rows are never read)
+  for (int i = 0; i < E; ++i) {
+    const int32_t b = offsets[i] + tot[i], end = offsets[i + 1];
+    for (int r = b + tid; r < end; r += SCAN_THREADS) src_tok[r] = 0;
+  }
 }
 
 __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restrict__ x,
@@ -128,6 +135,7 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
       }
     }
   }
+  if (xperm == nullptr) return;
   __syncthreads();
   // copy: one warp per token, 16-B vectors, each x row read once and written k times
   for (int tl = warp; tl < tn; tl += blockDim.x / 32) {
@@ -156,8 +164,8 @@ void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_
 }
 
 void launch_perm_scan(int32_t* blk_counts, int nblk, int E, int32_t* offsets, int32_t* tile_start,
-                      int32_t* counts, unsigned int* done, cudaStream_t s) {
-  perm_scan_kernel<<<E, SCAN_THREADS, 0, s>>>(blk_counts, nblk, E, offsets, tile_start, counts, done);
+                      int32_t* counts, unsigned int* done, int32_t* src_tok, cudaStream_t s) {
+  perm_scan_kernel<<<E, SCAN_THREADS, 0, s>>>(blk_counts, nblk, E, offsets, tile_start, counts, done, src_tok);
 }
 
 void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_base, const int32_t* offsets,

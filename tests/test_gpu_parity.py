@@ -38,7 +38,8 @@ def test_synth_generator_is_bit_identical_on_cpu_and_gpu():
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
-@pytest.mark.parametrize("flags", [0, 2, 8, 10], ids=["tcgen05", "simt_gemm", "simt_router", "simt_all"])
+@pytest.mark.parametrize("flags", [0, 2, 8, 10, 16], ids=["tcgen05", "simt_gemm", "simt_router", "simt_all",
+                                                          "gather_a"])
 @pytest.mark.parametrize("T", [256, 1, 63, 1000])
 def test_tiny_layer_parity(flags, T):
     wl = Workload(**TINY, seed=1)
