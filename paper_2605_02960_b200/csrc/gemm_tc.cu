@@ -54,7 +54,7 @@ struct Cfg {
                                  (kMaxExperts + 1) * sizeof(int32_t);
 };
 
-enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2 };
+enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
 
 struct TcArgs {
   const int32_t* tile_start;  // grouped mode: [E+1] prefix of row tiles (rows padded to 128*NCTA)
@@ -98,30 +98,37 @@ __device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
   return lo;
 }
 
-// Router epilogue, one thread = one token row of the logits tile (E <= 256 columns in
-// TMEM): running top-k in registers (descending logit, ties -> lower expert id, R2), then
-// w_j = softmax over the k selected logits (norm_topk, R1) or the full-E softmax entry.
+// Router epilogue, one thread = one token row of the logits tile (E <= 256 fp32 columns
+// in TMEM): a running top-KMAX list in registers (KMAX >= k), fed 8 columns at a time.
+// Logits arrive in increasing expert id, so a strict '>' keeps equal logits in id order
+// (ties -> lower expert id, R2); most columns fail the one-compare rejection test against
+// the current KMAX-th value and never touch the insertion network (compact code: the
+// fully unrolled version thrashed the instruction cache).  Weights: softmax over the k
+// selected logits (norm_topk, R1) or the full-E softmax entry (second TMEM pass).
+template <int KMAX>
 __device__ __forceinline__ void router_epilogue(uint32_t tb, int E, int k, int norm_topk, bool valid,
                                                 int32_t* ids, float* w) {
-  float tv[kMaxTopK];
-  int ti[kMaxTopK];
+  float tv[KMAX];
+  int ti[KMAX];
 #pragma unroll
-  for (int j = 0; j < kMaxTopK; ++j) { tv[j] = -INFINITY; ti[j] = 0x7fffffff; }
-  for (int c0 = 0; c0 < E; c0 += 32) {
-    uint32_t r[32];
-    tmem_ld32(tb + c0, r);
+  for (int j = 0; j < KMAX; ++j) { tv[j] = -INFINITY; ti[j] = 0; }
+#pragma unroll 1
+  for (int c0 = 0; c0 < E; c0 += 8) {
+    uint32_t r[8];
+    tmem_ld8(tb + c0, r);
     tmem_ld_wait();
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < 8; ++i) {
       float v = __uint_as_float(r[i]);
-      int e = c0 + i;
-      if (e >= E) break;
+      if (c0 + i < E && v > tv[KMAX - 1]) {
+        int e = c0 + i;
 #pragma unroll
-      for (int j = 0; j < kMaxTopK; ++j) {
-        if (j < k && (v > tv[j] || (v == tv[j] && e < ti[j]))) {
-          const float sv = tv[j];
-          const int se = ti[j];
-          tv[j] = v; ti[j] = e; v = sv; e = se;
+        for (int j = 0; j < KMAX; ++j) {
+          if (v > tv[j]) {
+            const float sv = tv[j];
+            const int se = ti[j];
+            tv[j] = v; ti[j] = e; v = sv; e = se;
+          }
         }
       }
     }
@@ -130,21 +137,22 @@ __device__ __forceinline__ void router_epilogue(uint32_t tb, int E, int k, int n
   const float ref = tv[0];
   if (norm_topk) {
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j)
+    for (int j = 0; j < KMAX; ++j)
       if (j < k) denom += expf(tv[j] - ref);
   } else {
-    for (int c0 = 0; c0 < E; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tb + c0, r);
+#pragma unroll 1
+    for (int c0 = 0; c0 < E; c0 += 8) {
+      uint32_t r[8];
+      tmem_ld8(tb + c0, r);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
+      for (int i = 0; i < 8; ++i)
         if (c0 + i < E) denom += expf(__uint_as_float(r[i]) - ref);
     }
   }
   if (valid) {
 #pragma unroll
-    for (int j = 0; j < kMaxTopK; ++j)
+    for (int j = 0; j < KMAX; ++j)
       if (j < k) {
         ids[j] = ti[j];
         w[j] = expf(tv[j] - ref) / denom;
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
-    if (MODE != EPI_ROUTER) tma_prefetch_desc(&map_out);
+    if (MODE == EPI_PLAIN || MODE == EPI_SWIGLU) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], NCTA);  // leader: own expect_tx arrive + peer's arrive
       mbar_init(&empty[s], 1);
@@ -321,10 +329,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
-      if (MODE == EPI_ROUTER) {
+      if (MODE == EPI_ROUTER || MODE == EPI_ROUTER16) {
         const int row = wrow0 + lane;
-        router_epilogue(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows, p.ids + (int64_t)row * p.top_k,
-                        p.w + (int64_t)row * p.top_k);
+        router_epilogue<MODE == EPI_ROUTER ? 8 : 16>(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows,
+                                                     p.ids + (int64_t)row * p.top_k, p.w + (int64_t)row * p.top_k);
       } else if (MODE == EPI_SWIGLU) {
         // accumulator columns [0,128) = gate, [128,256) = up of act columns nt*128 + [0,128)
 #pragma unroll 1
@@ -371,7 +379,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (MODE != EPI_ROUTER && lane == 0) bulk_wait0();  // all stores of this warp complete
+    if ((MODE == EPI_PLAIN || MODE == EPI_SWIGLU) && lane == 0) bulk_wait0();  // this warp's stores done
     __syncwarp();
   }
   tc_fence_before();
@@ -559,7 +567,8 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
   a.ids = ids;
   a.w = w;
   const int tiles = (int)((T + BM - 1) / BM);
-  launch_mode<EPI_ROUTER, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
+  if (k <= 8) launch_mode<EPI_ROUTER, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
+  else launch_mode<EPI_ROUTER16, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
   return true;
 }
 
