@@ -14,6 +14,7 @@ from __future__ import annotations
 import torch
 
 from . import asyncep as A
+from .schedule import layer_resident, shard_range, stack_schedule
 
 
 class MoEStack:
@@ -33,10 +34,9 @@ class MoEStack:
         self.expert_bytes = ebytes
         self.router_w = [router_fn(l).to(self.device, torch.bfloat16).contiguous() for l in range(L)]
         self.shards = []
-        per = E // world_size
         for l in range(L):
-            full = world_size == 1 or (l == 0 and replicate_layer0)
-            ex = range(E) if full else range(rank * per, (rank + 1) * per)
+            full = layer_resident(l, world_size, replicate_layer0)
+            ex = range(E) if full else shard_range(E, world_size, rank)
             buf = torch.empty(len(ex) * ebytes, dtype=torch.uint8, device=self.device)
             for c0 in range(0, len(ex), pack_chunk):
                 sub = ex[c0:c0 + pack_chunk]
@@ -58,7 +58,7 @@ class MoEStack:
         self._bufs = None
 
     def layer_resident(self, l: int) -> bool:
-        return self.N == 1 or (l == 0 and bool(self.cfg.replicate_layer0))
+        return layer_resident(l, self.N, bool(self.cfg.replicate_layer0))
 
     def prefetch(self, l: int, local_shards=None) -> None:
         if local_shards is not None:
@@ -80,11 +80,10 @@ class MoEStack:
             self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
                           for _ in range(2)]
         cur = x
-        if not self.layer_resident(0):
-            self.prefetch(0, local_shards)
-        for l in range(self.L):
-            if l + 1 < self.L:
-                self.prefetch(l + 1, local_shards)  # gather of layer l+1 overlaps layer l
+        for op, l, _slot in stack_schedule(self.L, self.N, bool(self.cfg.replicate_layer0)):
+            if op == "prefetch":
+                self.prefetch(l, local_shards)  # gather of layer l overlaps layer l-1
+                continue
             if record is not None:
                 record(l, cur)
             dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
