@@ -47,13 +47,15 @@ def _load():
             I64, I32, D = ctypes.c_int64, ctypes.c_int, ctypes.c_double
             lib.oracle_router.argtypes = [P, P, I64, I32, I32, I32, I32, P, P, P, P, P, P]
             lib.oracle_router.restype = I32
-            lib.oracle_moe_layer.argtypes = [P, P, P, P, P, I64, I32, I32, I32, I32, I32, I32, I32,
+            lib.oracle_moe_layer.argtypes = [P, P, P, P, P, I64, I32, I32, I32, I32, I32, I32, I32, I32,
                                              P, P, P, P, P, P]
             lib.oracle_moe_layer.restype = I32
             lib.oracle_e4m3_decode.argtypes = [ctypes.c_uint8]
             lib.oracle_e4m3_decode.restype = D
             lib.oracle_e4m3_encode.argtypes = [D]
             lib.oracle_e4m3_encode.restype = ctypes.c_uint8
+            lib.oracle_e4m3_encode_fast.argtypes = [D]
+            lib.oracle_e4m3_encode_fast.restype = ctypes.c_uint8
             lib.oracle_e4m3_decode_array.argtypes = [P, I64, P]
             lib.oracle_e4m3_decode_array.restype = None
             lib.oracle_eq1_threshold.argtypes = [D, D, D]
@@ -112,11 +114,13 @@ def router(x, wr, k: int, norm_topk: bool = True, ids_in=None):
 
 
 def moe_layer(x, wr, wg, wu, wd, k: int, norm_topk: bool = True, residual: bool = True,
-              identity_experts: bool = False, ids_in=None):
+              identity_experts: bool = False, ids_in=None, act_quant: bool = False):
     """One MoE FFN layer by definition (R1-R5, R9, R15).
 
     x [T,H]; wr [E,H]; wg, wu [E,h,H]; wd [E,H,h] (natural layout, fp32 holding exact
-    bf16/e4m3-dequantised values).  Returns dict(y [T,H] f64, ids, w, logits, gap).
+    bf16/e4m3-dequantised values).  act_quant emulates the FP8 path's activation
+    quantisation (R6: per-token e4m3 x, bf16 then per-row e4m3 intermediate).
+    Returns dict(y [T,H] f64, ids, w, logits, gap).
     """
     x, wr = _f32(x), _f32(wr)
     T, H = x.shape
@@ -138,7 +142,7 @@ def moe_layer(x, wr, wg, wu, wd, k: int, norm_topk: bool = True, residual: bool 
         ids_in = np.ascontiguousarray(ids_in, dtype=np.int32)
     rc = _load().oracle_moe_layer(_ptr(x), _ptr(wr), wg_p, wu_p, wd_p, T, H, E, k, h,
                                   int(norm_topk), int(residual), int(identity_experts),
-                                  _ptr(ids_in), _ptr(y), _ptr(ids), _ptr(w), _ptr(logits), _ptr(gap))
+                                  int(act_quant), _ptr(ids_in), _ptr(y), _ptr(ids), _ptr(w), _ptr(logits), _ptr(gap))
     if rc:
         raise ValueError(f"oracle_moe_layer rc={rc}")
     return dict(y=y, ids=ids, w=w, logits=logits, gap=gap)
@@ -159,6 +163,11 @@ def e4m3_decode_one(b: int) -> float:
 def e4m3_encode_one(v: float) -> int:
     """RNE satfinite encode by brute-force nearest search (R6)."""
     return int(_load().oracle_e4m3_encode(float(v)))
+
+
+def e4m3_encode_fast_one(v: float) -> int:
+    """The arithmetic RNE satfinite encoder the emulation mode uses."""
+    return int(_load().oracle_e4m3_encode_fast(float(v)))
 
 
 def eq1_threshold(t_ep: float, f_gpu: float, gamma: float) -> float:

@@ -159,8 +159,11 @@ int oracle_router(const float *x, const float *wr, int64_t T, int H, int E, int 
  * identity != 0 replaces the MLP with o = x (test hook for the plumbing pin).
  */
 #define NB 32
+static void quant_row_e4m3(const float *v, int n, double *out);
+static float to_bf16(double v);
+
 static void expert_block(const float *wg, const float *wu, const float *wd, int H, int h, int nb,
-                         const double *xt, double *at, double *out, int identity) {
+                         const double *xt, double *at, double *out, int identity, int act_quant) {
     if (identity) {
         for (int b = 0; b < nb; ++b)
             for (int i = 0; i < H; ++i) out[(size_t)b * H + i] = xt[(size_t)i * NB + b];
@@ -176,6 +179,16 @@ static void expert_block(const float *wg, const float *wu, const float *wd, int 
             for (int b = 0; b < NB; ++b) { g[b] += cg * xi[b]; u[b] += cu * xi[b]; }
         }
         for (int b = 0; b < NB; ++b) at[(size_t)r * NB + b] = silu(g[b]) * u[b];
+    }
+    if (act_quant) {  /* emulate the GPU: intermediate -> bf16 -> per-row e4m3 (R5, R6) */
+        float *row = (float *)malloc(sizeof(float) * (size_t)h);
+        double *dq = (double *)malloc(sizeof(double) * (size_t)h);
+        for (int b = 0; b < nb; ++b) {
+            for (int r = 0; r < h; ++r) row[r] = to_bf16(at[(size_t)r * NB + b]);
+            quant_row_e4m3(row, h, dq);
+            for (int r = 0; r < h; ++r) at[(size_t)r * NB + b] = dq[r];
+        }
+        free(row); free(dq);
     }
     double o[NB];
     for (int r = 0; r < H; ++r) {
@@ -202,8 +215,8 @@ static void expert_block(const float *wg, const float *wu, const float *wd, int 
  */
 int oracle_moe_layer(const float *x, const float *wr, const float *wg, const float *wu,
                      const float *wd, int64_t T, int H, int E, int k, int h, int norm_topk,
-                     int add_residual, int identity_experts, const int32_t *ids_in, double *y,
-                     int32_t *ids_out, double *w_out, double *logits, double *gap) {
+                     int add_residual, int identity_experts, int act_quant, const int32_t *ids_in,
+                     double *y, int32_t *ids_out, double *w_out, double *logits, double *gap) {
     if (T < 0 || H <= 0 || E <= 0 || k <= 0 || k > E || h <= 0 || !x || !wr || !y) return ORACLE_EINVAL;
     if (!identity_experts && (!wg || !wu || !wd)) return ORACLE_EINVAL;
     if (T == 0) return ORACLE_OK;
@@ -245,7 +258,8 @@ int oracle_moe_layer(const float *x, const float *wr, const float *wg, const flo
             double *xt = (double *)malloc(sizeof(double) * (size_t)H * NB);
             double *at = (double *)malloc(sizeof(double) * (size_t)h * NB);
             double *ob = (double *)malloc(sizeof(double) * (size_t)H * NB);
-            if (!xt || !at || !ob) {
+            double *xq = (double *)malloc(sizeof(double) * (size_t)H);
+            if (!xt || !at || !ob || !xq) {
 #pragma omp atomic write
                 err = 1;
             } else {
@@ -256,18 +270,23 @@ int oracle_moe_layer(const float *x, const float *wr, const float *wg, const flo
                     const int nb = (int)((cnt[e + 1] - s0) < NB ? (cnt[e + 1] - s0) : NB);
                     for (int b = 0; b < NB; ++b) {
                         const int64_t t = (b < nb) ? lst[s0 + b] / k : -1;
-                        for (int i = 0; i < H; ++i)
-                            xt[(size_t)i * NB + b] = (t >= 0) ? (double)x[(size_t)t * H + i] : 0.0;
+                        if (t >= 0 && act_quant) {  /* the experts see the e4m3-quantised token (R6) */
+                            quant_row_e4m3(x + (size_t)t * H, H, xq);
+                            for (int i = 0; i < H; ++i) xt[(size_t)i * NB + b] = xq[i];
+                        } else {
+                            for (int i = 0; i < H; ++i)
+                                xt[(size_t)i * NB + b] = (t >= 0) ? (double)x[(size_t)t * H + i] : 0.0;
+                        }
                     }
                     expert_block(identity_experts ? NULL : wg + (size_t)e * h * H,
                                  identity_experts ? NULL : wu + (size_t)e * h * H,
                                  identity_experts ? NULL : wd + (size_t)e * H * h, H, h, nb, xt, at,
-                                 ob, identity_experts);
+                                 ob, identity_experts, act_quant);
                     for (int b = 0; b < nb; ++b)
                         memcpy(o + (size_t)lst[s0 + b] * H, ob + (size_t)b * H, sizeof(double) * (size_t)H);
                 }
             }
-            free(xt); free(at); free(ob);
+            free(xt); free(at); free(ob); free(xq);
         }
         free(item_e); free(item_s);
         if (err) { rc = ORACLE_ENOMEM; goto done; }
@@ -324,6 +343,69 @@ uint8_t oracle_e4m3_encode(double v) {
         if (d < bestd || (d == bestd && (c & 1) == 0 && (best & 1) == 1)) { bestd = d; best = c; }
     }
     return (uint8_t)(best | (neg << 7));
+}
+
+/*
+ * The same encoder computed arithmetically (pinned against oracle_e4m3_encode by an
+ * exhaustive test): |v| = m * 2^e; normal codes carry 3 mantissa bits, subnormals are
+ * multiples of 2^-9; round half to even; saturate at 448.
+ */
+uint8_t oracle_e4m3_encode_fast(double v) {
+    if (isnan(v)) return 0x7F;
+    const int neg = signbit(v) ? 1 : 0;
+    double a = fabs(v);
+    int code;
+    if (a >= 448.0) {
+        code = 0x7E;
+    } else if (a < ldexp(1.0, -6)) {                 /* subnormal range: step 2^-9 */
+        double q = a / ldexp(1.0, -9);
+        double f = floor(q);
+        double r = q - f;
+        int m = (int)f;
+        if (r > 0.5 || (r == 0.5 && (m & 1))) m += 1;  /* m == 8 is the smallest normal, code 0x08 */
+        code = m;
+    } else {
+        int ex;
+        double fr = frexp(a, &ex);                    /* a = fr * 2^ex, fr in [0.5, 1) */
+        int e = ex - 1;                               /* a = (2 fr) * 2^e, 2fr in [1, 2) */
+        double q = (2.0 * fr - 1.0) * 8.0;            /* mantissa in units of 1/8 */
+        double f = floor(q);
+        double r = q - f;
+        int m = (int)f;
+        if (r > 0.5 || (r == 0.5 && (m & 1))) m += 1;
+        if (m == 8) { m = 0; e += 1; }
+        code = ((e + 7) << 3) | m;
+        if (code > 0x7E) code = 0x7E;
+    }
+    return (uint8_t)(code | (neg << 7));
+}
+
+/* bf16 round-to-nearest-even of a double (via float), as the GPU stores the intermediate (R5) */
+static float to_bf16(double v) {
+    float f = (float)v;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u) return f;  /* inf / nan */
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) & 0xFFFF0000u;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+/*
+ * FP8 activation-quantisation emulation (reading R6, the rule the CUDA path applies):
+ *   amax = max_i |v_i| (fp32); inv = 448 / amax (fp32); q_i = RNE_satfinite_e4m3(fp32(v_i * inv));
+ *   result_i = decode(q_i) * (amax / 448) (fp32 scale, product in fp64)
+ */
+static void quant_row_e4m3(const float *v, int n, double *out) {
+    float amax = 0.f;
+    for (int i = 0; i < n; ++i) { const float a = fabsf(v[i]); if (a > amax) amax = a; }
+    if (amax == 0.f) { for (int i = 0; i < n; ++i) out[i] = 0.0; return; }
+    const float inv = 448.0f / amax;
+    const float sc = amax / 448.0f;
+    for (int i = 0; i < n; ++i) {
+        const float p = v[i] * inv;
+        out[i] = oracle_e4m3_decode(oracle_e4m3_encode_fast((double)p)) * (double)sc;
+    }
 }
 
 /* ---------------- Saturation threshold, Eq. 1 ---------------- */

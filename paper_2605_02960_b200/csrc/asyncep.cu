@@ -61,6 +61,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
   size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, xperm, act, total;
+  size_t xq, xscale, amax, aq, ascale;  // FP8 experts only
 };
 WsLayout ws_layout(const asyncep_config& c) {
   WsLayout L{};
@@ -85,6 +86,13 @@ WsLayout ws_layout(const asyncep_config& c) {
   L.done = take(4);
   L.xperm = take(Rp * (size_t)c.hidden * 2);  // X_perm, reused as Y_perm after GEMM1
   L.act = take(Rp * (size_t)c.ffn * 2);
+  if (c.expert_dtype == ASYNCEP_FP8_E4M3) {
+    L.xq = take(Rp * (size_t)c.hidden);
+    L.xscale = take(Rp * 4);
+    L.amax = take(Rp * 4);
+    L.aq = take(Rp * (size_t)c.ffn);
+    L.ascale = take(Rp * 4);
+  }
   L.total = o;
   return L;
 }
@@ -100,8 +108,12 @@ asyncep_status check_config(const asyncep_config* c) {
   if (c->hidden >= 256 && c->hidden % 256)
     return fail(ASYNCEP_ERR_INVALID_ARG, "hidden >= 256 must be a multiple of 256");
   if (c->ffn <= 0 || c->ffn % 128) return fail(ASYNCEP_ERR_INVALID_ARG, "ffn must be a multiple of 128");
-  if (c->expert_dtype != ASYNCEP_BF16)
+  if (c->expert_dtype != ASYNCEP_BF16 && c->expert_dtype != ASYNCEP_FP8_E4M3)
     return fail(ASYNCEP_ERR_UNSUPPORTED, "expert_dtype %d not supported by this build", c->expert_dtype);
+  if (c->expert_dtype == ASYNCEP_FP8_E4M3 && (c->flags & ASYNCEP_FLAG_SIMT_GEMM))
+    return fail(ASYNCEP_ERR_UNSUPPORTED, "the SIMT reference GEMM is BF16 only");
+  if (c->expert_dtype == ASYNCEP_FP8_E4M3 && c->hidden < 256)
+    return fail(ASYNCEP_ERR_UNSUPPORTED, "FP8 experts need hidden >= 256");
   if (c->world_size <= 0 || c->rank < 0 || c->rank >= c->world_size)
     return fail(ASYNCEP_ERR_INVALID_ARG, "bad world_size/rank");
   if (c->num_experts % c->world_size)
@@ -179,6 +191,8 @@ const char* asyncep_last_error(void) { return g_last_error.c_str(); }
 
 size_t asyncep_expert_bytes(const asyncep_config* c) {
   if (!c) return 0;
+  if (c->expert_dtype == ASYNCEP_FP8_E4M3)  // codes + per-row fp32 scales of W_gu (2h) and W_down (H)
+    return (size_t)3 * c->hidden * c->ffn + (size_t)(2 * c->ffn + c->hidden) * 4;
   return (size_t)3 * c->hidden * c->ffn * 2;
 }
 size_t asyncep_slot_bytes(const asyncep_config* c) {
@@ -200,11 +214,17 @@ asyncep_status asyncep_pack_experts(const asyncep_config* cfg, int32_t count, co
   if (count < 0 || count > cfg->num_experts) return fail(ASYNCEP_ERR_INVALID_ARG, "bad expert count");
   if (count == 0) return ASYNCEP_OK;
   if (!gate || !up || !down || !out) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
-  if (gs || us || ds) return fail(ASYNCEP_ERR_INVALID_ARG, "scales must be NULL for BF16");
   if (((uintptr_t)gate | (uintptr_t)up | (uintptr_t)down | (uintptr_t)out) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "pointers must be 16-B aligned");
-  aep::launch_pack_bf16((const bf16*)gate, (const bf16*)up, (const bf16*)down, count, cfg->hidden, cfg->ffn,
-                        asyncep_expert_bytes(cfg), (uint8_t*)out, (cudaStream_t)stream);
+  if (cfg->expert_dtype == ASYNCEP_FP8_E4M3) {
+    if (!gs || !us || !ds) return fail(ASYNCEP_ERR_INVALID_ARG, "FP8 packing needs the three scale arrays");
+    aep::launch_pack_fp8((const uint8_t*)gate, (const uint8_t*)up, (const uint8_t*)down, gs, us, ds, count,
+                         cfg->hidden, cfg->ffn, asyncep_expert_bytes(cfg), (uint8_t*)out, (cudaStream_t)stream);
+  } else {
+    if (gs || us || ds) return fail(ASYNCEP_ERR_INVALID_ARG, "scales must be NULL for BF16");
+    aep::launch_pack_bf16((const bf16*)gate, (const bf16*)up, (const bf16*)down, count, cfg->hidden, cfg->ffn,
+                          asyncep_expert_bytes(cfg), (uint8_t*)out, (cudaStream_t)stream);
+  }
   CUDA_TRY(cudaGetLastError());
   return ASYNCEP_OK;
 }
@@ -263,12 +283,15 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
         cudaEventCreateWithFlags(&c->slot_free[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(ASYNCEP_ERR_CUDA, "cudaEventCreate failed"));
   }
-  if (cudaMemsetAsync(c->ws + c->L.done, 0, 4, c->cs) != cudaSuccess)
+  const bool fp8 = cfg->expert_dtype == ASYNCEP_FP8_E4M3;
+  const int64_t Rp = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
+  if (cudaMemsetAsync(c->ws + c->L.done, 0, 4, c->cs) != cudaSuccess ||
+      (fp8 && cudaMemsetAsync(c->ws + c->L.amax, 0, (size_t)Rp * 4, c->cs) != cudaSuccess))
     return bail(fail(ASYNCEP_ERR_CUDA, "cudaMemsetAsync failed"));
   // TMA descriptors: activations (fixed workspace addresses), each resident layer, both slots.
   const int64_t R = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
   if (!aep::make_act_maps(c->act_maps, (const bf16*)(c->ws + c->L.xperm), (const bf16*)(c->ws + c->L.act), R,
-                          cfg->hidden, cfg->ffn))
+                          cfg->hidden, cfg->ffn, fp8 ? c->ws + c->L.xq : nullptr, fp8 ? c->ws + c->L.aq : nullptr))
     return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
   c->layer_maps.resize(L);
   c->resident.assign(L, 0);
@@ -276,7 +299,7 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
     if (!layer_resident(c, l)) continue;
     c->resident[l] = 1;
     if (!aep::make_weight_maps(c->layer_maps[l], c->shard[l], c->expert_bytes, cfg->num_experts, cfg->hidden,
-                               cfg->ffn, c->act_maps.bn2))
+                               cfg->ffn, c->act_maps.bn2, fp8))
       return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l));
   }
   c->router_maps.resize(L);
@@ -285,7 +308,7 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
       return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router %d)", l));
   for (int i = 0; i < 2; ++i)
     if (c->slot[i] && !aep::make_weight_maps(c->slot_maps[i], c->slot[i], c->expert_bytes, cfg->num_experts,
-                                             cfg->hidden, cfg->ffn, c->act_maps.bn2))
+                                             cfg->hidden, cfg->ffn, c->act_maps.bn2, fp8))
       return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (slot %d)", i));
   *out = c;
   return ASYNCEP_OK;
@@ -390,13 +413,26 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // X_perm is materialised unless GEMM1 gathers the token rows itself (ASYNCEP_FLAG_GATHER_A:
   // TMA gather4 through src_tok -- correct, but measured 2.5x slower than the tiled loads
   // because gather4 issue throughput caps at ~512 B per ~70 cycles per SM).
-  const bool gather_a = (cf.flags & ASYNCEP_FLAG_GATHER_A) &&
+  const bool fp8 = cf.expert_dtype == ASYNCEP_FP8_E4M3;
+  const bool identity = (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) != 0;
+  const bool gather_a = (cf.flags & ASYNCEP_FLAG_GATHER_A) && !fp8 &&
                         !(cf.flags & (ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM));
-  const bool materialise = !gather_a;
+  const bool materialise = identity || (!gather_a && !fp8);
   aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
   aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok,
                            materialise ? xperm : nullptr, st);
   c->launches += 3;
+  aep::F8Args f8{};
+  if (fp8 && !identity) {  // per-token e4m3 quantisation of x into its permuted rows (R6)
+    f8.x_scale = (const float*)(ws + c->L.xscale);
+    f8.act_scale = (const float*)(ws + c->L.ascale);
+    f8.act_amax = (uint32_t*)(ws + c->L.amax);
+    f8.expert_bytes = c->expert_bytes;
+    f8.sgu_off = (size_t)3 * H * h;
+    f8.sd_off = f8.sgu_off + (size_t)2 * h * 4;
+    aep::launch_perm_quant((const bf16*)x, dest, T, H, k, ws + c->L.xq, (float*)(ws + c->L.xscale), st);
+    c->launches += 1;
+  }
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
   // wait for this layer's gathered experts (placed just before GEMM1 so router and
   // permute also overlap the gather tail)
@@ -414,6 +450,14 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_gemm2_simt(g, act, wl, c->expert_bytes, H, h, yperm, st);
     c->launches += 2;
+  } else if (fp8) {
+    f8.layer = wl;
+    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, nullptr, T, src_tok, c->num_sms, st, &f8);
+    aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
+                          (float*)(ws + c->L.ascale), st);
+    if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
+    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8);
+    c->launches += 3;
   } else {
     if (!aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const bf16*)x : nullptr, T, src_tok,
                               c->num_sms, st))

@@ -30,6 +30,13 @@ AEP_DEV uint32_t pack_bf16x2(float lo, float hi) {
 AEP_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 AEP_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
 
+// fp32 pair -> two OCP E4M3 codes (RNE, saturating to +-448), v0 in the low byte.
+AEP_DEV uint16_t e4m3x2(float v0, float v1) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(v1), "f"(v0));
+  return r;
+}
+
 // silu(z) = z * sigma(z) = z / (1 + e^-z)   (reading R4).  IEEE division, expf.
 AEP_DEV float silu_f(float z) { return z / (1.0f + __expf(-z)); }
 
@@ -246,6 +253,14 @@ AEP_DEV void tc_commit2_mc(uint64_t* bar, uint16_t mask) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
       "h"(mask)
+      : "memory");
+}
+AEP_DEV void mma_f8_2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
 AEP_DEV void mma_bf16_2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accum) {

@@ -67,6 +67,11 @@ struct TcArgs {
   int ts_scale; // row tiles (of 128*NCTA rows) per tile_start unit (kRowAlign rows)
   int raster;   // 0: row-tile-major order; G > 0: groups of G row tiles walked row-first
   int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first
+  // FP8 (kind::f8f6f4) scales: dequantised D[r][c] = acc * a_scale[r] * b_scale(e)[B row of c]
+  const float* a_scale;
+  const uint8_t* b_scale_base;  // layer base + offset of the scale block inside an expert blob
+  size_t expert_bytes;
+  uint32_t* amax_out;           // GEMM1 FP8: per-row max |act| (fp32 bits, atomicMax)
   const int32_t* gather_rows;  // non-null: A rows are gathered from the token matrix (map_a is a
                                // {H, T} gather4 map) with row ids gather_rows[permuted row]
   // router epilogue
@@ -179,7 +184,7 @@ __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t
   }
 }
 
-template <int MODE, int NCTA>
+template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
@@ -236,7 +241,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
   const int total_rt = s_ts[G];
   const int total = total_rt * p.n_tiles;
-  const int nkb = p.K / BK;
+  constexpr int KB_ELEMS = F8 ? 128 : BK;  // elements per 128-B k-block row
+  const int nkb = p.K / KB_ELEMS;
   const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
 
   if (warp == 0) {
@@ -262,12 +268,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (NCTA == 2) {
               if (leader) mbar_arrive_expect_tx(&full[stage], tx);
               else mbar_arrive_cluster_relaxed(&full[stage], 0);
-              if (!gather) tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0, pol_a);
-              tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+              if (!gather)
+                tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
             } else {
               mbar_arrive_expect_tx(&full[stage], tx);
-              if (!gather) tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * BK, row0, pol_a);
-              tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * BK, brow, e, pol_b);
+              if (!gather) tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
             }
           }
           if (gather) {
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      const uint32_t idesc = make_idesc(TM, p.BN, true);
+      const uint32_t idesc = make_idesc(TM, p.BN, !F8);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -298,13 +305,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
           const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES_MAX);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            if (NCTA == 2)
-              mma_bf16_2(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
-                         (kb | k) != 0 ? 1u : 0u);
-            else
-              mma_bf16(d, make_smem_desc_sw128(a0 + k * 32), make_smem_desc_sw128(b0 + k * 32), idesc,
-                       (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 B of K (16 bf16 / 32 e4m3) per 128-B k-block
+            const uint64_t ad = make_smem_desc_sw128(a0 + k * 32), bd = make_smem_desc_sw128(b0 + k * 32);
+            const uint32_t acc_on = (kb | k) != 0 ? 1u : 0u;
+            if (F8) {
+              if (NCTA == 2) mma_f8_2(d, ad, bd, idesc, acc_on);
+              else mma_f8(d, ad, bd, idesc, acc_on);
+            } else {
+              if (NCTA == 2) mma_bf16_2(d, ad, bd, idesc, acc_on);
+              else mma_bf16(d, ad, bd, idesc, acc_on);
+            }
           }
           if (NCTA == 2) tc_commit2_mc(&empty[stage], 0x3);
           else tc_commit(&empty[stage]);
@@ -335,6 +345,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                                      p.ids + (int64_t)row * p.top_k, p.w + (int64_t)row * p.top_k);
       } else if (MODE == EPI_SWIGLU) {
         // accumulator columns [0,128) = gate, [128,256) = up of act columns nt*128 + [0,128)
+        float sa = 1.f, amax = 0.f;
+        const float* sb = nullptr;
+        if (F8) {
+          sa = p.a_scale[wrow0 + lane];
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)find_expert(s_ts, G, mt) * p.expert_bytes) +
+               nt * 256;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 64) {
           uint32_t o[32];
@@ -346,14 +363,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const float a0 = silu_f(__uint_as_float(g[2 * i])) * __uint_as_float(u[2 * i]);
-              const float a1 = silu_f(__uint_as_float(g[2 * i + 1])) * __uint_as_float(u[2 * i + 1]);
-              o[16 * half + i] = pack_bf16x2(a0, a1);
+              float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+              float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+              if (F8) {
+                const int c = c0 + 32 * half + 2 * i;
+                g0 *= sa * __ldg(sb + c);
+                g1 *= sa * __ldg(sb + c + 1);
+                u0 *= sa * __ldg(sb + 128 + c);
+                u1 *= sa * __ldg(sb + 128 + c + 1);
+              }
+              const uint32_t pk = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+              o[16 * half + i] = pk;
+              if (F8) amax = fmaxf(amax, fmaxf(fabsf(bf16_lo(pk)), fabsf(bf16_hi(pk))));
             }
           }
           stage_and_store(o, stg, lane, &map_out, nt * 128 + c0, wrow0);
         }
+        if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
       } else {
+        float sa = 1.f;
+        const float* sb = nullptr;
+        if (F8) {
+          sa = p.a_scale[wrow0 + lane];
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)find_expert(s_ts, G, mt) * p.expert_bytes) +
+               nt * p.BN;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < p.BN; c0 += 64) {
           if (nt * p.BN + c0 >= p.n_out) break;
@@ -364,8 +398,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tmem_ld32(tb + c0 + 32 * half, r);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              o[16 * half + i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+            for (int i = 0; i < 16; ++i) {
+              float v0 = __uint_as_float(r[2 * i]), v1 = __uint_as_float(r[2 * i + 1]);
+              if (F8) {
+                const int c = c0 + 32 * half + 2 * i;
+                v0 *= sa * __ldg(sb + c);
+                v1 *= sa * __ldg(sb + c + 1);
+              }
+              o[16 * half + i] = pack_bf16x2(v0, v1);
+            }
           }
           stage_and_store(o, stg, lane, &map_out, nt * p.BN + c0, wrow0);
         }
@@ -391,12 +432,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-template <int MODE, int NCTA>
+template <int MODE, int NCTA, bool F8 = false>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
                  cudaStream_t s) {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)Cfg<NCTA>::SMEM);
   });
   cudaLaunchConfig_t cfg{};
@@ -411,7 +452,7 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA>, ma, mb, mo, a);
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, a);
 }
 
 // Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
@@ -427,8 +468,8 @@ int grouped_raster() {
 
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
-                    const int32_t* gather_rows = nullptr) {
-  const int ncta = grouped_ncta();
+                    const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false) {
+  const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
   a.tile_start = g.tile_start;
   a.E = g.E;
@@ -441,10 +482,19 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.pol_a = env_int("ASYNCEP_POL_A", 0);
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
   a.gather_rows = gather_rows;
+  if (f8) {
+    a.a_scale = gemm2 ? f8->act_scale : f8->x_scale;
+    a.b_scale_base = f8->layer + (gemm2 ? f8->sd_off : f8->sgu_off);
+    a.expert_bytes = f8->expert_bytes;
+    a.amax_out = gemm2 ? nullptr : f8->act_amax;
+  }
   const int units = num_sms / ncta;
   const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
   const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
-  if (ncta == 2) {
+  if (f8) {  // FP8 experts: CTA pairs only
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s);
+    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s);
+  } else if (ncta == 2) {
     if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s);
     else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s);
   } else {
@@ -456,8 +506,20 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
 
 int gemm2_bn(int H) { return H >= 256 ? 256 : H; }
 
-bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h) {
+bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h, const uint8_t* xq,
+                   const uint8_t* aq) {
   const uint32_t box[2] = {BK, BM};
+  if (xq && aq) {  // FP8 operands: 128 e4m3 = 128 B per k-block row
+    const uint32_t qbox[2] = {128, BM};
+    const uint64_t d1[2] = {(uint64_t)H, (uint64_t)R_max};
+    const uint64_t s1[1] = {(uint64_t)H};
+    if (!encode_tmap(&m.xq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, xq, d1, s1, qbox, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const uint64_t d2[2] = {(uint64_t)h, (uint64_t)R_max};
+    const uint64_t s2[1] = {(uint64_t)h};
+    if (!encode_tmap(&m.aq, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, aq, d2, s2, qbox, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
   {
     const uint64_t dims[2] = {(uint64_t)H, (uint64_t)R_max};
     const uint64_t strides[1] = {(uint64_t)H * 2};
@@ -489,29 +551,36 @@ bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max
   return true;
 }
 
-bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2) {
+bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2, bool fp8) {
+  const int b = fp8 ? 1 : 2;  // bytes per weight
+  const int ncta = fp8 ? 2 : grouped_ncta();
+  const CUtensorMapDataType dt = fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const uint32_t kb = 128 / b;  // elements per 128-B row of a k-block
   {
     const uint64_t dims[3] = {(uint64_t)H, (uint64_t)(2 * h), (uint64_t)E};
-    const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, (uint32_t)(256 / grouped_ncta()), 1};
-    if (!encode_tmap(&m.wgu, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, layer, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
+    const uint64_t strides[2] = {(uint64_t)H * b, (uint64_t)expert_bytes};
+    const uint32_t box[3] = {kb, (uint32_t)(256 / ncta), 1};
+    if (!encode_tmap(&m.wgu, dt, 3, layer, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
   {
-    const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * 2;
+    const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * b;
     const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};
-    const uint64_t strides[2] = {(uint64_t)h * 2, (uint64_t)expert_bytes};
-    const uint32_t box[3] = {BK, (uint32_t)(bn2 / grouped_ncta()), 1};
-    if (!encode_tmap(&m.wd, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wd, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
+    const uint64_t strides[2] = {(uint64_t)h * b, (uint64_t)expert_bytes};
+    const uint32_t box[3] = {kb, (uint32_t)(bn2 / ncta), 1};
+    if (!encode_tmap(&m.wd, dt, 3, wd, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
+  m.fp8 = fp8;
   return true;
 }
 
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s) {
+                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
+                     const F8Args* f8) {
+  if (f8) {
+    launch_grouped(g, am.xq, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, nullptr, f8,
+                   false);
+    return true;
+  }
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
   if (x_gather) {  // dispatch fused into the A load: gather token rows of x by src_tok
     CUtensorMap map_x;
@@ -529,9 +598,13 @@ bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
 }
 
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
-                     int num_sms, cudaStream_t s) {
+                     int num_sms, cudaStream_t s, const F8Args* f8) {
   const int bn = am.bn2;
-  launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
+  if (f8)
+    launch_grouped(g, am.aq, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s, nullptr, f8,
+                   true);
+  else
+    launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
 }
 
 // ------------------------------------------------------------------ router on tcgen05

@@ -41,6 +41,13 @@ void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_b
                          int64_t T, int H, int k, int E, int32_t* dest, int32_t* src_tok, bf16* xperm,
                          cudaStream_t s);
 
+// FP8 (R6): per-token e4m3 quantisation of x into its k permuted rows (after the scatter
+// computed dest), and per-row quantisation of the GEMM1 intermediate.
+void launch_perm_quant(const bf16* x, const int32_t* dest, int64_t T, int H, int k, uint8_t* xq, float* xscale,
+                       cudaStream_t s);
+void launch_act_quant(const bf16* act, uint32_t* act_amax, const int32_t* offsets, int E, int64_t R, int h,
+                      uint8_t* aq, float* ascale, cudaStream_t s);
+
 // Step (3): grouped expert GEMM.  Weights come from a packed layer (see asyncep.h):
 // per expert blob of expert_bytes; W_gu at blob offset 0 ([2h, H]), W_down at 2h*H*2.
 // Expert e's rows of X_perm / act / Y_perm are [offsets[e], offsets[e] + counts[e]);
@@ -65,33 +72,50 @@ void launch_gemm2_simt(const GroupedArgs& g, const bf16* act, const uint8_t* lay
 
 // tcgen05 path.  One set of TMA maps per weight source (resident layer or slot).
 struct GemmMaps {
-  CUtensorMap wgu;   // 3D {H, 2h, E} bf16, box {64, 256, 1}
-  CUtensorMap wd;    // 3D {h, H, E} bf16, box {64, BN2, 1}
+  CUtensorMap wgu;   // 3D {H, 2h, E}, box {128 B, 256/NCTA rows, 1}
+  CUtensorMap wd;    // 3D {h, H, E},  box {128 B, BN2/NCTA rows, 1}
+  bool fp8 = false;
+};
+// FP8 experts (R6): where the GEMMs find their scales.
+struct F8Args {
+  const float* x_scale;    // [R] per permuted row (per token), from the permute quantisation
+  const float* act_scale;  // [R] per row of the intermediate, from launch_act_quant
+  uint32_t* act_amax;      // [R] per-row max |act| accumulated by the GEMM1 epilogue
+  const uint8_t* layer;    // packed FP8 layer (E blobs)
+  size_t expert_bytes;
+  size_t sgu_off, sd_off;  // byte offsets of s_gu [2h] / s_down [H] inside a blob
 };
 struct ActMaps {
+  CUtensorMap xq;        // FP8: 2D {H, R_max} e4m3, box {128, 128}  (GEMM1 A)
+  CUtensorMap aq;        // FP8: 2D {h, R_max} e4m3, box {128, 128}  (GEMM2 A)
   CUtensorMap xperm;     // 2D {H, R_max}, box {64, 128}  (GEMM1 A)
   CUtensorMap act;       // 2D {h, R_max}, box {64, 128}  (GEMM2 A)
   CUtensorMap act_out;   // 2D {h, R_max}, box {64, 32}   (GEMM1 epilogue TMA store)
   CUtensorMap yperm_out; // 2D {H, R_max}, box {64, 32}   (GEMM2 epilogue TMA store)
   int bn2;               // GEMM2 N tile
 };
-bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2);
-bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h);
+bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2, bool fp8);
+// xq / aq: FP8 operand buffers (nullable when the experts are BF16)
+bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h, const uint8_t* xq,
+                   const uint8_t* aq);
 int gemm2_bn(int H);
 // x_gather != nullptr: A rows are gathered from x [T, H] through src_tok (TMA gather4),
 // i.e. the dispatch is fused into the GEMM and X_perm is never written.
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s);
+                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
+                     const F8Args* f8 = nullptr);
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
-                     int num_sms, cudaStream_t s);
+                     int num_sms, cudaStream_t s, const F8Args* f8 = nullptr);
 
 // Step (4): weighted combine (+ residual).
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
                     int64_t T, int H, int k, cudaStream_t s);
 
-// Weight packing (natural layout -> packed expert blobs), BF16.
+// Weight packing (natural layout -> packed expert blobs), BF16 and FP8 (codes + scales).
 void launch_pack_bf16(const bf16* gate, const bf16* up, const bf16* down, int count, int H, int h,
                       size_t expert_bytes, uint8_t* out, cudaStream_t s);
+void launch_pack_fp8(const uint8_t* gate, const uint8_t* up, const uint8_t* down, const float* gs, const float* us,
+                     const float* ds, int count, int H, int h, size_t expert_bytes, uint8_t* out, cudaStream_t s);
 
 // Driver entry point for cuTensorMapEncodeTiled (resolved once through the runtime).
 bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const void* base, const uint64_t* dims,

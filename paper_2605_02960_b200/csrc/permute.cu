@@ -156,7 +156,87 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
     }
   }
 }
+// FP8 dispatch (reading R6): x_t is quantised once per token to OCP E4M3 with a per-token
+// scale and written to its k permuted rows:
+//   amax = max_i |x_t[i]|;  inv = 448 / amax (fp32);  q_i = e4m3_rn_satfinite(x_t[i] * inv);
+//   scale = amax / 448 (fp32), dequantised value = q_i * scale   (amax == 0 -> q = 0, scale = 0)
+__global__ void __launch_bounds__(256) perm_quant_kernel(const bf16* __restrict__ x, const int32_t* __restrict__ dest,
+                                                         int64_t T, int H, int k, uint8_t* __restrict__ xq,
+                                                         float* __restrict__ xscale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+  const int nv = H / 8;
+  float amax = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    const uint4 u = src[v];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) amax = fmaxf(amax, fmaxf(fabsf(bf16_lo(w[q])), fabsf(bf16_hi(w[q]))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float inv = amax > 0.f ? 448.0f / amax : 0.f;
+  const float sc = amax / 448.0f;
+  int32_t d[kMaxTopK];
+#pragma unroll
+  for (int j = 0; j < kMaxTopK; ++j) d[j] = (j < k) ? dest[t * k + j] : 0;
+  for (int v = lane; v < nv; v += 32) {
+    const uint4 u = src[v];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint2 o;
+    o.x = (uint32_t)e4m3x2(bf16_lo(w[0]) * inv, bf16_hi(w[0]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[1]) * inv, bf16_hi(w[1]) * inv) << 16);
+    o.y = (uint32_t)e4m3x2(bf16_lo(w[2]) * inv, bf16_hi(w[2]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[3]) * inv, bf16_hi(w[3]) * inv) << 16);
+#pragma unroll
+    for (int j = 0; j < kMaxTopK; ++j)
+      if (j < k) reinterpret_cast<uint2*>(xq + (int64_t)d[j] * H)[v] = o;
+  }
+  if (lane < k) xscale[d[lane]] = sc;
+}
+
+// FP8 intermediate: act (bf16, written by the GEMM1 epilogue together with the row amax of
+// |act| in act_amax, as fp32 bits) -> e4m3 codes + per-row scale, same rule as above.
+__global__ void __launch_bounds__(256) act_quant_kernel(const bf16* __restrict__ act, uint32_t* __restrict__ act_amax,
+                                                        const int32_t* __restrict__ offsets, int E, int64_t R, int h,
+                                                        uint8_t* __restrict__ aq, float* __restrict__ ascale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= R || r >= offsets[E]) return;  // rows past the last expert tile were never written
+  const float amax = __uint_as_float(act_amax[r]);
+  const float inv = amax > 0.f ? 448.0f / amax : 0.f;
+  const uint4* src = reinterpret_cast<const uint4*>(act + r * h);
+  for (int v = lane; v < h / 8; v += 32) {
+    const uint4 u = src[v];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint2 o;
+    o.x = (uint32_t)e4m3x2(bf16_lo(w[0]) * inv, bf16_hi(w[0]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[1]) * inv, bf16_hi(w[1]) * inv) << 16);
+    o.y = (uint32_t)e4m3x2(bf16_lo(w[2]) * inv, bf16_hi(w[2]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[3]) * inv, bf16_hi(w[3]) * inv) << 16);
+    reinterpret_cast<uint2*>(aq + r * h)[v] = o;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    ascale[r] = amax / 448.0f;
+    act_amax[r] = 0u;  // re-armed for the next forward
+  }
+}
 }  // namespace
+
+void launch_perm_quant(const bf16* x, const int32_t* dest, int64_t T, int H, int k, uint8_t* xq, float* xscale,
+                       cudaStream_t s) {
+  if (T <= 0) return;
+  perm_quant_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, dest, T, H, k, xq, xscale);
+}
+
+void launch_act_quant(const bf16* act, uint32_t* act_amax, const int32_t* offsets, int E, int64_t R, int h,
+                      uint8_t* aq, float* ascale, cudaStream_t s) {
+  if (R <= 0) return;
+  act_quant_kernel<<<(unsigned)((R + 7) / 8), 256, 0, s>>>(act, act_amax, offsets, E, R, h, aq, ascale);
+}
 
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s) {
   const int nblk = (int)((T + kPermTokensPerBlock - 1) / kPermTokensPerBlock);

@@ -7,7 +7,9 @@ the library context, and runs the per-layer schedule of the "MoE gatherer"
 
 Weights are supplied by callables so this module holds no generator:
   router_fn(l)             -> [E, H] bf16 tensor
-  expert_fn(l, experts)    -> (gate [n,h,H], up [n,h,H], down [n,H,h]) bf16 tensors
+  expert_fn(l, experts)    -> (gate [n,h,H], up [n,h,H], down [n,H,h]) bf16 tensors, or for
+                              FP8 experts (codes uint8 x3, gate_scale [n,h], up_scale [n,h],
+                              down_scale [n,H] fp32)
 """
 from __future__ import annotations
 
@@ -20,11 +22,12 @@ from .schedule import layer_resident, shard_range, stack_schedule
 class MoEStack:
     def __init__(self, L, E, k, H, h, max_tokens, router_fn, expert_fn, *, world_size=1, rank=0,
                  replicate_layer0=True, norm_topk=True, flags=0, gamma=1.2, device="cuda",
-                 nccl_comm=None, compute_stream=None, comm_stream=None, pack_chunk=8):
+                 nccl_comm=None, compute_stream=None, comm_stream=None, pack_chunk=8, fp8=False):
         self.device = torch.device(device)
         self.cfg = A.make_config(L, E, k, H, h, world_size=world_size, rank=rank,
                                  replicate_layer0=int(replicate_layer0), norm_topk=int(norm_topk),
-                                 max_tokens=max_tokens, gamma=gamma, flags=flags)
+                                 max_tokens=max_tokens, gamma=gamma, flags=flags,
+                                 expert_dtype=A.FP8_E4M3 if fp8 else A.BF16)
         self.L, self.E, self.k, self.H, self.h = L, E, k, H, h
         self.N, self.rank = world_size, rank
         self.compute_stream = compute_stream or torch.cuda.current_stream(self.device)
@@ -40,10 +43,16 @@ class MoEStack:
             buf = torch.empty(len(ex) * ebytes, dtype=torch.uint8, device=self.device)
             for c0 in range(0, len(ex), pack_chunk):
                 sub = ex[c0:c0 + pack_chunk]
-                g, u, d = expert_fn(l, sub)
-                g, u, d = (t.to(self.device, torch.bfloat16).contiguous() for t in (g, u, d))
-                A.asyncep_pack_experts(self.cfg, g, u, d, buf[c0 * ebytes:(c0 + len(sub)) * ebytes],
-                                       stream=torch.cuda.current_stream(self.device))
+                dst = buf[c0 * ebytes:(c0 + len(sub)) * ebytes]
+                st = torch.cuda.current_stream(self.device)
+                if fp8:
+                    g, u, d, gs, us, ds = (t.to(self.device).contiguous() for t in expert_fn(l, sub))
+                    A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st, gate_scale=gs, up_scale=us,
+                                           down_scale=ds)
+                    del gs, us, ds
+                else:
+                    g, u, d = (t.to(self.device, torch.bfloat16).contiguous() for t in expert_fn(l, sub))
+                    A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st)
                 del g, u, d
             self.shards.append(buf)
         if world_size > 1:

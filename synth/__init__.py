@@ -127,3 +127,26 @@ def expert_weights(E: int, H: int, h: int, seed: int, layer: int, device="cpu",
         fill_normal_(u[i], seed, tensor_id(KIND_WU, layer, e), 1.0 / math.sqrt(H))
         fill_normal_(d[i], seed, tensor_id(KIND_WD, layer, e), 1.0 / math.sqrt(h))
     return g, u, d
+
+
+def expert_weights_fp8(E: int, H: int, h: int, seed: int, layer: int, device="cpu",
+                       experts: range | None = None):
+    """FP8 experts (reading R6: the model's expert weights ARE e4m3 + per-row scales):
+    the bf16 master weights of ``expert_weights`` quantised per output row,
+        s = amax_row / 448 (fp32);  code = e4m3_rne( w * (448 / amax_row) ).
+    Returns (gate, up, down codes as uint8, gate_scale [n,h], up_scale [n,h], down_scale [n,H]).
+    Every step is an IEEE fp32 op or the RNE fp32 -> e4m3 cast, so CPU and GPU agree."""
+    g, u, d = expert_weights(E, H, h, seed, layer, device=device, experts=experts)
+    out = []
+    scales = []
+    for w in (g, u, d):
+        wf = w.float()
+        amax = wf.abs().amax(dim=-1, keepdim=True)
+        inv = torch.where(amax > 0, torch.full_like(amax, 448.0) / amax, torch.zeros_like(amax))
+        codes = (wf * inv).to(torch.float8_e4m3fn).view(torch.uint8)
+        out.append(codes.contiguous())
+        # tensor / tensor (IEEE division on both devices; a python-scalar divisor becomes a
+        # reciprocal multiply on CUDA)
+        scales.append((amax / torch.full_like(amax, 448.0)).squeeze(-1).contiguous())
+        del wf
+    return out[0], out[1], out[2], scales[0], scales[1], scales[2]

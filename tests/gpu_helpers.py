@@ -15,25 +15,34 @@ def f32(t) -> np.ndarray:
 class Workload:
     """Natural-layout weights of an L-layer stack, generated on demand on any device."""
 
-    def __init__(self, L, E, k, H, h, seed=0, zipf_s=0.0):
+    def __init__(self, L, E, k, H, h, seed=0, zipf_s=0.0, fp8=False):
         self.L, self.E, self.k, self.H, self.h, self.seed, self.zipf_s = L, E, k, H, h, seed, zipf_s
+        self.fp8 = fp8
 
     def router(self, l, device="cuda"):
         return synth.router_weight(self.E, self.H, self.seed, l, device=device, zipf_s=self.zipf_s)
 
     def experts(self, l, experts=None, device="cuda"):
+        if self.fp8:
+            return synth.expert_weights_fp8(self.E, self.H, self.h, self.seed, l, device=device, experts=experts)
         return synth.expert_weights(self.E, self.H, self.h, self.seed, l, device=device, experts=experts)
 
     def tokens(self, T, device="cuda"):
         return synth.tokens(T, self.H, self.seed, device=device, zipf_s=self.zipf_s)
 
     def host_layer(self, l):
-        """fp32 numpy copies for the oracle (drawn on the GPU: synth is bit-identical)."""
+        """fp32 numpy copies for the oracle (drawn on the GPU: synth is bit-identical).
+        FP8 experts are dequantised code * row scale (exact up to one fp32 rounding)."""
         wr = f32(self.router(l))
+        if self.fp8:
+            import oracle
+            g, u, d, gs, us, ds = self.experts(l)
+            deq = lambda c, s: oracle.e4m3_decode(c.cpu().numpy()) * s.cpu().numpy()[..., None]
+            return wr, deq(g, gs), deq(u, us), deq(d, ds)
         g, u, d = self.experts(l)
         return wr, f32(g), f32(u), f32(d)
 
     def stack(self, max_tokens, **kw):
         from paper_2605_02960_b200.stack import MoEStack
         return MoEStack(self.L, self.E, self.k, self.H, self.h, max_tokens,
-                        lambda l: self.router(l), lambda l, ex: self.experts(l, ex), **kw)
+                        lambda l: self.router(l), lambda l, ex: self.experts(l, ex), fp8=self.fp8, **kw)

@@ -54,13 +54,14 @@ def output_error(y_gpu: np.ndarray, y_ref: np.ndarray) -> dict:
 
 
 def check_layer(x, wr, wg, wu, wd, k, y_gpu, ids_gpu, w_gpu, counts_gpu, residual=True, tol=2e-2,
-                norm_topk=True):
+                norm_topk=True, act_quant=False):
     """Full acceptance for one layer on tokens x (numpy fp32, bf16-valued).  ``counts_gpu``
     must be None when x is a sample of the tokens the GPU counted."""
     E = wr.shape[0]
     orc = oracle.router(x, wr, k, norm_topk=norm_topk)
     K, rep = check_router(ids_gpu, w_gpu, counts_gpu, orc, E)
-    ref = oracle.moe_layer(x, wr, wg, wu, wd, k, norm_topk=norm_topk, residual=residual, ids_in=ids_gpu)
+    ref = oracle.moe_layer(x, wr, wg, wu, wd, k, norm_topk=norm_topk, residual=residual, ids_in=ids_gpu,
+                           act_quant=act_quant)
     rep.update(output_error(y_gpu, ref["y"]))
     assert rep["err"] <= tol, f"output error {rep['err']} > {tol} ({rep})"
     return rep

@@ -255,3 +255,33 @@ def test_threshold_invariants():
     assert fp8 == pytest.approx(T0, rel=1e-12)
     with pytest.raises(ValueError):
         oracle.saturation_T(**{**base, "gamma": 0.5})
+
+
+def test_e4m3_fast_encoder_matches_brute_force_definition():
+    """The arithmetic encoder used by the emulation mode equals the nearest-code search."""
+    rng = np.random.default_rng(0)
+    vals = [0.0, -0.0, 448.0, 449.0, 464.0, 480.0, 1e9, -1e9, 2.0 ** -9, 2.0 ** -10, 3 * 2.0 ** -11,
+            2.0 ** -6, 2.0 ** -6 * (1 + 1 / 16), 7.5 * 2.0 ** -9]
+    codes = [oracle.e4m3_decode_one(c) for c in range(0x7F)]
+    for a, b in zip(codes, codes[1:]):  # every midpoint (ties) and its neighbours
+        m = (a + b) / 2
+        vals += [m, -m, np.nextafter(m, 0), np.nextafter(m, 1e9)]
+    vals += list(rng.standard_normal(3000) * 50) + list(rng.standard_normal(2000) * 0.01)
+    for v in vals:
+        assert oracle.e4m3_encode_fast_one(v) == oracle.e4m3_encode_one(v), v
+
+
+def test_act_quant_emulation_of_the_input_row():
+    """Identity experts + act_quant: y_t = (sum_j w_tj) * Q(x_t), Q = the R6 per-token rule
+    evaluated here with the brute-force encoder and numpy fp32 arithmetic."""
+    x, wr, *_ = _layer(T=20, H=64, E=8, k=2)
+    r = oracle.moe_layer(x, wr, 128, None, None, 2, residual=False, identity_experts=True, act_quant=True)
+    for t in range(x.shape[0]):
+        row = x[t].astype(np.float32)
+        amax = np.float32(np.abs(row).max())
+        inv = np.float32(448.0) / amax
+        sc = amax / np.float32(448.0)
+        q = np.array([oracle.e4m3_decode_one(oracle.e4m3_encode_one(float(np.float32(v * inv)))) for v in row])
+        np.testing.assert_allclose(r["y"][t], q * float(sc) * r["w"][t].sum(), rtol=1e-14, atol=0)
+    # quantisation error is bounded by half an e4m3 ulp (2^-4 relative) of each element
+    assert np.all(np.abs(r["y"] - x) <= np.abs(x) * 2.0 ** -4 + 2.0 ** -9 * np.abs(x).max(1, keepdims=True))
