@@ -60,7 +60,7 @@ constexpr int kNcclUint8 = 1;
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
-  size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, xperm, act, total;
+  size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, sched, xperm, act, total;
   size_t xq, xscale, amax, aq, ascale;  // FP8 experts only
 };
 WsLayout ws_layout(const asyncep_config& c) {
@@ -84,6 +84,7 @@ WsLayout ws_layout(const asyncep_config& c) {
   L.tile_start = take((E + 1) * 4);
   L.counts = take(E * 4);
   L.done = take(4);
+  L.sched = take(16);  // dynamic tile counters of the router / GEMM1 / GEMM2 launches
   L.xperm = take(Rp * (size_t)c.hidden * 2);  // X_perm, reused as Y_perm after GEMM1
   L.act = take(Rp * (size_t)c.ffn * 2);
   if (c.expert_dtype == ASYNCEP_FP8_E4M3) {
@@ -387,6 +388,8 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
 
   const bool timing = (cf.flags & ASYNCEP_FLAG_STAGE_TIMING) != 0;
   cudaEvent_t* ev = nullptr;
+  int* sched = (int*)(ws + c->L.sched);
+  CUDA_TRY(cudaMemsetAsync(sched, 0, 16, st));
   if (timing) {
     if (c->ev_used == kMaxPendingFwd) {
       asyncep_status fs = flush_timing(c);
@@ -404,7 +407,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (cf.flags & ASYNCEP_FLAG_SIMT_ROUTER)
     aep::launch_router_simt((const bf16*)x, (const bf16*)c->router_w[layer], T, H, E, k, cf.norm_topk, ids, w, st);
   else if (!aep::launch_router_tc(c->router_maps[layer], (const bf16*)x, T, H, E, k, cf.norm_topk, ids, w,
-                                  c->num_sms, st))
+                                  c->num_sms, st, sched))
     return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router x map)");
   c->launches += 1;
   if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
@@ -441,7 +444,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
   const uint8_t* wl = (const uint8_t*)(res ? c->shard[layer] : c->slot[s]);
   const aep::GemmMaps& wm = res ? c->layer_maps[layer] : c->slot_maps[s];
-  aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign)};
+  aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

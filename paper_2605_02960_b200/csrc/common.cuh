@@ -162,6 +162,26 @@ AEP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
       "r"(cta)
       : "memory");
 }
+// asynchronous DSMEM store of a 32-bit value to CTA `cta` (same smem offset as `p`), which
+// signals complete_tx(4 bytes) on that CTA's mbarrier at the offset of `bar`
+AEP_DEV void st_async_u32(const void* p, const uint64_t* bar, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra, rb;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %2;\n\t"
+      "mapa.shared::cluster.u32 rb, %1, %2;\n\t"
+      "st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b32 [ra], %3, [rb];\n\t}" ::"r"(smem_u32(p)),
+      "r"(smem_u32(bar)), "r"(cta), "r"(v)
+      : "memory");
+}
+// store a 32-bit value into CTA `cta`'s shared memory at the offset of `p` (DSMEM)
+AEP_DEV void st_cluster_u32(const void* p, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(p)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
 // relaxed variant: no release fence (a release would make the arriving thread wait for its
 // own previously issued TMA loads, serialising the producer)
 AEP_DEV void mbar_arrive_cluster_relaxed(uint64_t* bar, uint32_t cta) {

@@ -45,6 +45,7 @@ constexpr int NTHREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int TMEM_COLS = 512;
+constexpr int RING = 4;  // tile ids in flight between the scheduler and the consumers
 
 template <int NCTA>
 struct Cfg {
@@ -66,12 +67,13 @@ struct TcArgs {
   int n_out;    // output columns
   int ts_scale; // row tiles (of 128*NCTA rows) per tile_start unit (kRowAlign rows)
   int raster;   // 0: row-tile-major order; G > 0: groups of G row tiles walked row-first
-  int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first
+  int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first, 3 none (A)
   // FP8 (kind::f8f6f4) scales: dequantised D[r][c] = acc * a_scale[r] * b_scale(e)[B row of c]
   const float* a_scale;
   const uint8_t* b_scale_base;  // layer base + offset of the scale block inside an expert blob
   size_t expert_bytes;
   uint32_t* amax_out;           // GEMM1 FP8: per-row max |act| (fp32 bits, atomicMax)
+  int* sched;                   // dynamic tile counter (zeroed before the launch)
   const int32_t* gather_rows;  // non-null: A rows are gathered from the token matrix (map_a is a
                                // {H, T} gather4 map) with row ids gather_rows[permuted row]
   // router epilogue
@@ -184,6 +186,46 @@ __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t
   }
 }
 
+// Dynamic tile scheduler.  The leader CTA's producer thread takes the next tile id from a
+// global atomic counter (so the tiles in flight on the whole GPU always form one contiguous
+// window: no drift between persistent CTAs, which kept L2 reuse of the A row-tiles and the
+// expert weights poor with a static round-robin assignment) and publishes it through a
+// RING-deep smem ring: locally with an mbarrier arrive, to the peer CTA with st.async
+// (complete_tx on the peer's ring barrier).  Consumers release a ring slot on the leader's
+// sempty barrier.  p.sched == nullptr falls back to the static assignment unit + seq*nunits.
+struct TileRing {
+  uint64_t* sfull;
+  uint64_t* sempty;
+  int32_t* ring;
+};
+
+// scheduler side (leader producer thread): fetch + publish the id of tile number seq
+template <int NCTA>
+__device__ __forceinline__ int sched_publish(const TileRing& r, int* sched, int seq, int unit, int nunits) {
+  const int slot = seq % RING;
+  const uint32_t ph = (uint32_t)(seq / RING) & 1u;
+  mbar_wait(&r.sempty[slot], ph ^ 1u);
+  const int t = sched ? atomicAdd(sched, 1) : unit + seq * nunits;
+  r.ring[slot] = t;
+  mbar_arrive(&r.sfull[slot]);
+  if (NCTA == 2) st_async_u32(&r.ring[slot], &r.sfull[slot], 1, (uint32_t)t);
+  return t;
+}
+
+// consumer side (one thread): read tile id seq and release the slot to the leader.
+// arm = true for the single peer thread that arms the peer ring barrier for the st.async.
+template <int NCTA>
+__device__ __forceinline__ int sched_consume(const TileRing& r, int seq, bool leader, bool arm) {
+  const int slot = seq % RING;
+  const uint32_t ph = (uint32_t)(seq / RING) & 1u;
+  if (arm) mbar_arrive_expect_tx(&r.sfull[slot], 4);
+  mbar_wait(&r.sfull[slot], ph);
+  const int t = r.ring[slot];
+  if (NCTA == 2 && !leader) mbar_arrive_cluster_relaxed(&r.sempty[slot], 0);
+  else mbar_arrive(&r.sempty[slot]);
+  return t;
+}
+
 template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -199,7 +241,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sfull = tempty + 2;          // tile-id ring (dynamic scheduler): filled
+  uint64_t* sempty = sfull + RING;       //                                    released
+  int32_t* sring = reinterpret_cast<int32_t*>(sempty + RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sring + RING);
   int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
 
   const int warp = warp_id(), lane = lane_id();
@@ -229,6 +274,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4 * NCTA);  // one arrive per epilogue warp of each CTA
     }
+    for (int r = 0; r < RING; ++r) {
+      mbar_init(&sfull[r], 1);
+      // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue warps}
+      mbar_init(&sempty[r], 5 * NCTA);
+    }
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -244,6 +294,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   constexpr int KB_ELEMS = F8 ? 128 : BK;  // elements per 128-B k-block row
   const int nkb = p.K / KB_ELEMS;
   const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
+  const TileRing ring{sfull, sempty, sring};
 
   if (warp == 0) {
     // Producer warp.  Lane 0 arms the barriers and loads B (and A when it is a dense 2-D
@@ -254,7 +305,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = unit; t < total; t += nunits) {
+      for (int seq = 0;; ++seq) {
+        int t = 0;
+        if (lane == 0)
+          t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
+                     : sched_consume<NCTA>(ring, seq, false, true);
+        if (gather) t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= total) break;
         int mt, nt;
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
         const int e = find_expert(s_ts, G, mt);
@@ -268,12 +325,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (NCTA == 2) {
               if (leader) mbar_arrive_expect_tx(&full[stage], tx);
               else mbar_arrive_cluster_relaxed(&full[stage], 0);
-              if (!gather)
-                tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              if (!gather) {
+                if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
+                else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              }
               tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
             } else {
               mbar_arrive_expect_tx(&full[stage], tx);
-              if (!gather) tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              if (!gather) {
+                if (p.pol_a == 3) tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
+                else tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              }
               tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
             }
           }
@@ -295,7 +357,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = unit; t < total; t += nunits) {
+      for (int seq = 0;; ++seq) {
+        if (sched_consume<NCTA>(ring, seq, true, false) >= total) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -332,7 +395,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint8_t* stg = sStg + ew * STG_BYTES;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = unit; t < total; t += nunits) {
+    for (int seq = 0;; ++seq) {
+      int t = 0;
+      if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= total) break;
       int mt, nt;
       decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
       const int wrow0 = mt * TM + (int)rank * BM + ew * 32;  // first row of this warp's slice
@@ -469,6 +536,7 @@ int grouped_raster() {
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
                     const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false) {
+  static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
   a.tile_start = g.tile_start;
@@ -482,6 +550,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.pol_a = env_int("ASYNCEP_POL_A", 0);
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
   a.gather_rows = gather_rows;
+  a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
   if (f8) {
     a.a_scale = gemm2 ? f8->act_scale : f8->x_scale;
     a.b_scale_base = f8->layer + (gemm2 ? f8->sd_off : f8->sgu_off);
@@ -590,7 +659,8 @@ bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
     if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x_gather, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
-    launch_grouped(g, map_x, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, src_tok);
+    launch_grouped(g, map_x, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, src_tok, nullptr,
+                   false);
   } else {
     launch_grouped(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
   }
@@ -604,7 +674,8 @@ void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
     launch_grouped(g, am.aq, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s, nullptr, f8,
                    true);
   else
-    launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s);
+    launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s, nullptr,
+                   nullptr, true);
 }
 
 // ------------------------------------------------------------------ router on tcgen05
@@ -620,7 +691,7 @@ bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E) {
 }
 
 bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
-                      int32_t* ids, float* w, int num_sms, cudaStream_t s) {
+                      int32_t* ids, float* w, int num_sms, cudaStream_t s, int* sched) {
   if (T <= 0) return true;
   CUtensorMap map_x;
   const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
@@ -635,6 +706,7 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
   a.BN = rt.E_pad;
   a.n_tiles = 1;
   a.ts_scale = 1;
+  a.sched = sched;
   a.top_k = k;
   a.norm_topk = norm_topk;
   a.ids = ids;

@@ -29,7 +29,7 @@ struct RouterTc {
 bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E);
 // x map is built per call (x is the caller's buffer): [T, H] bf16, box {64, 128}
 bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
-                      int32_t* ids, float* w, int num_sms, cudaStream_t s);
+                      int32_t* ids, float* w, int num_sms, cudaStream_t s, int* sched = nullptr);
 
 // Step (2): permute / dispatch.
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s);
@@ -59,6 +59,8 @@ struct GroupedArgs {
   const int32_t* counts;     // [E] rows per expert
   int E;
   int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
+  int* sched = nullptr;      // [>= 3] dynamic tile counters, zeroed before each forward:
+                             // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
 };
 // rows of the permuted buffers for T tokens: T*k + E*(kRowAlign-1), rounded up to kRowAlign
 inline int64_t perm_rows(int64_t T, int k, int E) {
