@@ -99,19 +99,23 @@ class ClockSampler:
                 "samples": len(s)}
 
 
-def ncu_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+def ncu_traffic(fp8: bool = False):
+    """DRAM bytes per launch of the dominant kernel (GEMM1) from the committed ncu
+    --set full summary of the current kernel (profiles/r*/gemm_ncu_full*.json)."""
     import glob
-    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "gemm1_ncu_full.json")))
+    name = "gemm_ncu_full_fp8.json" if fp8 else "gemm_ncu_full.json"
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", name)))
     if not cands:
         return None
     try:
-        d = json.load(open(cands[-1]))
-        d = d[0] if isinstance(d, list) else d
-        return {"bytes_per_launch": d.get("dram_bytes_per_launch"),
-                "source": os.path.relpath(cands[-1], ROOT)}
+        for d in json.load(open(cands[-1])):
+            if "<1," in d.get("kernel", ""):
+                return {"bytes_per_launch": d.get("dram_bytes_per_launch"),
+                        "source": os.path.relpath(cands[-1], ROOT),
+                        "note": "ncu --set full, one launch (cold L2)"}
     except Exception:
         return None
+    return None
 
 
 # ------------------------------------------------------------------------------ oracle arm
@@ -292,7 +296,7 @@ def main():
         peak_tf *= 2.0
         spec *= 2.0
         peak_note = f"{peak_src} bf16_tflops_sustained x 2 (nominal fp8:bf16 dense ratio)"
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(args.fp8)
     per_layer_ms = {k: v / max(nfwd, 1) for k, v in stages.items()}
     step_layer_ms = ms_step / L
     line = {
