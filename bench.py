@@ -189,6 +189,9 @@ def main():
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
+    ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
+                    help="1-GPU emulation of the N-rank AsyncEP gather (D2D copies of all N shards into "
+                         "the slot on the comm stream); measures exposed wait + HBM interference")
     ap.add_argument("--fp8", action="store_true",
                     help="FP8 e4m3 experts (BASELINE config 4) instead of BF16 (config 3)")
     args = ap.parse_args()
@@ -218,11 +221,13 @@ def main():
     seed = 0
     flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0)
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
+    emu = args.emulate_gather if world == 1 else 0
     stack = MoEStack(L, E_, K_, H_, h_, T,
                      lambda l: synth.router_weight(E_, H_, seed, l, device=dev),
                      lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex),
-                     world_size=world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
+                     world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8)
+    local_shards = stack.peer_shards() if emu > 1 else None
     # tokens: DP -- every rank its own batch
     x = synth.tokens(T, H_, seed + 17 + rank, device=dev)
     out = torch.empty_like(x)
@@ -234,7 +239,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        stack.run(x, out=out)
+        stack.run(x, out=out, local_shards=local_shards)
     barrier()
     A.asyncep_reset_stage_times(stack.ctx)
     launches0 = A.asyncep_kernel_launches(stack.ctx)
@@ -244,7 +249,7 @@ def main():
     barrier()
     e0.record(cs)
     for _ in range(args.steps):
-        stack.run(x, out=out)
+        stack.run(x, out=out, local_shards=local_shards)
     e1.record(cs)
     barrier()
     clk = clocks.stop()
@@ -266,7 +271,7 @@ def main():
     xd = torch.empty_like(x)
     for _ in range(1):
         xd.copy_(xh, non_blocking=True)
-        stack.run(xd, out=out)
+        stack.run(xd, out=out, local_shards=local_shards)
         yh.copy_(out, non_blocking=True)
     barrier()
     f0 = torch.cuda.Event(enable_timing=True)
@@ -274,7 +279,7 @@ def main():
     f0.record(cs)
     for _ in range(args.steps):
         xd.copy_(xh, non_blocking=True)
-        stack.run(xd, out=out)
+        stack.run(xd, out=out, local_shards=local_shards)
         yh.copy_(out, non_blocking=True)
     f1.record(cs)
     barrier()
@@ -307,7 +312,9 @@ def main():
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights",
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
-                   "parallelism": f"dp{world}+asyncep{world}" if world > 1 else "dp1 (all experts resident)",
+                   "parallelism": (f"dp{world}+asyncep{world}" if world > 1 else
+                                   f"dp1, asyncep{emu} gather emulated on 1 GPU (D2D copies of the {emu} shards "
+                                   "into the slot on the comm stream)" if emu > 1 else "dp1 (all experts resident)"),
                    "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,
@@ -318,7 +325,8 @@ def main():
         "layer_ms": step_layer_ms,
         "exposed_ag": {"ms_per_layer": per_layer_ms["gather_wait"],
                        "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms else None,
-                       "note": "event gap before GEMM1 on gathered layers (0 when N=1)"},
+                       "note": ("stream wait before GEMM1 on gathered layers (0 when N=1)" if not emu else
+                                f"emulated {emu}-rank gather (local D2D, no NVLink): exposed wait")},
         "roofline": {"kernel": "grouped GEMM1 gate/up + SwiGLU (tcgen05)", "bound": "tensor",
                      "achieved": g1_tflops, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": g1_tflops / peak_tf,

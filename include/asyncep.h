@@ -184,6 +184,23 @@ ASYNCEP_API asyncep_status asyncep_stage_times(asyncep_ctx* ctx, double* ms_out,
                                    int64_t* forwards_out);
 ASYNCEP_API asyncep_status asyncep_reset_stage_times(asyncep_ctx* ctx);
 
+/*
+ * Per-forward wall time (ms, CUDA events around the whole forward) of the last recorded
+ * forwards, oldest first, with their layer ids (ASYNCEP_FLAG_STAGE_TIMING).  Writes up to n
+ * entries; returns the count through n_out.  Synchronises on the recorded events.
+ */
+ASYNCEP_API asyncep_status asyncep_forward_times(asyncep_ctx* ctx, double* ms_out, int32_t* layer_out, int32_t n,
+                                                 int32_t* n_out);
+
+/*
+ * Calibrated saturation threshold, App. B.4 Eq. 3:
+ *   T = gamma * (t_e / t_c) * C_dummy  [FLOPs],  collapsing to gamma * C_dummy when t_e <= t_c,
+ * with t_c = wall time of the resident layer 0 and t_e = max wall time of the gathered layers
+ * in one profile pass at n_ref tokens, C_dummy = f_tok * n_ref.  Pure; outputs may be NULL.
+ */
+ASYNCEP_API asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double c_dummy,
+                                                double* flops_out);
+
 /* Number of kernels the library launched since context creation (host-side counter). */
 ASYNCEP_API int64_t asyncep_kernel_launches(const asyncep_ctx* ctx);
 

@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
             "asyncep_stage_times": ([P, ctypes.POINTER(D), I32, ctypes.POINTER(I64)], I32),
             "asyncep_reset_stage_times": ([P], I32),
             "asyncep_kernel_launches": ([P], I64),
+            "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
+            "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
             "asyncep_destroy": ([P], I32),
         }
         for name, (args, res) in sig.items():
@@ -192,6 +194,22 @@ def asyncep_stage_times(ctx: Context):
     n = ctypes.c_int64()
     _check(lib().asyncep_stage_times(ctx.handle, ms, len(STAGES), ctypes.byref(n)))
     return dict(zip(STAGES, list(ms))), n.value
+
+
+def asyncep_forward_times(ctx: Context, n: int = 4096):
+    """[(layer, ms)] of the last recorded forwards (ASYNCEP_FLAG_STAGE_TIMING), oldest first."""
+    ms = (ctypes.c_double * n)()
+    ly = (ctypes.c_int32 * n)()
+    m = ctypes.c_int32()
+    _check(lib().asyncep_forward_times(ctx.handle, ms, ly, n, ctypes.byref(m)))
+    return [(ly[i], ms[i]) for i in range(m.value)]
+
+
+def asyncep_calibrated_T(gamma: float, t_e: float, t_c: float, c_dummy: float) -> float:
+    """App. B.4 Eq. 3: T = gamma * (t_e / t_c) * C_dummy [FLOPs]."""
+    out = ctypes.c_double()
+    _check(lib().asyncep_calibrated_T(gamma, t_e, t_c, c_dummy, ctypes.byref(out)))
+    return out.value
 
 
 def asyncep_reset_stage_times(ctx: Context) -> None:

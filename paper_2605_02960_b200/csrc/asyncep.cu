@@ -5,6 +5,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -158,6 +159,8 @@ struct asyncep_ctx {
   int ev_used = 0;  // forwards recorded since the last flush
   double stage_ms[kStages] = {0};
   int64_t fwd_count = 0;
+  std::vector<int32_t> ev_layer;                 // layer of each pending recorded forward
+  std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   int64_t launches = 0;
 };
 
@@ -177,7 +180,12 @@ asyncep_status flush_timing(asyncep_ctx* c) {
       CUDA_TRY(cudaEventElapsedTime(&ms, e[s], e[s + 1]));
       c->stage_ms[s] += ms;
     }
+    float tot = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&tot, e[0], e[kStages]));
+    c->recent.emplace_back(c->ev_layer[f], (double)tot);
+    if (c->recent.size() > 4096) c->recent.erase(c->recent.begin(), c->recent.begin() + 2048);
   }
+  c->ev_layer.clear();
   c->fwd_count += c->ev_used;
   c->ev_used = 0;
   return ASYNCEP_OK;
@@ -401,6 +409,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     }
     ev = &c->ev_pool[(size_t)c->ev_used * kEventsPerFwd];
     ++c->ev_used;
+    c->ev_layer.push_back(layer);
     CUDA_TRY(cudaEventRecord(ev[0], st));
   }
   // (1) router GEMM + softmax + top-k
@@ -520,6 +529,30 @@ asyncep_status asyncep_reset_stage_times(asyncep_ctx* c) {
   if (st) return st;
   for (double& v : c->stage_ms) v = 0.0;
   c->fwd_count = 0;
+  c->recent.clear();
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_forward_times(asyncep_ctx* c, double* ms_out, int32_t* layer_out, int32_t n, int32_t* n_out) {
+  if (!c || n < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "bad arguments");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  const int32_t m = (int32_t)std::min<size_t>((size_t)n, c->recent.size());
+  const size_t base = c->recent.size() - (size_t)m;
+  for (int32_t i = 0; i < m; ++i) {
+    if (ms_out) ms_out[i] = c->recent[base + i].second;
+    if (layer_out) layer_out[i] = c->recent[base + i].first;
+  }
+  if (n_out) *n_out = m;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double c_dummy, double* flops_out) {
+  if (!(gamma >= 1.0) || !(t_c > 0) || !(t_e >= 0) || !(c_dummy >= 0))
+    return fail(ASYNCEP_ERR_INVALID_ARG, "calibrated_T: need gamma >= 1, t_c > 0, t_e >= 0, C_dummy >= 0");
+  // T = gamma * (t_e / t_c) * C_dummy; collapses to gamma * C_dummy when transfers are hidden
+  const double ratio = t_e <= t_c ? 1.0 : t_e / t_c;
+  if (flops_out) *flops_out = gamma * ratio * c_dummy;
   return ASYNCEP_OK;
 }
 

@@ -36,25 +36,11 @@ class MoEStack:
         ebytes = A.asyncep_expert_bytes(self.cfg)
         self.expert_bytes = ebytes
         self.router_w = [router_fn(l).to(self.device, torch.bfloat16).contiguous() for l in range(L)]
+        self.fp8, self.expert_fn, self.pack_chunk = fp8, expert_fn, pack_chunk
         self.shards = []
         for l in range(L):
             full = layer_resident(l, world_size, replicate_layer0)
-            ex = range(E) if full else shard_range(E, world_size, rank)
-            buf = torch.empty(len(ex) * ebytes, dtype=torch.uint8, device=self.device)
-            for c0 in range(0, len(ex), pack_chunk):
-                sub = ex[c0:c0 + pack_chunk]
-                dst = buf[c0 * ebytes:(c0 + len(sub)) * ebytes]
-                st = torch.cuda.current_stream(self.device)
-                if fp8:
-                    g, u, d, gs, us, ds = (t.to(self.device).contiguous() for t in expert_fn(l, sub))
-                    A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st, gate_scale=gs, up_scale=us,
-                                           down_scale=ds)
-                    del gs, us, ds
-                else:
-                    g, u, d = (t.to(self.device, torch.bfloat16).contiguous() for t in expert_fn(l, sub))
-                    A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st)
-                del g, u, d
-            self.shards.append(buf)
+            self.shards.append(self.pack(l, range(E) if full else shard_range(E, world_size, rank)))
         if world_size > 1:
             sb = A.asyncep_slot_bytes(self.cfg)
             self.slots = [torch.empty(sb, dtype=torch.uint8, device=self.device) for _ in range(2)]
@@ -65,6 +51,37 @@ class MoEStack:
         self.ctx = A.asyncep_init(self.cfg, nccl_comm, self.compute_stream, self.comm_stream, self.router_w,
                                   self.shards, self.slots[0], self.slots[1], self.workspace)
         self._bufs = None
+
+    def pack(self, l: int, experts: range) -> torch.Tensor:
+        """Packed blobs of ``experts`` of layer l (the shard format of asyncep.h)."""
+        ebytes = self.expert_bytes
+        buf = torch.empty(len(experts) * ebytes, dtype=torch.uint8, device=self.device)
+        st = torch.cuda.current_stream(self.device)
+        for c0 in range(0, len(experts), self.pack_chunk):
+            sub = experts[c0:c0 + self.pack_chunk]
+            dst = buf[c0 * ebytes:(c0 + len(sub)) * ebytes]
+            if self.fp8:
+                g, u, d, gs, us, ds = (t.to(self.device).contiguous() for t in self.expert_fn(l, sub))
+                A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st, gate_scale=gs, up_scale=us,
+                                       down_scale=ds)
+                del gs, us, ds
+            else:
+                g, u, d = (t.to(self.device, torch.bfloat16).contiguous() for t in self.expert_fn(l, sub))
+                A.asyncep_pack_experts(self.cfg, g, u, d, dst, stream=st)
+            del g, u, d
+        return buf
+
+    def peer_shards(self):
+        """Single-GPU emulation of the other ranks (tests / --emulate-gather): the shards of
+        ranks != self.rank for every gathered layer, so asyncep_prefetch_layer_local can
+        assemble the slot with device-to-device copies.  Returns local_shards(l)."""
+        table = {}
+        for l in range(self.L):
+            if self.layer_resident(l):
+                continue
+            table[l] = [self.shards[l] if r == self.rank else self.pack(l, shard_range(self.E, self.N, r))
+                        for r in range(self.N)]
+        return lambda l: table[l]
 
     def layer_resident(self, l: int) -> bool:
         return layer_resident(l, self.N, bool(self.cfg.replicate_layer0))
@@ -99,3 +116,25 @@ class MoEStack:
             self.forward(l, cur, residual=cur if residual else None, y=dst)
             cur = dst
         return cur
+
+    def calibrate_T(self, x, gamma: float | None = None, local_shards=None):
+        """NEXT-1, App. B.4: one profile pass of the stack at
+        n_ref = len(x) tokens with per-forward CUDA-event timing; t_c = wall time of the
+        resident layer 0 (pure compute), t_e = max wall time of the layers >= 1 (each the
+        envelope max(compute, transfer)); C_dummy = f_tok * n_ref with f_tok the per-token
+        FLOPs of one MoE layer (2HE + 6kHh); returns T = gamma * (t_e/t_c) * C_dummy in FLOPs
+        and in tokens per GPU (T / f_tok), plus the measured (t_c, t_e)."""
+        if not (self.cfg.flags & A.FLAG_STAGE_TIMING):
+            raise ValueError("calibrate_T needs a context created with FLAG_STAGE_TIMING")
+        gamma = float(self.cfg.gamma) if gamma is None else gamma
+        A.asyncep_reset_stage_times(self.ctx)
+        self.run(x, local_shards=local_shards)
+        times = A.asyncep_forward_times(self.ctx, self.L)
+        t_c = next(ms for l, ms in times if l == 0)
+        rest = [ms for l, ms in times if l >= 1]
+        t_e = max(rest) if rest else t_c
+        f_tok = 2.0 * self.H * self.E + 6.0 * self.k * self.H * self.h
+        c_dummy = f_tok * x.shape[0]
+        T = A.asyncep_calibrated_T(gamma, t_e, t_c, c_dummy)
+        return {"T_flops": T, "T_tokens": T / f_tok, "t_c_ms": t_c, "t_e_ms": t_e, "n_ref": x.shape[0],
+                "f_tok": f_tok}

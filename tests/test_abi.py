@@ -78,3 +78,12 @@ def test_saturation_T_matches_oracle(A, N, dtype, b, F):
     assert t == pytest.approx(t0, rel=1e-12) and f == pytest.approx(f0, rel=1e-12)
     if N == 1:
         assert t == 0.0
+
+
+def test_calibrated_T_matches_oracle(A):
+    """App. B.4 Eq. 3 through the C ABI vs the oracle (and SPEC's worked example)."""
+    for g, te, tc, c in ((1.2, 2.0, 1.0, 1e12), (1.2, 0.5, 1.0, 7.0), (1.5, 3.3, 1.1, 4e13), (1.0, 1.0, 1.0, 5.0)):
+        assert A.asyncep_calibrated_T(g, te, tc, c) == pytest.approx(oracle.calibrated_T(g, te, tc, c), rel=1e-15)
+    assert A.asyncep_calibrated_T(1.2, 2.0, 1.0, 1e12) == pytest.approx(2.4e12, rel=1e-15)
+    with pytest.raises(A.AsyncEPError):
+        A.asyncep_calibrated_T(0.9, 1.0, 1.0, 1.0)

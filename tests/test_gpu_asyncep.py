@@ -123,3 +123,26 @@ def test_poisoned_slot_after_use_is_never_read():
         cur = dst
     torch.cuda.synchronize()
     assert torch.equal(_bits(cur), _bits(ref))
+
+
+def test_peer_shards_and_calibrated_T():
+    """MoEStack.peer_shards (1-GPU rank emulation) gives the resident output bitwise, and
+    the App. B.4 profile pass returns T = gamma * (t_e / t_c) * C_dummy with the measured
+    per-layer wall times."""
+    from paper_2605_02960_b200 import asyncep as A
+    wl = Workload(L=4, E=16, k=4, H=256, h=256, seed=16)
+    T = 1024
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    st = wl.stack(max_tokens=T, world_size=4, flags=A.FLAG_STAGE_TIMING)
+    sh = st.peer_shards()
+    out = st.run(x, local_shards=sh).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
+    cal = st.calibrate_T(x, local_shards=sh)
+    assert cal["t_c_ms"] > 0 and cal["t_e_ms"] > 0
+    f_tok = 2 * 256 * 16 + 6 * 4 * 256 * 256
+    ratio = max(1.0, cal["t_e_ms"] / cal["t_c_ms"])
+    assert cal["T_flops"] == pytest.approx(1.2 * ratio * f_tok * T, rel=1e-6)
+    times = A.asyncep_forward_times(st.ctx)
+    assert [l for l, _ in times][-4:] == [0, 1, 2, 3]
