@@ -2,6 +2,7 @@
 // double-buffered expert slot with its CUDA-event ordering, the NCCL AllGather
 // ("MoE gatherer") and the four-step forward.
 #include <dlfcn.h>
+#include <link.h>
 
 #include <cstdarg>
 #include <cstdio>
@@ -48,8 +49,20 @@ struct NcclApi {
   nccl_errstr_fn errstr = nullptr;
   nccl_async_err_fn async_err = nullptr;
 };
+// the path of the libnccl the process already loaded (torch's wheel copy), so we bind to the
+// very library that created the borrowed communicator and never load a second NCCL
+int find_nccl_cb(struct dl_phdr_info* info, size_t, void* data) {
+  if (info->dlpi_name && strstr(info->dlpi_name, "libnccl.so")) {
+    *static_cast<std::string*>(data) = info->dlpi_name;
+    return 1;
+  }
+  return 0;
+}
 bool resolve_nccl(NcclApi& api) {
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  std::string path;
+  dl_iterate_phdr(find_nccl_cb, &path);
+  void* h = path.empty() ? nullptr : dlopen(path.c_str(), RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = RTLD_DEFAULT;
   api.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
   api.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");

@@ -146,3 +146,42 @@ def test_peer_shards_and_calibrated_T():
     assert cal["T_flops"] == pytest.approx(1.2 * ratio * f_tok * T, rel=1e-6)
     times = A.asyncep_forward_times(st.ctx)
     assert [l for l, _ in times][-4:] == [0, 1, 2, 3]
+
+
+def test_nccl_allgather_path_with_borrowed_torch_comm():
+    """The real NCCL path on one GPU: borrow the communicator of a 1-rank torch NCCL process
+    group (ProcessGroupNCCL._comm_ptr) in a context configured as rank 0 of 2.  ncclAllGather
+    over that 1-rank communicator then writes this rank's shard into the first half of the
+    slot (rank-major placement), on the comm stream, ordered by the ag_done event before
+    GEMM1.  Checks the comm borrowing, the in-process NCCL symbol resolution, the stream and
+    event plumbing end to end."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_2605_02960_b200 import asyncep as A
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        dist.all_reduce(torch.ones(1, device="cuda"))
+        comm = A.nccl_comm_ptr()
+        assert comm
+        wl = Workload(L=3, E=8, k=2, H=64, h=128, seed=17)
+        full = wl.stack(max_tokens=64)
+        st = wl.stack(max_tokens=64, world_size=2, rank=0, nccl_comm=comm)
+        st.slots[1].fill_(0xAB)
+        A.asyncep_prefetch_layer(st.ctx, 1)
+        x = wl.tokens(64)
+        st.forward(0, x, y=torch.empty_like(x))
+        st.forward(1, x, y=torch.empty_like(x))   # waits on the NCCL gather's event
+        torch.cuda.synchronize()
+        half = st.shards[1].numel()
+        assert torch.equal(st.slots[1][:half], st.shards[1])
+        assert torch.equal(st.slots[1][:half], full.shards[1][:half])
+        assert torch.all(st.slots[1][half:] == 0xAB)  # the absent rank's half is untouched
+    finally:
+        dist.destroy_process_group()
