@@ -192,6 +192,11 @@ def main():
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
                     help="1-GPU emulation of the N-rank AsyncEP gather (D2D copies of all N shards into "
                          "the slot on the comm stream); measures exposed wait + HBM interference")
+    ap.add_argument("--link-gbs", type=float, default=0.0,
+                    help="with --emulate-gather: pace the peer-shard copies at this GB/s (NVLink receive "
+                         "bandwidth; B200_PROFILING.md measured peer copy: 770)")
+    ap.add_argument("--zipf", type=float, default=0.0, metavar="S",
+                    help="Zipf-skewed routing (reading R14, BASELINE config 5 uses S=0.35)")
     ap.add_argument("--fp8", action="store_true",
                     help="FP8 e4m3 experts (BASELINE config 4) instead of BF16 (config 3)")
     args = ap.parse_args()
@@ -223,13 +228,15 @@ def main():
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
     emu = args.emulate_gather if world == 1 else 0
     stack = MoEStack(L, E_, K_, H_, h_, T,
-                     lambda l: synth.router_weight(E_, H_, seed, l, device=dev),
+                     lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf),
                      lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex),
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8)
     local_shards = stack.peer_shards() if emu > 1 else None
+    if emu > 1 and args.link_gbs > 0:
+        A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
     # tokens: DP -- every rank its own batch
-    x = synth.tokens(T, H_, seed + 17 + rank, device=dev)
+    x = synth.tokens(T, H_, seed + 17 + rank, device=dev, zipf_s=args.zipf)
     out = torch.empty_like(x)
     cs = stack.compute_stream
 
@@ -303,6 +310,15 @@ def main():
         peak_note = f"{peak_src} bf16_tflops_sustained x 2 (nominal fp8:bf16 dense ratio)"
     traffic = ncu_traffic(args.fp8)
     per_layer_ms = {k: v / max(nfwd, 1) for k, v in stages.items()}
+    # Eq. 1 (R11/R12): T in tokens/GPU with F = this run's grouped-GEMM
+    # rate and the gather bandwidth of NVLink 5 (measured peer copy 770 GB/s, B200_PROFILING.md)
+    gemm_ms = per_layer_ms["gemm1_gateup_swiglu"] + per_layer_ms["gemm2_down"]
+    f_gemm = (GEMM1_FLOPS_TOK + GEMM2_FLOPS_TOK) * T / (gemm_ms / 1e3) if gemm_ms > 0 else 0.0
+    n_for_T = world if world > 1 else (emu if emu > 1 else 8)
+    bw = (args.link_gbs or 770.0) * 1e9
+    tcfg = A.make_config(L, E_, K_, H_, h_, expert_dtype=A.FP8_E4M3 if args.fp8 else A.BF16,
+                         world_size=n_for_T, max_tokens=T, gamma=1.2)
+    t_tok, t_flops = A.asyncep_saturation_T(tcfg, f_gemm, bw) if f_gemm > 0 else (None, None)
     step_layer_ms = ms_step / L
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -310,11 +326,13 @@ def main():
         "vs_baseline": None, "dtype": "fp8_e4m3" if args.fp8 else "bf16", "data": "synthetic",
         "config": {"workload": f"qwen3-235b-a22b moe-layer stack, {L} layers, E=128 k=8 H=4096 h=1536, "
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
-                               "random-init weights",
+                               "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
                    "parallelism": (f"dp{world}+asyncep{world}" if world > 1 else
                                    f"dp1, asyncep{emu} gather emulated on 1 GPU (D2D copies of the {emu} shards "
-                                   "into the slot on the comm stream)" if emu > 1 else "dp1 (all experts resident)"),
+                                   "into the slot on the comm stream" +
+                                   (f", peer shards paced at {args.link_gbs} GB/s" if args.link_gbs else "") + ")"
+                                   if emu > 1 else "dp1 (all experts resident)"),
                    "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,
@@ -322,6 +340,9 @@ def main():
                 "vs_measured_sustained": mfu_flops / (peak_tf * 1e12),
                 "flops_per_token_layer": FLOPS_TOK_LAYER},
         "stage_ms_per_layer": per_layer_ms,
+        "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
+                         "flops_per_s": f_gemm, "ag_bytes_per_s": bw,
+                         "note": "Eq. 1 per layer, F = measured grouped-GEMM rate of this run"},
         "layer_ms": step_layer_ms,
         "exposed_ag": {"ms_per_layer": per_layer_ms["gather_wait"],
                        "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms else None,

@@ -148,6 +148,14 @@ ASYNCEP_API asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* ctx, int32_
                                             const void* const* shards);
 
 /*
+ * Test / measurement hook for asyncep_prefetch_layer_local: pace the copies of the OTHER
+ * ranks' shards at `bytes_per_s` (0 = unpaced) to emulate the NVLink receive bandwidth of
+ * an N-rank AllGather on one GPU.  Each 64 MiB chunk is preceded on the comm stream by a
+ * one-thread kernel that spins for chunk_bytes / bytes_per_s.
+ */
+ASYNCEP_API asyncep_status asyncep_set_link_emulation(asyncep_ctx* ctx, double bytes_per_s);
+
+/*
  * The MoE FFN forward of layer `layer` on the compute stream.
  *  x         : [num_tokens, H] bf16 device, 16-B aligned rows.
  *  residual  : nullable [num_tokens, H] bf16 device; added to the output (reading R9).

@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_kernel_launches": ([P], I64),
             "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
+            "asyncep_set_link_emulation": ([P, D], I32),
             "asyncep_destroy": ([P], I32),
         }
         for name, (args, res) in sig.items():
@@ -169,6 +170,10 @@ def asyncep_prefetch_layer(ctx: Context, layer: int) -> None:
 def asyncep_prefetch_layer_local(ctx: Context, layer: int, shards) -> None:
     arr = (ctypes.c_void_p * len(shards))(*[_p(t) for t in shards])
     _check(lib().asyncep_prefetch_layer_local(ctx.handle, layer, arr))
+
+
+def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:
+    _check(lib().asyncep_set_link_emulation(ctx.handle, float(bytes_per_s)))
 
 
 def asyncep_moe_forward(ctx: Context, layer: int, x: torch.Tensor, residual=None, y=None,

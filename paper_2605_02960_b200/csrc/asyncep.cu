@@ -175,6 +175,7 @@ struct asyncep_ctx {
   std::vector<int32_t> ev_layer;                 // layer of each pending recorded forward
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   int64_t launches = 0;
+  double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
 };
 
 namespace {
@@ -348,10 +349,20 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
   // WAR: the slot's previous occupant must have finished its GEMMs.
   CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
   if (shards) {
+    constexpr size_t kChunk = (size_t)64 << 20;
     for (int r = 0; r < c->cfg.world_size; ++r) {
       if (!shards[r]) return fail(ASYNCEP_ERR_INVALID_ARG, "null shard %d", r);
-      CUDA_TRY(cudaMemcpyAsync((uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes, shards[r], c->shard_bytes,
-                               cudaMemcpyDeviceToDevice, c->ms));
+      uint8_t* dst = (uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes;
+      const uint8_t* src = (const uint8_t*)shards[r];
+      const bool paced = c->link_bps > 0 && r != c->cfg.rank;  // own shard is a local copy
+      for (size_t o = 0; o < c->shard_bytes; o += kChunk) {
+        const size_t n = std::min(kChunk, c->shard_bytes - o);
+        if (paced) {
+          aep::launch_spin_ns((uint64_t)((double)n / c->link_bps * 1e9), c->ms);
+          c->launches += 1;
+        }
+        CUDA_TRY(cudaMemcpyAsync(dst + o, src + o, n, cudaMemcpyDeviceToDevice, c->ms));
+      }
     }
   } else {
     if (!c->comm) return fail(ASYNCEP_ERR_NCCL, "no NCCL communicator (use asyncep_prefetch_layer_local)");
@@ -372,6 +383,12 @@ asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* c, int32_t layer, const
   if (c->cfg.world_size < 2) return fail(ASYNCEP_ERR_INVALID_ARG, "prefetch_layer_local needs world_size > 1");
   if (!shards) return fail(ASYNCEP_ERR_INVALID_ARG, "shards is NULL");
   return prefetch_common(c, layer, shards);
+}
+
+asyncep_status asyncep_set_link_emulation(asyncep_ctx* c, double bytes_per_s) {
+  if (!c || bytes_per_s < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "bad arguments");
+  c->link_bps = bytes_per_s;
+  return ASYNCEP_OK;
 }
 
 asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x, int64_t T, const void* residual,

@@ -61,7 +61,19 @@ __global__ void __launch_bounds__(256) combine_kernel(const bf16* __restrict__ y
     reinterpret_cast<uint4*>(y + t * H)[v] = o;
   }
 }
+__global__ void spin_ns_kernel(uint64_t ns) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
 }  // namespace
+
+void launch_spin_ns(uint64_t ns, cudaStream_t s) { spin_ns_kernel<<<1, 1, 0, s>>>(ns); }
 
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
                     int64_t T, int H, int k, cudaStream_t s) {

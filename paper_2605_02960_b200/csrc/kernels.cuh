@@ -119,6 +119,9 @@ void launch_pack_bf16(const bf16* gate, const bf16* up, const bf16* down, int co
 void launch_pack_fp8(const uint8_t* gate, const uint8_t* up, const uint8_t* down, const float* gs, const float* us,
                      const float* ds, int count, int H, int h, size_t expert_bytes, uint8_t* out, cudaStream_t s);
 
+// One thread spinning on %globaltimer for `ns` nanoseconds (link-bandwidth emulation).
+void launch_spin_ns(uint64_t ns, cudaStream_t s);
+
 // Driver entry point for cuTensorMapEncodeTiled (resolved once through the runtime).
 bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const void* base, const uint64_t* dims,
                  const uint64_t* strides_bytes /* rank-1 entries */, const uint32_t* box, CUtensorMapSwizzle sw);

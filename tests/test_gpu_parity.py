@@ -193,3 +193,23 @@ def test_qwen3_235b_full_size_sampled():
     wr, g, u, d = wl.host_layer(0)
     rep = check_layer(f32(x)[idx], wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None)
     print(rep)
+
+
+def test_config5_zipf_skewed_full_size_sampled():
+    """BASELINE config 5: one 32K-token prompt per GPU with Zipf-skewed routing (R14,
+    s = 0.35: max/min expert load ~16x, cf. the paper's 16.15x).  Checks the
+    skew is present and the sampled tokens pass the acceptance procedure."""
+    T = 32768
+    wl = Workload(**Q235, seed=5, zipf_s=0.35)
+    st = wl.stack(max_tokens=T)
+    x = wl.tokens(T)
+    y, ids, w, counts = run_layer(wl, st, 0, x)
+    ratio = counts.max() / max(counts.min(), 1)
+    print("max/min expert load", ratio, "max/mean", counts.max() / counts.mean())
+    assert 8 <= ratio <= 64
+    assert np.array_equal(counts, np.bincount(ids.ravel(), minlength=wl.E))
+    del st
+    torch.cuda.empty_cache()
+    idx = np.unique(np.concatenate([[0, T - 1], np.random.default_rng(3).choice(T, 94, replace=False)]))
+    wr, g, u, d = wl.host_layer(0)
+    print(check_layer(f32(x)[idx], wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None))
