@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=T_LOC, help="tokens per GPU")
+    ap.add_argument("--replicate-layer0", type=int, default=1)
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
@@ -195,6 +196,9 @@ def main():
     ap.add_argument("--link-gbs", type=float, default=0.0,
                     help="with --emulate-gather: pace the peer-shard copies at this GB/s (NVLink receive "
                          "bandwidth; B200_PROFILING.md measured peer copy: 770)")
+    ap.add_argument("--ep", action="store_true",
+                    help="contrast baseline: the same stack as synchronous DP x EP (two on-path AllToAlls "
+                         "per layer, PAPER.md:196-199) instead of AsyncEP")
     ap.add_argument("--zipf", type=float, default=0.0, metavar="S",
                     help="Zipf-skewed routing (reading R14, BASELINE config 5 uses S=0.35)")
     ap.add_argument("--fp8", action="store_true",
@@ -233,6 +237,10 @@ def main():
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8)
     local_shards = stack.peer_shards() if emu > 1 else None
+    if args.ep:  # contrast layer: every rank keeps its shard; tokens travel instead of weights
+        _run = lambda xin, out: stack.run_ep(xin, out=out)
+    else:
+        _run = lambda xin, out: stack.run(xin, out=out, local_shards=local_shards)
     if emu > 1 and args.link_gbs > 0:
         A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
     # tokens: DP -- every rank its own batch
@@ -246,7 +254,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
-        stack.run(x, out=out, local_shards=local_shards)
+        _run(x, out)
     barrier()
     A.asyncep_reset_stage_times(stack.ctx)
     launches0 = A.asyncep_kernel_launches(stack.ctx)
@@ -256,7 +264,7 @@ def main():
     barrier()
     e0.record(cs)
     for _ in range(args.steps):
-        stack.run(x, out=out, local_shards=local_shards)
+        _run(x, out)
     e1.record(cs)
     barrier()
     clk = clocks.stop()
@@ -278,7 +286,7 @@ def main():
     xd = torch.empty_like(x)
     for _ in range(1):
         xd.copy_(xh, non_blocking=True)
-        stack.run(xd, out=out, local_shards=local_shards)
+        _run(xd, out)
         yh.copy_(out, non_blocking=True)
     barrier()
     f0 = torch.cuda.Event(enable_timing=True)
@@ -286,7 +294,7 @@ def main():
     f0.record(cs)
     for _ in range(args.steps):
         xd.copy_(xh, non_blocking=True)
-        stack.run(xd, out=out, local_shards=local_shards)
+        _run(xd, out)
         yh.copy_(out, non_blocking=True)
     f1.record(cs)
     barrier()
@@ -300,7 +308,7 @@ def main():
     # compute stream around each launch inside the timed region
     g1_ms = stages["gemm1_gateup_swiglu"] / max(nfwd, 1)
     g1_flops = GEMM1_FLOPS_TOK * T
-    g1_tflops = g1_flops / (g1_ms / 1e3) / 1e12
+    g1_tflops = g1_flops / (g1_ms / 1e3) / 1e12 if g1_ms > 0 else 0.0  # 0: no stage events (--ep)
     peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
     peak_note = f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)"
     spec = SPEC_BF16
@@ -328,7 +336,8 @@ def main():
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
-                   "parallelism": (f"dp{world}+asyncep{world}" if world > 1 else
+                   "parallelism": (f"dp{world}xep{world} contrast (2 on-path AllToAlls/layer)" if args.ep else
+                                   f"dp{world}+asyncep{world}" if world > 1 else
                                    f"dp1, asyncep{emu} gather emulated on 1 GPU (D2D copies of the {emu} shards "
                                    "into the slot on the comm stream" +
                                    (f", peer shards paced at {args.link_gbs} GB/s" if args.link_gbs else "") + ")"
@@ -345,12 +354,12 @@ def main():
                          "note": "Eq. 1 per layer, F = measured grouped-GEMM rate of this run"},
         "layer_ms": step_layer_ms,
         "exposed_ag": {"ms_per_layer": per_layer_ms["gather_wait"],
-                       "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms else None,
+                       "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms and nfwd else None,
                        "note": ("stream wait before GEMM1 on gathered layers (0 when N=1)" if not emu else
                                 f"emulated {emu}-rank gather (local D2D, no NVLink): exposed wait")},
         "roofline": {"kernel": "grouped GEMM1 gate/up + SwiGLU (tcgen05)", "bound": "tensor",
                      "achieved": g1_tflops, "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": g1_tflops / peak_tf,
+                     "frac": g1_tflops / peak_tf if g1_tflops else None,
                      "peak_source": peak_note,
                      "algorithmic_flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "traffic": traffic},

@@ -172,6 +172,38 @@ ASYNCEP_API asyncep_status asyncep_moe_forward(asyncep_ctx* ctx, int32_t layer, 
                                    int32_t* expert_counts_out);
 
 /*
+ * ---- Contrast baseline: synchronous DP x EP (Table 1 "DPxEP") ----
+ * Rank r permanently owns experts [r*E/N, (r+1)*E/N) of every layer and computes them for
+ * the tokens of ALL ranks: per layer, one AllToAll dispatches each rank's permuted rows to
+ * the owners of their experts and a second returns the expert outputs, both ON the critical
+ * path of the compute stream (versus AsyncEP's off-path weight gather).  BF16 experts only.
+ *
+ * asyncep_ep_plan (host, pure): from this rank's per-expert row counts (send_counts [E]) and
+ * the counts other ranks send to it (recv_counts [E]: source-major, E/N per source), the row
+ * ranges of the exchange; rows of every expert are padded to 256 (the GEMM pair tile):
+ *   send_off[d], send_rows[d]  : rows of this rank's X_perm going to rank d
+ *   recv_off[s], recv_rows[s]  : rows arriving from rank s in the receive buffer
+ *   group_off [E+1]            : receive-side row offset of group g = s*(E/N) + local expert
+ * Returns the total receive rows through recv_total.
+ */
+ASYNCEP_API asyncep_status asyncep_ep_plan(const asyncep_config* cfg, const int32_t* send_counts,
+                                           const int32_t* recv_counts, int64_t* send_off, int64_t* send_rows,
+                                           int64_t* recv_off, int64_t* recv_rows, int64_t* group_off,
+                                           int64_t* recv_total);
+/* device bytes of the EP receive workspace for up to max_recv_rows received rows */
+ASYNCEP_API size_t asyncep_ep_workspace_size(const asyncep_config* cfg, int64_t max_recv_rows);
+/*
+ * One synchronous DP x EP layer forward (host-synchronous: the exchanged counts are read back
+ * to size the variable AllToAlls, as an EP layer must).  Uses the context's NCCL communicator
+ * (ncclSend/ncclRecv groups on the compute stream; a device copy when world_size == 1 and no
+ * communicator is given) and this rank's shard of `layer`.  x, residual, y as in
+ * asyncep_moe_forward.  ERR_WORKSPACE if more than max_recv_rows rows arrive.
+ */
+ASYNCEP_API asyncep_status asyncep_ep_forward(asyncep_ctx* ctx, int32_t layer, const void* x, int64_t num_tokens,
+                                              const void* residual, void* y, void* ep_workspace,
+                                              int64_t max_recv_rows);
+
+/*
  * Saturation threshold, Eq. 1 in per-layer form (readings R11, R12):
  *   t_AG = (N-1)/N * E*3*H*h*b / ag_bytes_per_s;  T_FLOPs = gamma * t_AG * flops_per_s;
  *   T_tok = T_FLOPs / (6*k*H*h)  [tokens per GPU per layer].

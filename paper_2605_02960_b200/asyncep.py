@@ -79,6 +79,9 @@ def lib() -> ctypes.CDLL:
             "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
+            "asyncep_ep_plan": ([CP, P, P, P, P, P, P, P, ctypes.POINTER(I64)], I32),
+            "asyncep_ep_workspace_size": ([CP, I64], SZ),
+            "asyncep_ep_forward": ([P, I32, P, I64, P, P, P, I64], I32),
             "asyncep_destroy": ([P], I32),
         }
         for name, (args, res) in sig.items():
@@ -170,6 +173,38 @@ def asyncep_prefetch_layer(ctx: Context, layer: int) -> None:
 def asyncep_prefetch_layer_local(ctx: Context, layer: int, shards) -> None:
     arr = (ctypes.c_void_p * len(shards))(*[_p(t) for t in shards])
     _check(lib().asyncep_prefetch_layer_local(ctx.handle, layer, arr))
+
+
+def asyncep_ep_plan(cfg: Config, send_counts, recv_counts):
+    """Host-side row plan of the DP x EP exchange (see asyncep.h).  Counts: int32 numpy [E]."""
+    import numpy as np
+    N, E = cfg.world_size, cfg.num_experts
+    sc = np.ascontiguousarray(send_counts, dtype=np.int32)
+    rc = np.ascontiguousarray(recv_counts, dtype=np.int32)
+    out = {k: np.zeros(n, np.int64) for k, n in (("send_off", N), ("send_rows", N), ("recv_off", N),
+                                                    ("recv_rows", N), ("group_off", E + 1))}
+    tot = ctypes.c_int64()
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(lib().asyncep_ep_plan(ctypes.byref(cfg), vp(sc), vp(rc), vp(out["send_off"]), vp(out["send_rows"]),
+                                 vp(out["recv_off"]), vp(out["recv_rows"]), vp(out["group_off"]),
+                                 ctypes.byref(tot)))
+    out["recv_total"] = tot.value
+    return out
+
+
+def asyncep_ep_workspace_size(cfg: Config, max_recv_rows: int) -> int:
+    n = lib().asyncep_ep_workspace_size(ctypes.byref(cfg), max_recv_rows)
+    if n == 0:
+        _check(ERR_INVALID_ARG)
+    return n
+
+
+def asyncep_ep_forward(ctx: Context, layer: int, x, ep_workspace, max_recv_rows: int, residual=None, y=None):
+    if y is None:
+        y = torch.empty_like(x)
+    _check(lib().asyncep_ep_forward(ctx.handle, layer, _p(x), x.shape[0], _p(residual), _p(y), _p(ep_workspace),
+                                    max_recv_rows))
+    return y
 
 
 def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:

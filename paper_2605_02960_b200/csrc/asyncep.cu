@@ -44,10 +44,16 @@ asyncep_status fail(asyncep_status st, const char* fmt, ...) {
 typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
 typedef const char* (*nccl_errstr_fn)(int);
 typedef int (*nccl_async_err_fn)(void*, int*);
+typedef int (*nccl_p2p_fn)(const void*, size_t, int, int, void*, cudaStream_t);  // send: buf,count,type,peer
+typedef int (*nccl_recv_fn)(void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_group_fn)();
 struct NcclApi {
   nccl_allgather_fn allgather = nullptr;
   nccl_errstr_fn errstr = nullptr;
   nccl_async_err_fn async_err = nullptr;
+  nccl_p2p_fn send = nullptr;
+  nccl_recv_fn recv = nullptr;
+  nccl_group_fn group_start = nullptr, group_end = nullptr;
 };
 // the path of the libnccl the process already loaded (torch's wheel copy), so we bind to the
 // very library that created the borrowed communicator and never load a second NCCL
@@ -67,9 +73,14 @@ bool resolve_nccl(NcclApi& api) {
   api.allgather = (nccl_allgather_fn)dlsym(h, "ncclAllGather");
   api.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
   api.async_err = (nccl_async_err_fn)dlsym(h, "ncclCommGetAsyncError");
+  api.send = (nccl_p2p_fn)dlsym(h, "ncclSend");
+  api.recv = (nccl_recv_fn)dlsym(h, "ncclRecv");
+  api.group_start = (nccl_group_fn)dlsym(h, "ncclGroupStart");
+  api.group_end = (nccl_group_fn)dlsym(h, "ncclGroupEnd");
   return api.allgather != nullptr;
 }
 constexpr int kNcclUint8 = 1;
+constexpr int kNcclInt32 = 2;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -176,6 +187,8 @@ struct asyncep_ctx {
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   int64_t launches = 0;
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
+  std::vector<aep::GemmMaps> ep_maps;  // EP contrast: maps over this rank's shard of each layer
+  std::vector<char> ep_maps_ok;
 };
 
 namespace {
@@ -521,6 +534,196 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (ids_out) CUDA_TRY(cudaMemcpyAsync(ids_out, ids, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, st));
   if (w_out) CUDA_TRY(cudaMemcpyAsync(w_out, w, (size_t)T * k * 4, cudaMemcpyDeviceToDevice, st));
   if (counts_out) CUDA_TRY(cudaMemcpyAsync(counts_out, counts, (size_t)E * 4, cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaGetLastError());
+  return ASYNCEP_OK;
+}
+
+
+// ------------------------------------------------------------------ EP contrast layer
+namespace {
+int64_t pad_rows(int64_t n) { return (n + aep::kRowAlign - 1) / aep::kRowAlign * aep::kRowAlign; }
+
+struct EpWs {
+  size_t recv, act, offsets, tile_start, counts, rcounts, total;
+};
+EpWs ep_layout(const asyncep_config& c, int64_t max_recv_rows) {
+  EpWs L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  const size_t R = (size_t)pad_rows(max_recv_rows);
+  L.recv = take(R * (size_t)c.hidden * 2);  // received X rows, then the expert outputs (Y)
+  L.act = take(R * (size_t)c.ffn * 2);
+  L.offsets = take(((size_t)c.num_experts + 1) * 4);
+  L.tile_start = take(((size_t)c.num_experts + 1) * 4);
+  L.counts = take((size_t)c.num_experts * 4);
+  L.rcounts = take((size_t)c.num_experts * 4);
+  L.total = o;
+  return L;
+}
+}  // namespace
+
+asyncep_status asyncep_ep_plan(const asyncep_config* cfg, const int32_t* sc, const int32_t* rc, int64_t* send_off,
+                               int64_t* send_rows, int64_t* recv_off, int64_t* recv_rows, int64_t* group_off,
+                               int64_t* recv_total) {
+  if (!cfg || !sc || !rc) return fail(ASYNCEP_ERR_INVALID_ARG, "null argument");
+  const int E = cfg->num_experts, N = cfg->world_size;
+  if (N <= 0 || E % N) return fail(ASYNCEP_ERR_INVALID_ARG, "E %% N != 0");
+  const int per = E / N;
+  // send side: this rank's X_perm lays experts out in order, each padded to kRowAlign, so
+  // the rows for rank d are one contiguous range
+  int64_t o = 0;
+  for (int d = 0; d < N; ++d) {
+    int64_t n = 0;
+    for (int j = 0; j < per; ++j) n += pad_rows(sc[d * per + j]);
+    if (send_off) send_off[d] = o;
+    if (send_rows) send_rows[d] = n;
+    o += n;
+  }
+  // receive side: source-major, each source's chunk expert-ordered and padded the same way
+  int64_t r = 0;
+  for (int s = 0; s < N; ++s) {
+    int64_t n = 0;
+    for (int j = 0; j < per; ++j) {
+      if (group_off) group_off[s * per + j] = r + n;
+      n += pad_rows(rc[s * per + j]);
+    }
+    if (recv_off) recv_off[s] = r;
+    if (recv_rows) recv_rows[s] = n;
+    r += n;
+  }
+  if (group_off) group_off[E] = r;
+  if (recv_total) *recv_total = r;
+  return ASYNCEP_OK;
+}
+
+size_t asyncep_ep_workspace_size(const asyncep_config* cfg, int64_t max_recv_rows) {
+  if (check_config(cfg) != ASYNCEP_OK || max_recv_rows <= 0) return 0;
+  return ep_layout(*cfg, max_recv_rows).total;
+}
+
+asyncep_status asyncep_ep_forward(asyncep_ctx* c, int32_t layer, const void* x, int64_t T, const void* residual,
+                                  void* y, void* ep_ws, int64_t max_recv_rows) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  const asyncep_config& cf = c->cfg;
+  if (layer < 0 || layer >= cf.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
+  if (cf.expert_dtype != ASYNCEP_BF16) return fail(ASYNCEP_ERR_UNSUPPORTED, "EP contrast layer is BF16 only");
+  if (T < 0 || T > cf.max_tokens) return fail(ASYNCEP_ERR_WORKSPACE, "num_tokens out of range");
+  if (T == 0) return ASYNCEP_OK;
+  if (!x || !y || !ep_ws || max_recv_rows <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "null argument");
+  if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual | (uintptr_t)ep_ws) & 15)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "pointers must be 16-B aligned");
+  const int N = cf.world_size, E = cf.num_experts, per = E / N, k = cf.top_k, H = cf.hidden, h = cf.ffn;
+  if (N > 1 && (!c->comm || !c->nccl.send || !c->nccl.recv))
+    return fail(ASYNCEP_ERR_NCCL, "EP contrast with world_size > 1 needs an NCCL communicator");
+  cudaStream_t st = c->cs;
+  uint8_t* ws = c->ws;
+  const EpWs EL = ep_layout(cf, max_recv_rows);
+  uint8_t* ew = (uint8_t*)ep_ws;
+  // this rank's shard of the layer: E/N expert blobs
+  if (c->ep_maps.empty()) {
+    c->ep_maps.resize(cf.num_layers);
+    c->ep_maps_ok.assign(cf.num_layers, 0);
+  }
+  const bool full = layer_resident(c, layer) && N > 1;  // a full layer: take this rank's part
+  const uint8_t* wl = (const uint8_t*)c->shard[layer] + (full ? (size_t)cf.rank * c->shard_bytes : 0);
+  if (!c->ep_maps_ok[layer]) {
+    if (!aep::make_weight_maps(c->ep_maps[layer], wl, c->expert_bytes, per, H, h, c->act_maps.bn2, false))
+      return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (EP shard maps)");
+    c->ep_maps_ok[layer] = 1;
+  }
+  int32_t* ids = (int32_t*)(ws + c->L.ids);
+  float* w = (float*)(ws + c->L.w);
+  int32_t* dest = (int32_t*)(ws + c->L.dest);
+  int32_t* src_tok = (int32_t*)(ws + c->L.src_tok);
+  int32_t* blk = (int32_t*)(ws + c->L.blk);
+  int32_t* offsets = (int32_t*)(ws + c->L.offsets);
+  int32_t* tile_start = (int32_t*)(ws + c->L.tile_start);
+  int32_t* counts = (int32_t*)(ws + c->L.counts);
+  bf16* xperm = (bf16*)(ws + c->L.xperm);
+  int* sched = (int*)(ws + c->L.sched);
+  const int nblk = (int)((T + aep::kPermTokensPerBlock - 1) / aep::kPermTokensPerBlock);
+  CUDA_TRY(cudaMemsetAsync(sched, 0, 16, st));
+  // (1) router + (2) local permute, as in the AsyncEP forward
+  if (!aep::launch_router_tc(c->router_maps[layer], (const bf16*)x, T, H, E, k, cf.norm_topk, ids, w, c->num_sms,
+                             st, sched))
+    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router x map)");
+  aep::launch_perm_hist(ids, T, k, E, blk, st);
+  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
+  aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok, xperm, st);
+  c->launches += 4;
+  // (a) exchange the per-expert counts (E/N to every rank), read them back: host sync
+  int32_t* d_rc = (int32_t*)(ew + EL.rcounts);
+  if (N > 1) {
+    c->nccl.group_start();
+    for (int d = 0; d < N; ++d) {
+      c->nccl.send(counts + d * per, (size_t)per, kNcclInt32, d, c->comm, st);
+      c->nccl.recv(d_rc + d * per, (size_t)per, kNcclInt32, d, c->comm, st);
+    }
+    if (c->nccl.group_end() != 0) return fail(ASYNCEP_ERR_NCCL, "count exchange failed");
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(d_rc, counts, (size_t)E * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  std::vector<int32_t> hsc(E), hrc(E);
+  CUDA_TRY(cudaMemcpyAsync(hsc.data(), counts, (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hrc.data(), d_rc, (size_t)E * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int64_t> so(N), sr(N), ro(N), rr(N), go(E + 1);
+  int64_t rtot = 0;
+  asyncep_status ps = asyncep_ep_plan(&cf, hsc.data(), hrc.data(), so.data(), sr.data(), ro.data(), rr.data(),
+                                      go.data(), &rtot);
+  if (ps) return ps;
+  if (rtot > pad_rows(max_recv_rows))
+    return fail(ASYNCEP_ERR_WORKSPACE, "EP receive rows %lld > capacity %lld", (long long)rtot,
+                (long long)max_recv_rows);
+  // receive-side group table (groups = (source rank, local expert))
+  std::vector<int32_t> g_off(E + 1), g_ts(E + 1);
+  for (int g = 0; g <= E; ++g) {
+    g_off[g] = (int32_t)go[g];
+    g_ts[g] = (int32_t)(go[g] / aep::kRowAlign);
+  }
+  int32_t* d_goff = (int32_t*)(ew + EL.offsets);
+  int32_t* d_gts = (int32_t*)(ew + EL.tile_start);
+  CUDA_TRY(cudaMemcpyAsync(d_goff, g_off.data(), (size_t)(E + 1) * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_gts, g_ts.data(), (size_t)(E + 1) * 4, cudaMemcpyHostToDevice, st));
+  // (b) dispatch AllToAll of the permuted rows (on the critical path)
+  bf16* recv = (bf16*)(ew + EL.recv);
+  const size_t row_b = (size_t)H * 2;
+  auto exchange = [&](const bf16* sbuf, const std::vector<int64_t>& soff, const std::vector<int64_t>& srows,
+                      bf16* rbuf, const std::vector<int64_t>& roff, const std::vector<int64_t>& rrows) -> asyncep_status {
+    if (N > 1) {
+      c->nccl.group_start();
+      for (int d = 0; d < N; ++d) {
+        if (srows[d]) c->nccl.send(sbuf + soff[d] * H, (size_t)srows[d] * row_b, kNcclUint8, d, c->comm, st);
+        if (rrows[d]) c->nccl.recv(rbuf + roff[d] * H, (size_t)rrows[d] * row_b, kNcclUint8, d, c->comm, st);
+      }
+      if (c->nccl.group_end() != 0) return fail(ASYNCEP_ERR_NCCL, "AllToAll failed");
+    } else if (srows[0]) {
+      CUDA_TRY(cudaMemcpyAsync(rbuf + roff[0] * H, sbuf + soff[0] * H, (size_t)srows[0] * row_b,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    return ASYNCEP_OK;
+  };
+  asyncep_status xs = exchange(xperm, so, sr, recv, ro, rr);
+  if (xs) return xs;
+  // (c) this rank's experts on the rows of all ranks: groups g -> expert g % (E/N)
+  aep::ActMaps am{};
+  bf16* act = (bf16*)(ew + EL.act);
+  if (!aep::make_act_maps(am, recv, act, std::max<int64_t>(rtot, aep::kRowAlign), H, h, nullptr, nullptr))
+    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (EP activations)");
+  aep::GroupedArgs g{d_goff, d_gts, nullptr, E, (int)(rtot / aep::kRowAlign), sched, per};
+  aep::launch_gemm1_tc(g, am, c->ep_maps[layer], H, h, act, nullptr, rtot, nullptr, c->num_sms, st);
+  aep::launch_gemm2_tc(g, am, c->ep_maps[layer], H, h, recv, c->num_sms, st);
+  c->launches += 2;
+  // (d) combine AllToAll: expert outputs back to their tokens' ranks, into X_perm's rows
+  xs = exchange(recv, ro, rr, xperm, so, sr);
+  if (xs) return xs;
+  // (e) weighted combine (+ residual)
+  aep::launch_combine(xperm, dest, w, (const bf16*)residual, (bf16*)y, T, H, k, st);
+  c->launches += 1;
   CUDA_TRY(cudaGetLastError());
   return ASYNCEP_OK;
 }

@@ -74,6 +74,8 @@ struct TcArgs {
   size_t expert_bytes;
   uint32_t* amax_out;           // GEMM1 FP8: per-row max |act| (fp32 bits, atomicMax)
   int* sched;                   // dynamic tile counter (zeroed before the launch)
+  int group_mod;                // > 0: B expert = group % group_mod (EP contrast: groups are
+                                // (source rank, local expert) pairs over a shard of group_mod experts)
   const int32_t* gather_rows;  // non-null: A rows are gathered from the token matrix (map_a is a
                                // {H, T} gather4 map) with row ids gather_rows[permuted row]
   // router epilogue
@@ -314,7 +316,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (t >= total) break;
         int mt, nt;
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
-        const int e = find_expert(s_ts, G, mt);
+        int e = find_expert(s_ts, G, mt);
+        if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
         const int row0 = mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
         int4 rows = make_int4(0, 0, 0, 0);
@@ -416,8 +419,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float* sb = nullptr;
         if (F8) {
           sa = p.a_scale[wrow0 + lane];
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)find_expert(s_ts, G, mt) * p.expert_bytes) +
-               nt * 256;
+          int ge = find_expert(s_ts, G, mt);
+          if (p.group_mod > 0) ge %= p.group_mod;
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256;
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 64) {
@@ -452,8 +456,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float* sb = nullptr;
         if (F8) {
           sa = p.a_scale[wrow0 + lane];
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)find_expert(s_ts, G, mt) * p.expert_bytes) +
-               nt * p.BN;
+          int ge = find_expert(s_ts, G, mt);
+          if (p.group_mod > 0) ge %= p.group_mod;
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN;
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < p.BN; c0 += 64) {
@@ -551,6 +556,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
   a.gather_rows = gather_rows;
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
+  a.group_mod = g.group_mod;
   if (f8) {
     a.a_scale = gemm2 ? f8->act_scale : f8->x_scale;
     a.b_scale_base = f8->layer + (gemm2 ? f8->sd_off : f8->sgu_off);

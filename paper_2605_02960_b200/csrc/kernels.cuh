@@ -61,6 +61,7 @@ struct GroupedArgs {
   int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
   int* sched = nullptr;      // [>= 3] dynamic tile counters, zeroed before each forward:
                              // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
+  int group_mod = 0;         // > 0: group g uses expert g % group_mod of the weight blob
 };
 // rows of the permuted buffers for T tokens: T*k + E*(kRowAlign-1), rounded up to kRowAlign
 inline int64_t perm_rows(int64_t T, int k, int E) {

@@ -117,6 +117,28 @@ class MoEStack:
             cur = dst
         return cur
 
+    def run_ep(self, x, residual=True, out=None, recv_factor: float = 2.0):
+        """Contrast baseline: the same stack as synchronous DP x EP: each
+        layer dispatches its permuted rows to the owners of their experts and returns the
+        outputs with two on-path AllToAlls (asyncep_ep_forward).  recv_factor sizes the
+        receive buffer in units of this rank's own rows (dropless within it)."""
+        T = x.shape[0]
+        cap = int(recv_factor * self.cfg.max_tokens * self.k) + self.E * 256
+        if getattr(self, "_ep_ws", None) is None or self._ep_cap < cap:
+            self._ep_ws = torch.empty(A.asyncep_ep_workspace_size(self.cfg, cap), dtype=torch.uint8,
+                                      device=self.device)
+            self._ep_cap = cap
+        if self._bufs is None or self._bufs[0].shape[0] < T:
+            self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
+                          for _ in range(2)]
+        cur = x
+        for l in range(self.L):
+            dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
+            A.asyncep_ep_forward(self.ctx, l, cur, self._ep_ws, self._ep_cap, residual=cur if residual else None,
+                                 y=dst)
+            cur = dst
+        return cur
+
     def calibrate_T(self, x, gamma: float | None = None, local_shards=None):
         """NEXT-1, App. B.4: one profile pass of the stack at
         n_ref = len(x) tokens with per-forward CUDA-event timing; t_c = wall time of the

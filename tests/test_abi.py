@@ -87,3 +87,19 @@ def test_calibrated_T_matches_oracle(A):
     assert A.asyncep_calibrated_T(1.2, 2.0, 1.0, 1e12) == pytest.approx(2.4e12, rel=1e-15)
     with pytest.raises(A.AsyncEPError):
         A.asyncep_calibrated_T(0.9, 1.0, 1.0, 1.0)
+
+
+def test_ep_plan_layout(A):
+    """DP x EP exchange plan: rank d's experts are one contiguous padded
+    range of the sender's X_perm; the receive buffer is source-major, expert-ordered."""
+    import numpy as np
+    cfg = A.make_config(1, 8, 2, 256, 256, world_size=4, rank=1, max_tokens=1024)
+    sc = np.array([5, 0, 300, 256, 1, 2, 0, 513], np.int32)
+    rc = np.array([1, 2, 3, 4, 0, 0, 257, 255], np.int32)
+    p = A.asyncep_ep_plan(cfg, sc, rc)
+    pad = lambda n: (n + 255) // 256 * 256
+    assert list(p["send_rows"]) == [pad(5) + pad(0), pad(300) + pad(256), pad(1) + pad(2), pad(0) + pad(513)]
+    assert list(p["send_off"]) == list(np.concatenate([[0], np.cumsum(p["send_rows"])[:-1]]))
+    assert list(p["recv_rows"]) == [pad(1) + pad(2), pad(3) + pad(4), 0, pad(257) + pad(255)]
+    assert p["group_off"][-1] == p["recv_total"] == sum(p["recv_rows"])
+    assert all(o % 256 == 0 for o in p["group_off"])

@@ -185,3 +185,16 @@ def test_nccl_allgather_path_with_borrowed_torch_comm():
         assert torch.all(st.slots[1][half:] == 0xAB)  # the absent rank's half is untouched
     finally:
         dist.destroy_process_group()
+
+
+def test_ep_contrast_layer_matches_asyncep_forward():
+    """The synchronous DP x EP contrast layer (world_size 1: local exchange) computes the
+    same layer bit for bit as the AsyncEP forward (same tiles, same K order)."""
+    wl = Workload(L=2, E=16, k=4, H=256, h=256, seed=18)
+    T = 777
+    x = wl.tokens(T)
+    st = wl.stack(max_tokens=T)
+    ref = st.run(x).clone()
+    out = st.run_ep(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
