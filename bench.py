@@ -199,6 +199,8 @@ def main():
     ap.add_argument("--ep", action="store_true",
                     help="contrast baseline: the same stack as synchronous DP x EP (two on-path AllToAlls "
                          "per layer, PAPER.md:196-199) instead of AsyncEP")
+    ap.add_argument("--offload", type=int, default=0, metavar="W",
+                    help="NEXT-2: expert shards in pinned host memory, a W-deep device window filled over PCIe")
     ap.add_argument("--zipf", type=float, default=0.0, metavar="S",
                     help="Zipf-skewed routing (reading R14, BASELINE config 5 uses S=0.35)")
     ap.add_argument("--fp8", action="store_true",
@@ -235,7 +237,7 @@ def main():
                      lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf),
                      lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex),
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
-                     nccl_comm=comm, fp8=args.fp8)
+                     nccl_comm=comm, fp8=args.fp8, offload_window=args.offload)
     local_shards = stack.peer_shards() if emu > 1 else None
     if args.ep:  # contrast layer: every rank keeps its shard; tokens travel instead of weights
         _run = lambda xin, out: stack.run_ep(xin, out=out)
@@ -341,7 +343,9 @@ def main():
                                    f"dp1, asyncep{emu} gather emulated on 1 GPU (D2D copies of the {emu} shards "
                                    "into the slot on the comm stream" +
                                    (f", peer shards paced at {args.link_gbs} GB/s" if args.link_gbs else "") + ")"
-                                   if emu > 1 else "dp1 (all experts resident)"),
+                                   if emu > 1 else "dp1 (all experts resident)") +
+                                  (f", shards offloaded to pinned host memory, {args.offload}-deep device window "
+                                   "(NEXT-2)" if args.offload else ""),
                    "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,

@@ -62,6 +62,7 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
 #define ASYNCEP_FLAG_STAGE_TIMING     0x4 /* record CUDA events around each stage (asyncep_stage_times) */
 #define ASYNCEP_FLAG_SIMT_ROUTER      0x8 /* CUDA-core router logits instead of tcgen05                */
 #define ASYNCEP_FLAG_GATHER_A        0x10 /* GEMM1 gathers token rows with TMA gather4 (no X_perm)     */
+#define ASYNCEP_FLAG_OFFLOAD         0x20 /* NEXT-2: expert_shard[l] may be NULL for offloaded layers  */
 
 typedef struct {
   int32_t num_layers;      /* L                                                         */
@@ -146,6 +147,24 @@ ASYNCEP_API asyncep_status asyncep_prefetch_layer(asyncep_ctx* ctx, int32_t laye
  */
 ASYNCEP_API asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* ctx, int32_t layer,
                                             const void* const* shards);
+
+/*
+ * ---- NEXT-2: hybrid weight offload (PAPER.md:343-349 "two-channel pipeline", :630 "H2D
+ * offloader") ----
+ * The expert shards of layers >= 1 live in pinned host memory (host_shards[l], asyncep_shard_bytes
+ * each; the full layer, asyncep_slot_bytes, when world_size == 1); only a sliding window of w
+ * device buffers (window[i], same size) holds upcoming shards.  asyncep_stage_layer(l) copies
+ * layer l's shard host->device into window[l % w] on h2d_stream, after the window buffer's
+ * previous occupant (layer l - w) has been read (by its AllGather, or by its forward when
+ * world_size == 1), and records h2d_done.  asyncep_prefetch_layer(l) then gathers from the
+ * window (waiting h2d_done on the comm stream); with world_size == 1 the forward reads the
+ * window buffer directly.  Layer 0 stays resident (replicated) as before.
+ * The two channels (NVLink gather of l+1, PCIe staging of l+2..l+w) run concurrently, and
+ * t_EP = max(t_AG, t_H2D).  Pinned host memory and window buffers are caller-owned.
+ */
+ASYNCEP_API asyncep_status asyncep_enable_offload(asyncep_ctx* ctx, const void* const* host_shards,
+                                                  void* const* window, int32_t w, void* h2d_stream);
+ASYNCEP_API asyncep_status asyncep_stage_layer(asyncep_ctx* ctx, int32_t layer);
 
 /*
  * Test / measurement hook for asyncep_prefetch_layer_local: pace the copies of the OTHER

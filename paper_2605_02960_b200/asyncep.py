@@ -25,6 +25,7 @@ FLAG_SIMT_GEMM = 0x2
 FLAG_STAGE_TIMING = 0x4
 FLAG_SIMT_ROUTER = 0x8
 FLAG_GATHER_A = 0x10
+FLAG_OFFLOAD = 0x20
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 
 
@@ -79,6 +80,8 @@ def lib() -> ctypes.CDLL:
             "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
+            "asyncep_enable_offload": ([P, P, P, I32, P], I32),
+            "asyncep_stage_layer": ([P, I32], I32),
             "asyncep_ep_plan": ([CP, P, P, P, P, P, P, P, ctypes.POINTER(I64)], I32),
             "asyncep_ep_workspace_size": ([CP, I64], SZ),
             "asyncep_ep_forward": ([P, I32, P, I64, P, P, P, I64], I32),
@@ -205,6 +208,18 @@ def asyncep_ep_forward(ctx: Context, layer: int, x, ep_workspace, max_recv_rows:
     _check(lib().asyncep_ep_forward(ctx.handle, layer, _p(x), x.shape[0], _p(residual), _p(y), _p(ep_workspace),
                                     max_recv_rows))
     return y
+
+
+def asyncep_enable_offload(ctx: Context, host_shards, window, w: int, h2d_stream) -> None:
+    L = ctx.cfg.num_layers
+    hs = (ctypes.c_void_p * L)(*[_p(t) for t in host_shards])
+    wb = (ctypes.c_void_p * w)(*[_p(t) for t in window])
+    _check(lib().asyncep_enable_offload(ctx.handle, hs, wb, w, _stream(h2d_stream)))
+    ctx.keep += [list(host_shards), list(window), h2d_stream]
+
+
+def asyncep_stage_layer(ctx: Context, layer: int) -> None:
+    _check(lib().asyncep_stage_layer(ctx.handle, layer))
 
 
 def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:

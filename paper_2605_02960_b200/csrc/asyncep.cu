@@ -189,6 +189,16 @@ struct asyncep_ctx {
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
   std::vector<aep::GemmMaps> ep_maps;  // EP contrast: maps over this rank's shard of each layer
   std::vector<char> ep_maps_ok;
+  // NEXT-2 offload: host backing store + w-deep device window
+  bool offload = false;
+  int w = 0;
+  cudaStream_t hs = nullptr;
+  std::vector<const void*> host_shard;
+  std::vector<void*> window;
+  std::vector<cudaEvent_t> h2d_done, win_free;
+  std::vector<int> win_layer;
+  std::vector<char> win_consumed;
+  std::vector<aep::GemmMaps> win_maps;  // world_size == 1: the forward reads the window
 };
 
 namespace {
@@ -274,8 +284,12 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   *out = nullptr;
   if ((uintptr_t)workspace & 255) return fail(ASYNCEP_ERR_INVALID_ARG, "workspace must be 256-B aligned");
   const int L = cfg->num_layers;
+  const bool offload = (cfg->flags & ASYNCEP_FLAG_OFFLOAD) != 0;
   for (int l = 0; l < L; ++l) {
-    if (!router_w[l] || !expert_shard[l]) return fail(ASYNCEP_ERR_INVALID_ARG, "null weight pointer (layer %d)", l);
+    // offloaded layers (every layer >= 1 at N == 1, every gathered layer at N > 1) live on the host
+    const bool host_only = offload && (cfg->world_size == 1 ? l > 0 : !(l == 0 && cfg->replicate_layer0));
+    if (!router_w[l] || (!expert_shard[l] && !host_only))
+      return fail(ASYNCEP_ERR_INVALID_ARG, "null weight pointer (layer %d)", l);
     if (((uintptr_t)router_w[l] | (uintptr_t)expert_shard[l]) & 15)
       return fail(ASYNCEP_ERR_INVALID_ARG, "weights must be 16-B aligned (layer %d)", l);
   }
@@ -332,7 +346,7 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   c->layer_maps.resize(L);
   c->resident.assign(L, 0);
   for (int l = 0; l < L; ++l) {
-    if (!layer_resident(c, l)) continue;
+    if (!layer_resident(c, l) || !c->shard[l]) continue;
     c->resident[l] = 1;
     if (!aep::make_weight_maps(c->layer_maps[l], c->shard[l], c->expert_bytes, cfg->num_experts, cfg->hidden,
                                cfg->ffn, c->act_maps.bn2, fp8))
@@ -361,12 +375,21 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
                 c->slot_layer[s]);
   // WAR: the slot's previous occupant must have finished its GEMMs.
   CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
+  const void* own = c->shard[layer];
+  int wi = -1;
+  if (c->offload) {  // the own shard comes from the H2D window (staged by asyncep_stage_layer)
+    wi = layer % c->w;
+    if (c->win_layer[wi] != layer || c->win_consumed[wi])
+      return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not staged (asyncep_stage_layer)", layer);
+    CUDA_TRY(cudaStreamWaitEvent(c->ms, c->h2d_done[wi], 0));
+    own = c->window[wi];
+  }
   if (shards) {
     constexpr size_t kChunk = (size_t)64 << 20;
     for (int r = 0; r < c->cfg.world_size; ++r) {
       if (!shards[r]) return fail(ASYNCEP_ERR_INVALID_ARG, "null shard %d", r);
       uint8_t* dst = (uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes;
-      const uint8_t* src = (const uint8_t*)shards[r];
+      const uint8_t* src = (const uint8_t*)(r == c->cfg.rank && c->offload ? own : shards[r]);
       const bool paced = c->link_bps > 0 && r != c->cfg.rank;  // own shard is a local copy
       for (size_t o = 0; o < c->shard_bytes; o += kChunk) {
         const size_t n = std::min(kChunk, c->shard_bytes - o);
@@ -379,13 +402,71 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     }
   } else {
     if (!c->comm) return fail(ASYNCEP_ERR_NCCL, "no NCCL communicator (use asyncep_prefetch_layer_local)");
-    const int r = c->nccl.allgather(c->shard[layer], c->slot[s], c->shard_bytes, kNcclUint8, c->comm, c->ms);
+    const int r = c->nccl.allgather(own, c->slot[s], c->shard_bytes, kNcclUint8, c->comm, c->ms);
     if (r != 0)
       return fail(ASYNCEP_ERR_NCCL, "ncclAllGather: %s", c->nccl.errstr ? c->nccl.errstr(r) : "error");
   }
   CUDA_TRY(cudaEventRecord(c->ag_done[s], c->ms));
+  if (wi >= 0) {  // the gather has read the window buffer: it may be re-staged
+    CUDA_TRY(cudaEventRecord(c->win_free[wi], c->ms));
+    c->win_consumed[wi] = true;
+  }
   c->slot_layer[s] = layer;
   c->slot_consumed[s] = false;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_enable_offload(asyncep_ctx* c, const void* const* host_shards, void* const* window, int32_t w,
+                                      void* h2d_stream) {
+  if (!c || !host_shards || !window || w < 1 || !h2d_stream) return fail(ASYNCEP_ERR_INVALID_ARG, "bad arguments");
+  if (c->offload) return fail(ASYNCEP_ERR_INVALID_ARG, "offload already enabled");
+  const asyncep_config& cf = c->cfg;
+  const size_t bytes = cf.world_size == 1 ? c->slot_bytes : c->shard_bytes;
+  c->host_shard.assign(cf.num_layers, nullptr);
+  for (int l = 0; l < cf.num_layers; ++l) {
+    const bool needs = cf.world_size == 1 ? l > 0 : !layer_resident(c, l);
+    if (needs && !host_shards[l]) return fail(ASYNCEP_ERR_INVALID_ARG, "null host shard (layer %d)", l);
+    c->host_shard[l] = host_shards[l];
+  }
+  c->window.assign(window, window + w);
+  for (int i = 0; i < w; ++i)
+    if (!window[i] || ((uintptr_t)window[i] & 15)) return fail(ASYNCEP_ERR_INVALID_ARG, "bad window buffer %d", i);
+  c->h2d_done.assign(w, nullptr);
+  c->win_free.assign(w, nullptr);
+  for (int i = 0; i < w; ++i) {
+    CUDA_TRY(cudaEventCreateWithFlags(&c->h2d_done[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->win_free[i], cudaEventDisableTiming));
+  }
+  c->win_layer.assign(w, -1);
+  c->win_consumed.assign(w, 1);
+  if (cf.world_size == 1) {
+    c->win_maps.resize(w);
+    for (int i = 0; i < w; ++i)
+      if (!aep::make_weight_maps(c->win_maps[i], window[i], c->expert_bytes, cf.num_experts, cf.hidden, cf.ffn,
+                                 c->act_maps.bn2, cf.expert_dtype == ASYNCEP_FP8_E4M3))
+        return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (window %d)", i);
+  }
+  c->w = w;
+  c->hs = (cudaStream_t)h2d_stream;
+  c->offload = true;
+  (void)bytes;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_stage_layer(asyncep_ctx* c, int32_t layer) {
+  if (!c || !c->offload) return fail(ASYNCEP_ERR_INVALID_ARG, "offload not enabled");
+  if (layer < 0 || layer >= c->cfg.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
+  const bool n1 = c->cfg.world_size == 1;
+  if (n1 ? layer == 0 : layer_resident(c, layer)) return ASYNCEP_OK;  // resident: nothing to stage
+  const int i = layer % c->w;
+  if (!c->win_consumed[i] && c->win_layer[i] != layer)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "window %d still holds layer %d, not yet consumed", i, c->win_layer[i]);
+  CUDA_TRY(cudaStreamWaitEvent(c->hs, c->win_free[i], 0));  // WAR vs the previous occupant's reader
+  CUDA_TRY(cudaMemcpyAsync(c->window[i], c->host_shard[layer], n1 ? c->slot_bytes : c->shard_bytes,
+                           cudaMemcpyHostToDevice, c->hs));
+  CUDA_TRY(cudaEventRecord(c->h2d_done[i], c->hs));
+  c->win_layer[i] = layer;
+  c->win_consumed[i] = false;
   return ASYNCEP_OK;
 }
 
@@ -417,9 +498,13 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "x / y / residual must be 16-B aligned");
   if (x == y) return fail(ASYNCEP_ERR_INVALID_ARG, "y must not alias x");
-  const bool res = layer_resident(c, layer);
+  const bool from_window = c->offload && cf.world_size == 1 && layer > 0;  // NEXT-2, N == 1
+  const bool res = !from_window && layer_resident(c, layer);
   const int s = layer % 2;
-  if (!res && (c->slot_layer[s] != layer || c->slot_consumed[s]))
+  const int wi = from_window ? layer % c->w : -1;
+  if (from_window && (c->win_layer[wi] != layer || c->win_consumed[wi]))
+    return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not staged (asyncep_stage_layer)", layer);
+  if (!res && !from_window && (c->slot_layer[s] != layer || c->slot_consumed[s]))
     return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not prefetched", layer);
 
   const int E = cf.num_experts, k = cf.top_k, H = cf.hidden, h = cf.ffn;
@@ -491,11 +576,12 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
   // wait for this layer's gathered experts (placed just before GEMM1 so router and
   // permute also overlap the gather tail)
-  if (!res) CUDA_TRY(cudaStreamWaitEvent(st, c->ag_done[s], 0));
+  if (from_window) CUDA_TRY(cudaStreamWaitEvent(st, c->h2d_done[wi], 0));
+  else if (!res) CUDA_TRY(cudaStreamWaitEvent(st, c->ag_done[s], 0));
   if (timing) CUDA_TRY(cudaEventRecord(ev[3], st));
   // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
-  const uint8_t* wl = (const uint8_t*)(res ? c->shard[layer] : c->slot[s]);
-  const aep::GemmMaps& wm = res ? c->layer_maps[layer] : c->slot_maps[s];
+  const uint8_t* wl = (const uint8_t*)(from_window ? c->window[wi] : res ? c->shard[layer] : c->slot[s]);
+  const aep::GemmMaps& wm = from_window ? c->win_maps[wi] : res ? c->layer_maps[layer] : c->slot_maps[s];
   aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
@@ -523,7 +609,10 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   }
   if (timing && (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS)) CUDA_TRY(cudaEventRecord(ev[4], st));
   if (timing) CUDA_TRY(cudaEventRecord(ev[5], st));
-  if (!res) {
+  if (from_window) {
+    CUDA_TRY(cudaEventRecord(c->win_free[wi], st));
+    c->win_consumed[wi] = true;
+  } else if (!res) {
     CUDA_TRY(cudaEventRecord(c->slot_free[s], st));
     c->slot_consumed[s] = true;
   }
@@ -798,6 +887,10 @@ asyncep_status asyncep_destroy(asyncep_ctx* c) {
     if (c->slot_free[i]) cudaEventDestroy(c->slot_free[i]);
   }
   for (auto& e : c->ev_pool)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->h2d_done)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->win_free)
     if (e) cudaEventDestroy(e);
   delete c;
   return ASYNCEP_OK;

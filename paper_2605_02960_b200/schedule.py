@@ -26,28 +26,69 @@ def layer_resident(l: int, N: int, replicate_layer0: bool = True) -> bool:
     return N == 1 or (l == 0 and replicate_layer0)
 
 
-def stack_schedule(L: int, N: int, replicate_layer0: bool = True):
+def staged_layers(L: int, N: int, replicate_layer0: bool = True):
+    """NEXT-2 offload: layers whose shard comes from the host window:
+    every layer >= 1 at N == 1, every gathered layer at N > 1."""
+    return [l for l in range(L) if (l > 0 if N == 1 else not layer_resident(l, N, replicate_layer0))]
+
+
+def stack_schedule(L: int, N: int, replicate_layer0: bool = True, offload_w: int = 0):
     """Issue order of one pass over an L-layer stack: a list of ("prefetch", l, slot) and
-    ("forward", l, slot) with slot = l % 2 for gathered layers, -1 for resident ones."""
+    ("forward", l, slot) with slot = l % 2 for gathered layers, -1 for resident ones; with a
+    host-offload window of offload_w shards also ("stage", l, l % offload_w): the PCIe
+    channel runs up to offload_w layers ahead of the layer being gathered (or, at N == 1,
+    computed), and a window buffer is re-staged right after its layer has been read."""
     ops = []
     slot = lambda l: -1 if layer_resident(l, N, replicate_layer0) else l % 2
+    todo = staged_layers(L, N, replicate_layer0) if offload_w else []
+    nxt = 0
+
+    def stage_next():
+        nonlocal nxt
+        if nxt < len(todo):
+            ops.append(("stage", todo[nxt], todo[nxt] % offload_w))
+            nxt += 1
+
+    for _ in range(min(offload_w, len(todo))):
+        stage_next()
     if not layer_resident(0, N, replicate_layer0):
         ops.append(("prefetch", 0, 0))
+        if 0 in todo:
+            stage_next()
     for l in range(L):
         if l + 1 < L and not layer_resident(l + 1, N, replicate_layer0):
             ops.append(("prefetch", l + 1, slot(l + 1)))   # overlaps forward(l)
+            if N > 1 and (l + 1) in todo:
+                stage_next()                                  # its window buffer was read
         ops.append(("forward", l, slot(l)))
+        if N == 1 and l in todo:
+            stage_next()                                      # forward(l) read its window buffer
     return ops
 
 
-def check_schedule(ops, L: int) -> None:
+def check_schedule(ops, L: int, N: int = 2, offload_w: int = 0) -> None:
     """Invariants of the double buffer: every gathered forward(l) reads a slot that holds
     layer l; a slot is re-filled only after the forward of its previous layer; at most two
-    gathered layers are in flight.  Raises AssertionError on violation."""
+    gathered layers are in flight.  With an offload window: a layer is staged before it is
+    gathered (N > 1) or computed (N == 1), and a window buffer is re-staged only after its
+    previous layer was read.  Raises AssertionError on violation."""
     held = {0: None, 1: None}          # slot -> layer gathered into it
     consumed = {0: True, 1: True}      # its forward has been issued
+    whold = {}                         # window buffer -> staged layer
+    wcons = {}                         # ... has been read
+    staged = set()
     done = set()
     for op, l, s in ops:
+        if op == "stage":
+            assert s == l % offload_w, (op, l, s)
+            assert wcons.get(s, True), f"stage({l}) overwrites window {s} before layer {whold.get(s)} was read"
+            whold[s], wcons[s] = l, False
+            staged.add(l)
+            continue
+        if offload_w and ((op == "prefetch") or (op == "forward" and N == 1 and l > 0)):
+            assert l in staged and whold.get(l % offload_w) == l and not wcons[l % offload_w], \
+                f"{op}({l}) before its layer was staged"
+            wcons[l % offload_w] = True
         if op == "prefetch":
             assert s == l % 2, (op, l, s)
             assert consumed[s], f"prefetch({l}) would overwrite slot {s} before forward({held[s]})"

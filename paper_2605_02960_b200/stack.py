@@ -16,14 +16,17 @@ from __future__ import annotations
 import torch
 
 from . import asyncep as A
-from .schedule import layer_resident, shard_range, stack_schedule
+from .schedule import layer_resident, shard_range, stack_schedule, staged_layers
 
 
 class MoEStack:
     def __init__(self, L, E, k, H, h, max_tokens, router_fn, expert_fn, *, world_size=1, rank=0,
                  replicate_layer0=True, norm_topk=True, flags=0, gamma=1.2, device="cuda",
-                 nccl_comm=None, compute_stream=None, comm_stream=None, pack_chunk=8, fp8=False):
+                 nccl_comm=None, compute_stream=None, comm_stream=None, pack_chunk=8, fp8=False,
+                 offload_window=0):
         self.device = torch.device(device)
+        flags |= A.FLAG_OFFLOAD if offload_window else 0
+        self.offload_w = offload_window
         self.cfg = A.make_config(L, E, k, H, h, world_size=world_size, rank=rank,
                                  replicate_layer0=int(replicate_layer0), norm_topk=int(norm_topk),
                                  max_tokens=max_tokens, gamma=gamma, flags=flags,
@@ -38,9 +41,16 @@ class MoEStack:
         self.router_w = [router_fn(l).to(self.device, torch.bfloat16).contiguous() for l in range(L)]
         self.fp8, self.expert_fn, self.pack_chunk = fp8, expert_fn, pack_chunk
         self.shards = []
+        self.host_shards = [None] * L
+        staged = set(staged_layers(L, world_size, replicate_layer0)) if offload_window else set()
         for l in range(L):
             full = layer_resident(l, world_size, replicate_layer0)
-            self.shards.append(self.pack(l, range(E) if full else shard_range(E, world_size, rank)))
+            buf = self.pack(l, range(E) if full else shard_range(E, world_size, rank))
+            if l in staged:  # NEXT-2: the backing store is pinned host memory
+                self.host_shards[l] = buf.cpu().pin_memory()
+                del buf
+                buf = None
+            self.shards.append(buf)
         if world_size > 1:
             sb = A.asyncep_slot_bytes(self.cfg)
             self.slots = [torch.empty(sb, dtype=torch.uint8, device=self.device) for _ in range(2)]
@@ -51,6 +61,11 @@ class MoEStack:
         self.ctx = A.asyncep_init(self.cfg, nccl_comm, self.compute_stream, self.comm_stream, self.router_w,
                                   self.shards, self.slots[0], self.slots[1], self.workspace)
         self._bufs = None
+        if offload_window:
+            nb = A.asyncep_slot_bytes(self.cfg) if world_size == 1 else A.asyncep_shard_bytes(self.cfg)
+            self.window = [torch.empty(nb, dtype=torch.uint8, device=self.device) for _ in range(offload_window)]
+            self.h2d_stream = torch.cuda.Stream(self.device)
+            A.asyncep_enable_offload(self.ctx, self.host_shards, self.window, offload_window, self.h2d_stream)
 
     def pack(self, l: int, experts: range) -> torch.Tensor:
         """Packed blobs of ``experts`` of layer l (the shard format of asyncep.h)."""
@@ -79,7 +94,8 @@ class MoEStack:
         for l in range(self.L):
             if self.layer_resident(l):
                 continue
-            table[l] = [self.shards[l] if r == self.rank else self.pack(l, shard_range(self.E, self.N, r))
+            own = self.shards[l] if self.shards[l] is not None else self.window[0]  # offload: C reads the window
+            table[l] = [own if r == self.rank else self.pack(l, shard_range(self.E, self.N, r))
                         for r in range(self.N)]
         return lambda l: table[l]
 
@@ -106,7 +122,10 @@ class MoEStack:
             self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
                           for _ in range(2)]
         cur = x
-        for op, l, _slot in stack_schedule(self.L, self.N, bool(self.cfg.replicate_layer0)):
+        for op, l, _slot in stack_schedule(self.L, self.N, bool(self.cfg.replicate_layer0), self.offload_w):
+            if op == "stage":
+                A.asyncep_stage_layer(self.ctx, l)  # PCIe channel, up to w layers ahead
+                continue
             if op == "prefetch":
                 self.prefetch(l, local_shards)  # gather of layer l overlaps layer l-1
                 continue

@@ -18,7 +18,8 @@ import torch.multiprocessing as mp
 
 import oracle
 import synth
-from paper_2605_02960_b200.schedule import check_schedule, layer_resident, shard_range, stack_schedule
+from paper_2605_02960_b200.schedule import (check_schedule, layer_resident, shard_range, stack_schedule,
+                                            staged_layers)
 
 L, E, K, H, h, T = 4, 8, 2, 64, 128, 40
 
@@ -112,6 +113,17 @@ def test_schedule_invariants():
                 check_schedule(ops, Lx)
                 n_pref = sum(1 for o in ops if o[0] == "prefetch")
                 assert n_pref == sum(1 for l in range(Lx) if not layer_resident(l, N, rep))
+    # NEXT-2 offload windows
+    for N in (1, 2, 8):
+        for w in (1, 2, 3):
+            for Lx in (2, 5, 8):
+                ops = stack_schedule(Lx, N, True, w)
+                check_schedule(ops, Lx, N, w)
+                assert sum(1 for o in ops if o[0] == "stage") == len(staged_layers(Lx, N))
+    with pytest.raises(AssertionError):  # computing an unstaged layer
+        check_schedule([("forward", 0, -1), ("forward", 1, -1)], 2, 1, 1)
+    with pytest.raises(AssertionError):  # re-staging a window before its layer was read
+        check_schedule([("stage", 1, 0), ("stage", 2, 0)], 3, 1, 1)
     # a broken order is rejected: two gathers into the same slot before its forward
     with pytest.raises(AssertionError):
         check_schedule([("prefetch", 1, 1), ("prefetch", 3, 1), ("forward", 0, -1)], 4)
