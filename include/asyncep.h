@@ -260,6 +260,41 @@ ASYNCEP_API asyncep_status asyncep_forward_times(asyncep_ctx* ctx, double* ms_ou
 ASYNCEP_API asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double c_dummy,
                                                 double* flops_out);
 
+/*
+ * ---- NEXT-4: saturation-bounded admission (frontend consumer of T; host only) ----
+ * Algorithm 1 (App. A) with the Eq. 2 cost and the load
+ * band [T, T + Delta_last].  Functional forms of Eq. 2 (reading R18):
+ *   C_pfx(n)   = n f_tok + 2 n^2 HL
+ *   C_sfx(S,P) = S f_tok + 2 S^2 HL + 4 S P HL          (HL = hidden x attention layers)
+ * Requests are block-hash chains (block_size tokens per hash; hashes[chain_off[q] ..
+ * chain_off[q+1]) for request q), prefix_len / suffix_len in tokens.
+ */
+typedef struct asyncep_router asyncep_router;
+typedef struct {
+  int32_t num_gpus;   /* N data-parallel GPUs                                  */
+  int32_t block_size; /* tokens per hashed block (e.g. 16)       */
+  double f_tok;       /* FLOPs per token of the linear terms                   */
+  double attn_hl;     /* hidden x attention layers (quadratic attention terms) */
+  double T_flops;     /* saturation threshold T [FLOPs], e.g. T_tok * f_tok    */
+} asyncep_router_config;
+ASYNCEP_API double asyncep_cost_delta(const asyncep_router_config* cfg, int64_t P, int64_t M, int64_t S); /* NaN on bad args */
+ASYNCEP_API asyncep_status asyncep_router_create(const asyncep_router_config* cfg, asyncep_router** out);
+ASYNCEP_API asyncep_status asyncep_router_destroy(asyncep_router* r);
+ASYNCEP_API asyncep_status asyncep_router_set_T(asyncep_router* r, double T_flops);
+ASYNCEP_API asyncep_status asyncep_router_loads(const asyncep_router* r, double* loads_out); /* [num_gpus] */
+/* One round of Algorithm 1 over n_req queued requests in arrival order.  reset_loads = 1
+ * starts the round with L_i = 0 (Alg. 1 line 1); 0 carries loads over (App. B.2 mode).
+ * gpu_out[q] = assigned GPU, or -1 when every GPU is saturated (the request stays queued);
+ * delta_out[q] = the charged cost (nullable). */
+ASYNCEP_API asyncep_status asyncep_router_schedule_round(asyncep_router* r, int32_t reset_loads, int64_t n_req,
+                                                         const int64_t* chain_off, const uint64_t* hashes,
+                                                         const int64_t* prefix_len, const int64_t* suffix_len,
+                                                         int32_t* gpu_out, double* delta_out, int64_t* admitted_out);
+/* engine events (App. B.3): stored blocks pending -> committed; progress decays L_i by tokens*f_tok */
+ASYNCEP_API asyncep_status asyncep_router_blocks_stored(asyncep_router* r, int32_t gpu, const uint64_t* hashes,
+                                                        int64_t n);
+ASYNCEP_API asyncep_status asyncep_router_progress(asyncep_router* r, int32_t gpu, int64_t tokens);
+
 /* Number of kernels the library launched since context creation (host-side counter). */
 ASYNCEP_API int64_t asyncep_kernel_launches(const asyncep_ctx* ctx);
 

@@ -82,6 +82,14 @@ def lib() -> ctypes.CDLL:
             "asyncep_set_link_emulation": ([P, D], I32),
             "asyncep_enable_offload": ([P, P, P, I32, P], I32),
             "asyncep_stage_layer": ([P, I32], I32),
+            "asyncep_cost_delta": ([P, I64, I64, I64], D),
+            "asyncep_router_create": ([P, ctypes.POINTER(P)], I32),
+            "asyncep_router_destroy": ([P], I32),
+            "asyncep_router_set_T": ([P, D], I32),
+            "asyncep_router_loads": ([P, P], I32),
+            "asyncep_router_schedule_round": ([P, I32, I64, P, P, P, P, P, P, ctypes.POINTER(I64)], I32),
+            "asyncep_router_blocks_stored": ([P, I32, P, I64], I32),
+            "asyncep_router_progress": ([P, I32, I64], I32),
             "asyncep_ep_plan": ([CP, P, P, P, P, P, P, P, ctypes.POINTER(I64)], I32),
             "asyncep_ep_workspace_size": ([CP, I64], SZ),
             "asyncep_ep_forward": ([P, I32, P, I64, P, P, P, I64], I32),
@@ -290,3 +298,61 @@ def nccl_comm_ptr(pg=None) -> int:
     import torch.distributed as dist
     pg = pg or dist.group.WORLD
     return pg._get_backend(torch.device("cuda"))._comm_ptr()
+
+
+# ------------------------------------------------------------------------------ NEXT-4 admission
+class RouterConfig(ctypes.Structure):
+    _fields_ = [("num_gpus", ctypes.c_int32), ("block_size", ctypes.c_int32), ("f_tok", ctypes.c_double),
+                ("attn_hl", ctypes.c_double), ("T_flops", ctypes.c_double)]
+
+
+def asyncep_cost_delta(rcfg: RouterConfig, P: int, M: int, S: int) -> float:
+    return lib().asyncep_cost_delta(ctypes.byref(rcfg), P, M, S)
+
+
+class Router:
+    """Saturation-bounded admission (Algorithm 1) -- thin wrapper."""
+
+    def __init__(self, num_gpus, block_size, f_tok, attn_hl, T_flops):
+        self.cfg = RouterConfig(num_gpus, block_size, f_tok, attn_hl, T_flops)
+        self.h = ctypes.c_void_p()
+        _check(lib().asyncep_router_create(ctypes.byref(self.cfg), ctypes.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.asyncep_router_destroy(self.h)
+            self.h = None
+
+    def schedule_round(self, chains, prefix_len, suffix_len, reset_loads=True):
+        import numpy as np
+        n = len(chains)
+        off = np.zeros(n + 1, np.int64)
+        off[1:] = np.cumsum([len(c) for c in chains])
+        hashes = np.ascontiguousarray(np.concatenate([np.asarray(c, np.uint64) for c in chains])
+                                      if n else np.zeros(0, np.uint64), dtype=np.uint64)
+        pl = np.ascontiguousarray(prefix_len, np.int64)
+        sl = np.ascontiguousarray(suffix_len, np.int64)
+        gpu = np.empty(n, np.int32)
+        delta = np.empty(n, np.float64)
+        adm = ctypes.c_int64()
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+        _check(lib().asyncep_router_schedule_round(self.h, int(reset_loads), n, vp(off), vp(hashes), vp(pl), vp(sl),
+                                                   vp(gpu), vp(delta), ctypes.byref(adm)))
+        return gpu, delta
+
+    def loads(self):
+        import numpy as np
+        out = np.empty(self.cfg.num_gpus, np.float64)
+        _check(lib().asyncep_router_loads(self.h, out.ctypes.data_as(ctypes.c_void_p)))
+        return out
+
+    def blocks_stored(self, gpu, hashes):
+        import numpy as np
+        a = np.ascontiguousarray(hashes, np.uint64)
+        _check(lib().asyncep_router_blocks_stored(self.h, gpu, a.ctypes.data_as(ctypes.c_void_p), a.size))
+
+    def progress(self, gpu, tokens):
+        _check(lib().asyncep_router_progress(self.h, gpu, tokens))
+
+    def set_T(self, T_flops):
+        _check(lib().asyncep_router_set_T(self.h, T_flops))

@@ -16,7 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libasyncep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["asyncep.cu", "router.cu", "permute.cu", "gemm_simt.cu", "gemm_tc.cu", "combine.cu", "pack.cu"]
+SOURCES = ["asyncep.cu", "router.cu", "permute.cu", "gemm_simt.cu", "gemm_tc.cu", "combine.cu", "pack.cu",
+           "admission.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr"]
 
@@ -28,7 +29,7 @@ def _inputs():
 
 
 def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
     dep_mtime = max(os.path.getmtime(d) for d in _inputs())
     if os.path.exists(obj) and os.path.getmtime(obj) >= dep_mtime:
         return obj
