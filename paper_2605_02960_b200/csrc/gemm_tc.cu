@@ -44,6 +44,7 @@ constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
 constexpr int NTHREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
+constexpr int SCL_BYTES = 256 * 4;             // per epilogue warp: the tile's 256 FP8 weight scales
 constexpr int TMEM_COLS = 512;
 constexpr int RING = 4;  // tile ids in flight between the scheduler and the consumers
 
@@ -51,8 +52,8 @@ template <int NCTA>
 struct Cfg {
   static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
   static constexpr int STAGES = NCTA == 2 ? 6 : 4;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES + 256 +
-                                 (kMaxExperts + 1) * sizeof(int32_t);
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES +
+                                 4 * SCL_BYTES + 256 + (kMaxExperts + 1) * sizeof(int32_t);
 };
 
 enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
@@ -228,6 +229,16 @@ __device__ __forceinline__ int sched_consume(const TileRing& r, int seq, bool le
   return t;
 }
 
+// FP8 epilogue: the 256 per-channel weight scales of this tile (contiguous in the blob) are
+// copied once per tile into the warp's smem buffer and then read as broadcasts (a per-element
+// global load for every thread made the FP8 epilogue, not the MMA, the limiter).
+__device__ __forceinline__ const float* stage_scales(float* dst, const float* src, int n, int lane) {
+  __syncwarp();
+  for (int i = lane * 4; i < n; i += 128) *reinterpret_cast<float4*>(dst + i) = __ldg(reinterpret_cast<const float4*>(src + i));
+  __syncwarp();
+  return dst;
+}
+
 template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -239,7 +250,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
   uint8_t* sStg = sB + STAGES * C::B_BYTES_MAX;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG_BYTES);
+  float* sScl = reinterpret_cast<float*>(sStg + 4 * STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG_BYTES + 4 * SCL_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -421,7 +433,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sa = p.a_scale[wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256;
+          sb = stage_scales(sScl + ew * 256,
+                            reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256, 256,
+                            lane);
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 64) {
@@ -438,10 +452,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
               if (F8) {
                 const int c = c0 + 32 * half + 2 * i;
-                g0 *= sa * __ldg(sb + c);
-                g1 *= sa * __ldg(sb + c + 1);
-                u0 *= sa * __ldg(sb + 128 + c);
-                u1 *= sa * __ldg(sb + 128 + c + 1);
+                const float2 sg = *reinterpret_cast<const float2*>(sb + c);
+                const float2 su = *reinterpret_cast<const float2*>(sb + 128 + c);
+                g0 *= sa * sg.x;
+                g1 *= sa * sg.y;
+                u0 *= sa * su.x;
+                u1 *= sa * su.y;
               }
               const uint32_t pk = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
               o[16 * half + i] = pk;
@@ -458,7 +474,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sa = p.a_scale[wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN;
+          sb = stage_scales(sScl + ew * 256,
+                            reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN,
+                            p.BN, lane);
         }
 #pragma unroll 1
         for (int c0 = 0; c0 < p.BN; c0 += 64) {
@@ -474,8 +492,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               float v0 = __uint_as_float(r[2 * i]), v1 = __uint_as_float(r[2 * i + 1]);
               if (F8) {
                 const int c = c0 + 32 * half + 2 * i;
-                v0 *= sa * __ldg(sb + c);
-                v1 *= sa * __ldg(sb + c + 1);
+                const float2 sv = *reinterpret_cast<const float2*>(sb + c);
+                v0 *= sa * sv.x;
+                v1 *= sa * sv.y;
               }
               o[16 * half + i] = pack_bf16x2(v0, v1);
             }
