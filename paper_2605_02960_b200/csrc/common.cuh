@@ -38,7 +38,28 @@ AEP_DEV uint16_t e4m3x2(float v0, float v1) {
 }
 
 // silu(z) = z * sigma(z) = z / (1 + e^-z)   (reading R4).  IEEE division, expf.
-AEP_DEV float silu_f(float z) { return z / (1.0f + __expf(-z)); }
+// SiLU z * sigmoid(z) with the SFU: ex2.approx (rel. err ~2^-22) and rcp.approx (~2^-23);
+// exact limits: z -> -inf gives 1/inf = 0 (times finite z), z -> +inf gives z.
+AEP_DEV float silu_f(float z) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(z * -1.4426950408889634f));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+  return z * r;
+}
+
+// Packed fp32x2 multiply (FMUL2, sm_100): (x0, x1) = (a0 * b0, a1 * b1), round-to-nearest.
+AEP_DEV void mul2(float& x0, float& x1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+      "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+      : "=f"(x0), "=f"(x1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+AEP_DEV float4 ld_shared_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
 
 // ----------------------------------------------------------------------------- mbarrier
 AEP_DEV void mbar_init(uint64_t* bar, uint32_t count) {
@@ -346,6 +367,15 @@ AEP_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: 
 //   bits [46,48) version = 1 (sm_100)
 //   bits [49,52) base offset = 0, bit 52 lbo mode = 0
 //   bits [61,64) layout: 2 = SWIZZLE_128B
+// One lane of the (converged) warp returns true: the issuing lane for tcgen05.mma/commit, so
+// the issue loop stays warp-uniform and its operands live in uniform registers.
+AEP_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+
 AEP_DEV uint64_t make_smem_desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);

@@ -366,40 +366,52 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {
+      // MMA issuer: the whole warp runs the loop (warp-uniform state in uniform registers);
+      // one elected lane issues the MMAs and the commits that track them.
       const uint32_t idesc = make_idesc(TM, p.BN, !F8);
+      const uint64_t a_desc0 = make_smem_desc_sw128(smem_u32(sA));
+      const uint64_t b_desc0 = make_smem_desc_sw128(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int seq = 0;; ++seq) {
-        if (sched_consume<NCTA>(ring, seq, true, false) >= total) break;
+        int t = 0;
+        if (lane == 0) t = sched_consume<NCTA>(ring, seq, true, false);
+        if (__shfl_sync(0xffffffffu, t, 0) >= total) break;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES_MAX);
+          // descriptor start address field is addr >> 4: a stage / a 32-B K step are plain adds
+          const uint64_t ad = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * C::B_BYTES_MAX) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 B of K (16 bf16 / 32 e4m3) per 128-B k-block
-            const uint64_t ad = make_smem_desc_sw128(a0 + k * 32), bd = make_smem_desc_sw128(b0 + k * 32);
-            const uint32_t acc_on = (kb | k) != 0 ? 1u : 0u;
-            if (F8) {
-              if (NCTA == 2) mma_f8_2(d, ad, bd, idesc, acc_on);
-              else mma_f8(d, ad, bd, idesc, acc_on);
-            } else {
-              if (NCTA == 2) mma_bf16_2(d, ad, bd, idesc, acc_on);
-              else mma_bf16(d, ad, bd, idesc, acc_on);
+            for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 B of K (16 bf16 / 32 e4m3) per 128-B k-block
+              const uint32_t acc_on = (kb | k) != 0 ? 1u : 0u;
+              if (F8) {
+                if (NCTA == 2) mma_f8_2(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+                else mma_f8(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+              } else {
+                if (NCTA == 2) mma_bf16_2(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+                else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+              }
             }
+            if (NCTA == 2) tc_commit2_mc(&empty[stage], 0x3);
+            else tc_commit(&empty[stage]);
           }
-          if (NCTA == 2) tc_commit2_mc(&empty[stage], 0x3);
-          else tc_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (NCTA == 2) tc_commit2_mc(&tfull[acc], 0x3);
-        else tc_commit(&tfull[acc]);
+        if (elect_one()) {
+          if (NCTA == 2) tc_commit2_mc(&tfull[acc], 0x3);
+          else tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -440,6 +452,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 64) {
           uint32_t o[32];
+          uint32_t amax2 = 0;  // |bf16| bit patterns of both halves: unsigned order = magnitude order
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             uint32_t g[32], u[32];
@@ -447,24 +460,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tmem_ld32(tb + 128 + c0 + 32 * half, u);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
-              float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
-              if (F8) {
-                const int c = c0 + 32 * half + 2 * i;
-                const float2 sg = *reinterpret_cast<const float2*>(sb + c);
-                const float2 su = *reinterpret_cast<const float2*>(sb + 128 + c);
-                g0 *= sa * sg.x;
-                g1 *= sa * sg.y;
-                u0 *= sa * su.x;
-                u1 *= sa * su.y;
+            for (int q = 0; q < 8; ++q) {  // 4 columns per step
+              float gv[4], uv[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                gv[j] = __uint_as_float(g[4 * q + j]);
+                uv[j] = __uint_as_float(u[4 * q + j]);
               }
-              const uint32_t pk = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
-              o[16 * half + i] = pk;
-              if (F8) amax = fmaxf(amax, fmaxf(fabsf(bf16_lo(pk)), fabsf(bf16_hi(pk))));
+              if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
+                const uint32_t sc = smem_u32(sb) + 4 * (c0 + 32 * half + 4 * q);
+                const float4 sg = ld_shared_f4(sc), su = ld_shared_f4(sc + 512);
+                float s0, s1, s2, s3, t0, t1, t2, t3;
+                mul2(s0, s1, sa, sa, sg.x, sg.y);
+                mul2(s2, s3, sa, sa, sg.z, sg.w);
+                mul2(t0, t1, sa, sa, su.x, su.y);
+                mul2(t2, t3, sa, sa, su.z, su.w);
+                mul2(gv[0], gv[1], gv[0], gv[1], s0, s1);
+                mul2(gv[2], gv[3], gv[2], gv[3], s2, s3);
+                mul2(uv[0], uv[1], uv[0], uv[1], t0, t1);
+                mul2(uv[2], uv[3], uv[2], uv[3], t2, t3);
+              }
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                float a0, a1;
+                mul2(a0, a1, silu_f(gv[2 * j]), silu_f(gv[2 * j + 1]), uv[2 * j], uv[2 * j + 1]);
+                const uint32_t pk = pack_bf16x2(a0, a1);
+                o[16 * half + 2 * q + j] = pk;
+                if (F8) amax2 = __vmaxu2(amax2, pk & 0x7fff7fffu);
+              }
             }
           }
           stage_and_store(o, stg, lane, &map_out, nt * 128 + c0, wrow0);
+          if (F8) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
         }
         if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
       } else {
@@ -488,15 +515,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tmem_ld32(tb + c0 + 32 * half, r);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float v0 = __uint_as_float(r[2 * i]), v1 = __uint_as_float(r[2 * i + 1]);
-              if (F8) {
-                const int c = c0 + 32 * half + 2 * i;
-                const float2 sv = *reinterpret_cast<const float2*>(sb + c);
-                v0 *= sa * sv.x;
-                v1 *= sa * sv.y;
+            for (int q = 0; q < 8; ++q) {  // 4 columns per step
+              float v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[j] = __uint_as_float(r[4 * q + j]);
+              if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
+                const float4 sv = ld_shared_f4(smem_u32(sb) + 4 * (c0 + 32 * half + 4 * q));
+                float s0, s1, s2, s3;
+                mul2(s0, s1, sa, sa, sv.x, sv.y);
+                mul2(s2, s3, sa, sa, sv.z, sv.w);
+                mul2(v[0], v[1], v[0], v[1], s0, s1);
+                mul2(v[2], v[3], v[2], v[3], s2, s3);
               }
-              o[16 * half + i] = pack_bf16x2(v0, v1);
+              o[16 * half + 2 * q] = pack_bf16x2(v[0], v[1]);
+              o[16 * half + 2 * q + 1] = pack_bf16x2(v[2], v[3]);
             }
           }
           stage_and_store(o, stg, lane, &map_out, nt * p.BN + c0, wrow0);

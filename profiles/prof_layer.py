@@ -19,8 +19,9 @@ ap.add_argument("--tokens", type=int, default=32768)
 ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--H", type=int, default=4096)
 ap.add_argument("--h", type=int, default=1536)
+ap.add_argument("--fp8", action="store_true")
 a = ap.parse_args()
-wl = Workload(L=1, E=128, k=8, H=a.H, h=a.h, seed=0)
+wl = Workload(L=1, E=128, k=8, H=a.H, h=a.h, seed=0, fp8=a.fp8)
 st = wl.stack(max_tokens=a.tokens, flags=a.flags)
 x = wl.tokens(a.tokens)
 y = torch.empty_like(x)
