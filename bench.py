@@ -190,6 +190,7 @@ def main():
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
+    ap.add_argument("--xperm", action="store_true", help="materialise X_perm (unfused dispatch, FLAG_XPERM)")
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
                     help="1-GPU emulation of the N-rank AsyncEP gather (D2D copies of all N shards into "
                          "the slot on the comm stream); measures exposed wait + HBM interference")
@@ -230,7 +231,7 @@ def main():
         comm = A.nccl_comm_ptr()
     L, T = args.layers, args.tokens
     seed = 0
-    flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0)
+    flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0) | (A.FLAG_XPERM if args.xperm else 0)
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
     emu = args.emulate_gather if world == 1 else 0
     stack = MoEStack(L, E_, K_, H_, h_, T,

@@ -61,7 +61,8 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
 #define ASYNCEP_FLAG_SIMT_GEMM        0x2 /* CUDA-core grouped GEMM instead of tcgen05 (sanitizer runs) */
 #define ASYNCEP_FLAG_STAGE_TIMING     0x4 /* record CUDA events around each stage (asyncep_stage_times) */
 #define ASYNCEP_FLAG_SIMT_ROUTER      0x8 /* CUDA-core router logits instead of tcgen05                */
-#define ASYNCEP_FLAG_GATHER_A        0x10 /* GEMM1 gathers token rows with TMA gather4 (no X_perm)     */
+#define ASYNCEP_FLAG_XPERM           0x10 /* materialise X_perm and TMA-load it (default: GEMM1 gathers
+                                               the token rows itself through src_tok, cp.async)     */
 #define ASYNCEP_FLAG_OFFLOAD         0x20 /* NEXT-2: expert_shard[l] may be NULL for offloaded layers  */
 
 typedef struct {

@@ -16,7 +16,8 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libasyncep.so")
+# ASYNCEP_LIB: an in-tree variant build (build.py -D ... --out ...) for same-box A/B runs
+LIB_PATH = os.environ.get("ASYNCEP_LIB") or os.path.join(_HERE, "libasyncep.so")
 
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_NOT_PREFETCHED, ERR_WORKSPACE = range(7)
 BF16, FP8_E4M3 = 0, 1
@@ -24,7 +25,7 @@ FLAG_IDENTITY_EXPERTS = 0x1
 FLAG_SIMT_GEMM = 0x2
 FLAG_STAGE_TIMING = 0x4
 FLAG_SIMT_ROUTER = 0x8
-FLAG_GATHER_A = 0x10
+FLAG_XPERM = 0x10
 FLAG_OFFLOAD = 0x20
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 

@@ -28,12 +28,12 @@ def _inputs():
     return deps
 
 
-def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, build_dir: str = BUILD, defines=()) -> str:
+    obj = os.path.join(build_dir, os.path.splitext(src)[0] + ".o")
     dep_mtime = max(os.path.getmtime(d) for d in _inputs())
     if os.path.exists(obj) and os.path.getmtime(obj) >= dep_mtime:
         return obj
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-c",
            os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -41,26 +41,36 @@ def _compile(src: str) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Build the library.  defines / out: a variant (extra -D macros) for same-box A/B runs,
+    linked to another path (loaded with ASYNCEP_LIB=path); the default build is LIB."""
+    build_dir = BUILD if not defines else os.path.join(BUILD, "v_" + "_".join(defines).replace("=", ""))
+    os.makedirs(build_dir, exist_ok=True)
     if force:
-        for f in os.listdir(BUILD):
-            os.remove(os.path.join(BUILD, f))
+        for f in os.listdir(build_dir):
+            if f.endswith(".o"):
+                os.remove(os.path.join(build_dir, f))
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(_compile, SOURCES))
+        objs = list(ex.map(lambda f: _compile(f, build_dir, defines), SOURCES))
     newest = max(os.path.getmtime(o) for o in objs)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        tmp = LIB + f".tmp{os.getpid()}"
+    if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+        tmp = out + f".tmp{os.getpid()}"
         cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
                *objs, "-o", tmp, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, out)
         if verbose:
-            print("built", LIB)
-    return LIB
+            print("built", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="variant macro NAME=VALUE")
+    ap.add_argument("--out", default=LIB)
+    a = ap.parse_args()
+    build(force=a.force, verbose=True, defines=tuple(a.defines), out=a.out)

@@ -550,13 +550,13 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
   // (2) permute / dispatch
   aep::launch_perm_hist(ids, T, k, E, blk, st);
-  // X_perm is materialised unless GEMM1 gathers the token rows itself (ASYNCEP_FLAG_GATHER_A:
-  // TMA gather4 through src_tok -- correct, but measured 2.5x slower than the tiled loads
-  // because gather4 issue throughput caps at ~512 B per ~70 cycles per SM).
+  // Fused dispatch (default): GEMM1's cp.async gather warps read the token rows of x -- or of
+  // the token-major x_q -- through src_tok, so X_perm is never written.  ASYNCEP_FLAG_XPERM
+  // (and the identity / SIMT debug paths) materialise X_perm instead.
   const bool fp8 = cf.expert_dtype == ASYNCEP_FP8_E4M3;
   const bool identity = (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) != 0;
-  const bool gather_a = (cf.flags & ASYNCEP_FLAG_GATHER_A) && !fp8 &&
-                        !(cf.flags & (ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM));
+  const bool gather_a = !(cf.flags & (ASYNCEP_FLAG_XPERM | ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM)) &&
+                        ((uintptr_t)x % 16 == 0) && ((size_t)H * 2) % 16 == 0;
   const bool materialise = identity || (!gather_a && !fp8);
   aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
   aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok,
@@ -570,7 +570,8 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     f8.expert_bytes = c->expert_bytes;
     f8.sgu_off = (size_t)3 * H * h;
     f8.sd_off = f8.sgu_off + (size_t)2 * h * 4;
-    aep::launch_perm_quant((const bf16*)x, dest, T, H, k, ws + c->L.xq, (float*)(ws + c->L.xscale), st);
+    aep::launch_perm_quant((const bf16*)x, gather_a ? nullptr : dest, T, H, k, ws + c->L.xq,
+                           (float*)(ws + c->L.xscale), st);
     c->launches += 1;
   }
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
@@ -593,16 +594,15 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     c->launches += 2;
   } else if (fp8) {
     f8.layer = wl;
-    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, nullptr, T, src_tok, c->num_sms, st, &f8);
+    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const void*)(ws + c->L.xq) : nullptr, T, src_tok,
+                         c->num_sms, st, &f8);
     aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
                           (float*)(ws + c->L.ascale), st);
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8);
     c->launches += 3;
   } else {
-    if (!aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const bf16*)x : nullptr, T, src_tok,
-                              c->num_sms, st))
-      return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (gather map)");
+    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? x : nullptr, T, src_tok, c->num_sms, st);
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st);
     c->launches += 2;

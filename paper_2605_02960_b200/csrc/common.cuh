@@ -119,6 +119,14 @@ AEP_DEV void tma_store_2d(const void* tmap, const void* src, int c0, int c1) {
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+// 16-B global -> shared copy through L2 only (LDGSTS), and an mbarrier arrival that fires when
+// all of this thread's prior cp.async copies have landed (.noinc: counted in the init count).
+AEP_DEV void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+AEP_DEV void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 AEP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 AEP_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 AEP_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }

@@ -46,14 +46,15 @@ constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int SCL_BYTES = 256 * 4;             // per epilogue warp: the tile's 256 FP8 weight scales
 constexpr int TMEM_COLS = 512;
-constexpr int RING = 4;  // tile ids in flight between the scheduler and the consumers
+constexpr int RING = 4;
+  // tile ids in flight between the scheduler and the consumers
 
 template <int NCTA>
 struct Cfg {
   static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
   static constexpr int STAGES = NCTA == 2 ? 6 : 4;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES +
-                                 4 * SCL_BYTES + 256 + (kMaxExperts + 1) * sizeof(int32_t);
+                                 4 * SCL_BYTES + 512 + (kMaxExperts + 1) * sizeof(int32_t);
 };
 
 enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
@@ -77,8 +78,12 @@ struct TcArgs {
   int* sched;                   // dynamic tile counter (zeroed before the launch)
   int group_mod;                // > 0: B expert = group % group_mod (EP contrast: groups are
                                 // (source rank, local expert) pairs over a shard of group_mod experts)
-  const int32_t* gather_rows;  // non-null: A rows are gathered from the token matrix (map_a is a
-                               // {H, T} gather4 map) with row ids gather_rows[permuted row]
+  // fused dispatch: non-null gather_rows = A rows are gathered by warps 2-3 (cp.async) from the
+  // token-major matrix gather_src (gather_ld bytes per token) at token gather_rows[permuted row];
+  // the FP8 a_scale is then indexed by token
+  const int32_t* gather_rows;
+  const uint8_t* gather_src;
+  int64_t gather_ld;
   // router epilogue
   int top_k, norm_topk;
   int32_t* ids;
@@ -257,9 +262,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* sfull = tempty + 2;          // tile-id ring (dynamic scheduler): filled
   uint64_t* sempty = sfull + RING;       //                                    released
-  int32_t* sring = reinterpret_cast<int32_t*>(sempty + RING);
+  uint64_t* afull = sempty + RING;       // fused dispatch: this CTA's gathered A stage landed
+  int32_t* sring = reinterpret_cast<int32_t*>(afull + STAGES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sring + RING);
-  int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 256);
+  int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 512);
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = NCTA == 2 ? cluster_ctarank() : 0;
@@ -276,13 +282,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i] * p.ts_scale;
   }
+  const bool gather = p.gather_rows != nullptr;
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_a);
+    if (!gather) tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
     if (MODE == EPI_PLAIN || MODE == EPI_SWIGLU) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], NCTA);  // leader: own expect_tx arrive + peer's arrive
+      // leader: own expect_tx arrive + peer producer's arrive (+ peer's gathered-A forward)
+      mbar_init(&full[s], NCTA + (gather && NCTA == 2 ? 1 : 0));
       mbar_init(&empty[s], 1);
+      mbar_init(&afull[s], 64);  // one .noinc cp.async arrival per gather thread
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -290,8 +299,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int r = 0; r < RING; ++r) {
       mbar_init(&sfull[r], 1);
-      // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue warps}
-      mbar_init(&sempty[r], 5 * NCTA);
+      // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue
+      // warps}; fused dispatch adds the 2 gather warps of each CTA and the peer's forwarder
+      mbar_init(&sempty[r], 5 * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0));
     }
     fence_barrier_init();
   }
@@ -311,20 +321,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const TileRing ring{sfull, sempty, sring};
 
   if (warp == 0) {
-    // Producer warp.  Lane 0 arms the barriers and loads B (and A when it is a dense 2-D
-    // tile); with a gathered A every lane issues one gather4 of 4 of the tile's 128 rows.
-    const bool gather = p.gather_rows != nullptr;
-    if (gather || lane == 0) {
-      const uint32_t tx = (uint32_t)NCTA * ((uint32_t)A_BYTES + (uint32_t)bn_cta * BK * 2);
+    // Producer warp, lane 0: arms the stage barrier and loads B (and A unless it is gathered).
+    if (lane == 0) {
+      const uint32_t tx = (uint32_t)NCTA * ((gather ? 0u : (uint32_t)A_BYTES) + (uint32_t)bn_cta * BK * 2);
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
       for (int seq = 0;; ++seq) {
-        int t = 0;
-        if (lane == 0)
-          t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
-                     : sched_consume<NCTA>(ring, seq, false, true);
-        if (gather) t = __shfl_sync(0xffffffffu, t, 0);
+        const int t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
+                             : sched_consume<NCTA>(ring, seq, false, true);
         if (t >= total) break;
         int mt, nt;
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
@@ -332,41 +337,80 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
         const int row0 = mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
-        int4 rows = make_int4(0, 0, 0, 0);
-        if (gather) rows = reinterpret_cast<const int4*>(p.gather_rows + row0)[lane];  // rows 4*lane..+3
         for (int kb = 0; kb < nkb; ++kb) {
-          if (lane == 0) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            if (NCTA == 2) {
-              if (leader) mbar_arrive_expect_tx(&full[stage], tx);
-              else mbar_arrive_cluster_relaxed(&full[stage], 0);
-              if (!gather) {
-                if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
-                else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
-              }
-              tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
-            } else {
-              mbar_arrive_expect_tx(&full[stage], tx);
-              if (!gather) {
-                if (p.pol_a == 3) tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
-                else tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
-              }
-              tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (NCTA == 2) {
+            if (leader) mbar_arrive_expect_tx(&full[stage], tx);
+            else mbar_arrive_cluster_relaxed(&full[stage], 0);
+            if (!gather) {
+              if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
+              else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-          }
-          if (gather) {
-            __syncwarp();  // the stage is free and armed
-            uint8_t* dst = sA + stage * A_BYTES + lane * 4 * 128;
-            if (NCTA == 2) tma_gather4_pair(dst, &map_a, &full[stage], kb * BK, rows);
-            else tma_gather4(dst, &map_a, &full[stage], kb * BK, rows);
+            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], tx);
+            if (!gather) {
+              if (p.pol_a == 3) tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
+              else tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+            }
+            tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
     __syncwarp();
+  } else if (gather && (warp == 2 || warp == 3)) {
+    // Fused dispatch (step 2 folded into the A load): 64 threads gather the CTA's 128 A rows of
+    // each k-block straight from the token-major input.  Thread g copies 16-B chunk (g & 7) of
+    // rows (g >> 3) + 8i, i < 16: 8 consecutive threads read one row's contiguous 128 B, and
+    // the chunk lands at its 128-B-swizzle position j ^ (row & 7) (row & 7 is fixed per thread).
+    const int gt = (int)threadIdx.x - 64;
+    const int rr = gt >> 3, ch = gt & 7;
+    const uint32_t dst0 = smem_u32(sA) + (uint32_t)(rr * 128 + ((ch ^ (rr & 7)) << 4));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int seq = 0;; ++seq) {
+      int t = 0;
+      if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= total) break;
+      int mt, nt;
+      decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+      const int row0 = mt * TM + (int)rank * BM;
+      const uint8_t* src[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        src[i] = p.gather_src + (int64_t)__ldg(p.gather_rows + row0 + rr + 8 * i) * p.gather_ld + ch * 16;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        const uint32_t dst = dst0 + (uint32_t)(stage * A_BYTES);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+        cp_async_mbar_arrive_noinc(&afull[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
   } else if (warp == 1) {
-    if (leader) {
+    if (gather && NCTA == 2 && !leader) {
+      // peer forwarder: this CTA's gathered A stage has landed -> one arrival on the leader's
+      // stage barrier (the MMA reads both CTAs' A halves).  Relaxed and without a proxy fence
+      // (as CUTLASS's cp.async -> UMMA pipelines): completion of the copies is observed through
+      // the mbarrier; a release.cluster arrive + fence.proxy.async here cost 1.8x on GEMM1.
+      if (lane == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int seq = 0;; ++seq) {
+          if (sched_consume<NCTA>(ring, seq, false, false) >= total) break;
+          for (int kb = 0; kb < nkb; ++kb) {
+            mbar_wait(&afull[stage], phase);
+            mbar_arrive_cluster_relaxed(&full[stage], 0);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+        }
+      }
+    } else if (leader) {
       // MMA issuer: the whole warp runs the loop (warp-uniform state in uniform registers);
       // one elected lane issues the MMAs and the commits that track them.
       const uint32_t idesc = make_idesc(TM, p.BN, !F8);
@@ -385,6 +429,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
+          if (gather) mbar_wait(&afull[stage], phase);  // own gathered A half
           tc_fence_after();
           // descriptor start address field is addr >> 4: a stage / a 32-B K step are plain adds
           const uint64_t ad = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
@@ -442,7 +487,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float sa = 1.f, amax = 0.f;
         const float* sb = nullptr;
         if (F8) {
-          sa = p.a_scale[wrow0 + lane];
+          sa = p.a_scale[gather ? __ldg(p.gather_rows + wrow0 + lane) : wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
           sb = stage_scales(sScl + ew * 256,
@@ -591,7 +636,8 @@ int grouped_raster() {
 
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
-                    const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false) {
+                    const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false,
+                    const void* gather_src = nullptr, int64_t gather_ld = 0) {
   static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
@@ -606,6 +652,8 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.pol_a = env_int("ASYNCEP_POL_A", 0);
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
   a.gather_rows = gather_rows;
+  a.gather_src = static_cast<const uint8_t*>(gather_src);
+  a.gather_ld = gather_ld;
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
   a.group_mod = g.group_mod;
   if (f8) {
@@ -700,27 +748,16 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 }
 
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
+                     const void* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
                      const F8Args* f8) {
-  if (f8) {
-    launch_grouped(g, am.xq, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, nullptr, f8,
-                   false);
-    return true;
-  }
-  // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns
-  if (x_gather) {  // dispatch fused into the A load: gather token rows of x by src_tok
-    CUtensorMap map_x;
-    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
-    const uint64_t strides[1] = {(uint64_t)H * 2};
-    const uint32_t box[2] = {BK, 1};
-    if (!encode_tmap(&map_x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x_gather, dims, strides, box,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
-    launch_grouped(g, map_x, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s, src_tok, nullptr,
-                   false);
-  } else {
-    launch_grouped(g, am.xperm, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s);
-  }
+  // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns.
+  // x_gather != nullptr: dispatch fused into the A load (rows gathered from the token-major
+  // x / x_q through src_tok); the A map is then unused.
+  const int64_t ld = (int64_t)H * (f8 ? 1 : 2);
+  const CUtensorMap& ma = f8 ? am.xq : am.xperm;
+  launch_grouped(g, ma, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s,
+                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld);
+  (void)T;
   return true;
 }
 

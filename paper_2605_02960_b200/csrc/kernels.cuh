@@ -42,7 +42,8 @@ void launch_perm_scatter(const bf16* x, const int32_t* ids, const int32_t* blk_b
                          cudaStream_t s);
 
 // FP8 (R6): per-token e4m3 quantisation of x into its k permuted rows (after the scatter
-// computed dest), and per-row quantisation of the GEMM1 intermediate.
+// computed dest; dest == nullptr: into token row t of a token-major x_q, for the fused
+// dispatch), and per-row quantisation of the GEMM1 intermediate.
 void launch_perm_quant(const bf16* x, const int32_t* dest, int64_t T, int H, int k, uint8_t* xq, float* xscale,
                        cudaStream_t s);
 void launch_act_quant(const bf16* act, uint32_t* act_amax, const int32_t* offsets, int E, int64_t R, int h,
@@ -102,10 +103,11 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h, const uint8_t* xq,
                    const uint8_t* aq);
 int gemm2_bn(int H);
-// x_gather != nullptr: A rows are gathered from x [T, H] through src_tok (TMA gather4),
-// i.e. the dispatch is fused into the GEMM and X_perm is never written.
+// x_gather != nullptr: A rows are gathered from the token-major x [T, H] (bf16, or the e4m3
+// x_q with f8) through src_tok by cp.async warps inside the GEMM, i.e. the dispatch is fused
+// into the GEMM and X_perm is never written.
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
-                     const bf16* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
+                     const void* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
                      const F8Args* f8 = nullptr);
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
                      int num_sms, cudaStream_t s, const F8Args* f8 = nullptr);

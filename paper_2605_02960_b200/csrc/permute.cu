@@ -180,8 +180,9 @@ __global__ void __launch_bounds__(256) perm_quant_kernel(const bf16* __restrict_
   const float inv = amax > 0.f ? 448.0f / amax : 0.f;
   const float sc = amax / 448.0f;
   int32_t d[kMaxTopK];
+  if (!dest) k = 1;  // token-major output: row t
 #pragma unroll
-  for (int j = 0; j < kMaxTopK; ++j) d[j] = (j < k) ? dest[t * k + j] : 0;
+  for (int j = 0; j < kMaxTopK; ++j) d[j] = (j < k) ? (dest ? dest[t * k + j] : (int32_t)t) : 0;
   for (int v = lane; v < nv; v += 32) {
     const uint4 u = src[v];
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};

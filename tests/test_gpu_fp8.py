@@ -33,10 +33,11 @@ def test_fp8_weights_bit_identical_cpu_gpu():
                            tb.cpu().view(torch.uint8) if tb.dtype == torch.uint8 else tb.cpu().view(torch.int32))
 
 
+@pytest.mark.parametrize("flags", [0, 16], ids=["fused_dispatch", "xperm"])
 @pytest.mark.parametrize("T", [300, 2048])
-def test_fp8_layer_parity(T):
+def test_fp8_layer_parity(T, flags):
     wl = Workload(L=2, E=16, k=4, H=512, h=256, seed=21, fp8=True)
-    st = wl.stack(max_tokens=2048)
+    st = wl.stack(max_tokens=2048, flags=flags)
     x = wl.tokens(T)
     for l in range(2):
         y, ids, w, counts = run_layer(wl, st, l, x, residual=False)
@@ -64,3 +65,17 @@ def test_fp8_qwen3_235b_shape_sampled():
     print("plain", check_layer(xs, wr, g, u, d, 8, y[idx], ids[idx], w[idx], None, residual=False, tol=6e-2))
     print("emul", check_layer(xs, wr, g, u, d, 8, y[idx], ids[idx], w[idx], None, residual=False, tol=1e-2,
                               act_quant=True))
+
+
+@pytest.mark.parametrize("T", [1, 777, 4096])
+def test_fp8_fused_dispatch_bitwise(T):
+    """GEMM1 gathering e4m3 token rows itself (default: token-major x_q + per-token scale)
+    computes exactly what the materialised X_perm path (FLAG_XPERM) computes."""
+    wl = Workload(L=1, E=64, k=6, H=1024, h=512, seed=5, fp8=True)
+    x = wl.tokens(T)
+    outs = []
+    for flags in (0, 16):
+        st = wl.stack(max_tokens=4096, flags=flags)
+        outs.append(run_layer(wl, st, 0, x)[0])
+        del st
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))

@@ -39,7 +39,7 @@ def test_synth_generator_is_bit_identical_on_cpu_and_gpu():
 
 
 @pytest.mark.parametrize("flags", [0, 2, 8, 10, 16], ids=["tcgen05", "simt_gemm", "simt_router", "simt_all",
-                                                          "gather_a"])
+                                                          "xperm"])
 @pytest.mark.parametrize("T", [256, 1, 63, 1000])
 def test_tiny_layer_parity(flags, T):
     wl = Workload(**TINY, seed=1)
@@ -213,3 +213,18 @@ def test_config5_zipf_skewed_full_size_sampled():
     idx = np.unique(np.concatenate([[0, T - 1], np.random.default_rng(3).choice(T, 94, replace=False)]))
     wr, g, u, d = wl.host_layer(0)
     print(check_layer(f32(x)[idx], wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None))
+
+
+@pytest.mark.parametrize("T", [1, 129, 5000])
+def test_fused_dispatch_bitwise(T):
+    """GEMM1 gathering token rows of x itself (default: cp.async warps through src_tok)
+    computes exactly what the materialised X_perm path (FLAG_XPERM) computes: same A bytes,
+    same MMAs."""
+    wl = Workload(L=1, E=64, k=8, H=1024, h=768, seed=9)
+    x = wl.tokens(T)
+    outs = []
+    for flags in (0, 16):
+        st = wl.stack(max_tokens=8192, flags=flags)
+        outs.append(run_layer(wl, st, 0, x)[0])
+        del st
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
