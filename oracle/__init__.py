@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "moe_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "attn_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -31,9 +32,9 @@ CFLAGS = ["-O2", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off", "-std=c11"
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (building the checker is not using it)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -64,6 +65,15 @@ def _load():
             lib.oracle_saturation_T.restype = I32
             lib.oracle_calibrated_T.argtypes = [D, D, D, D]
             lib.oracle_calibrated_T.restype = D
+            lib.oracle_rmsnorm.argtypes = [P, P, I64, I32, D, P]
+            lib.oracle_rmsnorm.restype = I32
+            lib.oracle_rope.argtypes = [P, P, I64, I32, I32, D]
+            lib.oracle_rope.restype = I32
+            lib.oracle_attention.argtypes = [P, P, P, P, I32, I32, I32, I32, I32, D, P, I64, P]
+            lib.oracle_attention.restype = I32
+            lib.oracle_attn_layer.argtypes = [P, I64, I32, P, I32, I32, I32, I32, P, P, P, P, P, P, D, D, P, I64,
+                                              P, P]
+            lib.oracle_attn_layer.restype = I32
             lib.oracle_num_threads.argtypes = []
             lib.oracle_num_threads.restype = I32
             lib.oracle_set_num_threads.argtypes = [I32]
@@ -190,3 +200,68 @@ def saturation_T(E, k, H, h, bytes_per_elem, N, gamma, flops_per_s, ag_bytes_per
 def calibrated_T(gamma: float, t_e: float, t_c: float, c_dummy: float) -> float:
     """App. B.4 Eq. 3: T = gamma * (t_e/t_c) * C_dummy."""
     return _load().oracle_calibrated_T(gamma, t_e, t_c, c_dummy)
+
+
+# ------------------------------------------------------------------ NEXT-3: DP attention layer
+# (oracle/attn_oracle.c; PAPER.md:275, :311, :351-353; reading R19)
+
+def rmsnorm(x, w=None, eps: float = 1e-6) -> np.ndarray:
+    """Row-wise RMSNorm x / sqrt(mean(x^2) + eps) * w, fp64."""
+    x = _f32(x)
+    n = x.shape[-1]
+    out = np.empty(x.shape, np.float64)
+    rc = _load().oracle_rmsnorm(_ptr(x), _ptr(None if w is None else _f32(w)), x.size // n, n, float(eps),
+                                _ptr(out))
+    if rc:
+        raise ValueError(f"oracle_rmsnorm rc={rc}")
+    return out
+
+
+def rope(x, pos, theta: float = 1e6) -> np.ndarray:
+    """Rotate-half rotary embedding of x [T, nh, d] at positions pos [T], fp64."""
+    out = np.array(x, dtype=np.float64, copy=True, order="C")
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    T, nh, d = out.shape
+    rc = _load().oracle_rope(_ptr(out), _ptr(pos), T, nh, d, float(theta))
+    if rc:
+        raise ValueError(f"oracle_rope rc={rc}")
+    return out
+
+
+def attention(q, k, v, cu_seqlens, causal: bool = True, scale=None, rows=None) -> np.ndarray:
+    """GQA softmax attention over packed prompts; q [n, Hq, d] (one row per entry of rows,
+    or [T, Hq, d] when rows is None), k / v [T, Hkv, d]; returns [n, Hq, d] fp64."""
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    k = np.ascontiguousarray(k, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
+    Hq, d = q.shape[1], q.shape[2]
+    Hkv = k.shape[1]
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    n = q.shape[0]
+    out = np.empty((n, Hq, d), np.float64)
+    sc = float(1.0 / np.sqrt(d)) if scale is None else float(scale)
+    rc = _load().oracle_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(cu), len(cu) - 1, Hq, Hkv, d, int(causal), sc,
+                                  _ptr(r), 0 if r is None else len(r), _ptr(out))
+    if rc:
+        raise ValueError(f"oracle_attention rc={rc}")
+    return out
+
+
+def attn_layer(x, cu_seqlens, Hq: int, Hkv: int, d: int, w_ln1, w_qkv, w_qn, w_kn, w_o, w_ln2,
+               eps: float = 1e-6, theta: float = 1e6, rows=None):
+    """One DP attention layer (R19) for the tokens in rows (None = all):
+    returns (x' = x + attn, RMSNorm(x'; w_ln2)) as fp32 arrays [n, H]."""
+    x = _f32(x)
+    T, H = x.shape
+    cu = np.ascontiguousarray(cu_seqlens, dtype=np.int32)
+    r = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+    n = T if r is None else len(r)
+    xo = np.empty((n, H), np.float32)
+    xn2 = np.empty((n, H), np.float32)
+    ws = [_f32(a) for a in (w_ln1, w_qkv, w_qn, w_kn, w_o, w_ln2)]
+    rc = _load().oracle_attn_layer(_ptr(x), T, H, _ptr(cu), len(cu) - 1, Hq, Hkv, d, *[_ptr(a) for a in ws],
+                                   float(eps), float(theta), _ptr(r), 0 if r is None else len(r), _ptr(xo), _ptr(xn2))
+    if rc:
+        raise ValueError(f"oracle_attn_layer rc={rc}")
+    return xo, xn2

@@ -150,3 +150,41 @@ def expert_weights_fp8(E: int, H: int, h: int, seed: int, layer: int, device="cp
         scales.append((amax / torch.full_like(amax, 448.0)).squeeze(-1).contiguous())
         del wf
     return out[0], out[1], out[2], scales[0], scales[1], scales[2]
+
+
+# ----------------------------------------------------------------------------------
+# NEXT-3 attention layer recipe (S4, reading R19; Qwen3-235B-A22B attention:
+# H=4096, Hq=64, Hkv=4, d=128): W_qkv ~ N(0, 1/H) [(Hq+2Hkv)d, H]; W_o ~ N(0, 1/(Hq d))
+# [H, Hq d]; RMSNorm weights 1 + N(0, 0.1^2) (w_ln1 [H], w_qn [d], w_kn [d], w_ln2 [H]).
+# Prompt mix: packed prompts of the lengths prompt_lengths() draws.
+# ----------------------------------------------------------------------------------
+KIND_WQKV, KIND_WO, KIND_LN1, KIND_QN, KIND_KN, KIND_LN2 = 7, 8, 9, 10, 11, 12
+
+
+def _norm_weight(n: int, seed: int, tid: int, device) -> torch.Tensor:
+    # 1 + 0.1 z, rounded once to bf16 (fp32 add of a bf16 value and 1.0 is exact)
+    return (normal((n,), seed, tid, 0.1, device).float() + 1.0).to(torch.bfloat16)
+
+
+def attn_weights(H: int, Hq: int, Hkv: int, d: int, seed: int, layer: int, device="cpu"):
+    """(w_ln1, w_qkv, w_qn, w_kn, w_o, w_ln2), bf16."""
+    w_qkv = normal(((Hq + 2 * Hkv) * d, H), seed, tensor_id(KIND_WQKV, layer), 1.0 / math.sqrt(H), device)
+    w_o = normal((H, Hq * d), seed, tensor_id(KIND_WO, layer), 1.0 / math.sqrt(Hq * d), device)
+    return (_norm_weight(H, seed, tensor_id(KIND_LN1, layer), device), w_qkv,
+            _norm_weight(d, seed, tensor_id(KIND_QN, layer), device),
+            _norm_weight(d, seed, tensor_id(KIND_KN, layer), device), w_o,
+            _norm_weight(H, seed, tensor_id(KIND_LN2, layer), device))
+
+
+def prompt_lengths(total: int, mean: int, seed: int, spread: float = 0.5) -> list:
+    """Seeded prompt lengths summing to ``total``: uniform in [mean(1-spread), mean(1+spread)]
+    (spread 0: all equal to mean), the last prompt takes the remainder."""
+    out, left, i = [], total, 0
+    while left > 0:
+        u = _h32_int(_h32_int(seed) ^ _h32_int(0x5EED0000 + i)) / float(M32)
+        n = max(1, int(round(mean * (1.0 - spread + 2.0 * spread * u))))
+        n = min(n, left)
+        out.append(n)
+        left -= n
+        i += 1
+    return out
