@@ -296,6 +296,67 @@ ASYNCEP_API asyncep_status asyncep_router_blocks_stored(asyncep_router* r, int32
                                                         int64_t n);
 ASYNCEP_API asyncep_status asyncep_router_progress(asyncep_router* r, int32_t gpu, int64_t tokens);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3: the data-parallel attention layer before each MoE layer, KV-cache-free
+ * (PAPER.md:275 "pure DP attention"; :311 "after computing attention locally, each GPU
+ * evaluates the current MoE layer"; :351-353 "disables KV storage entirely and computes
+ * attention on the fly").  The paper fixes no attention architecture; reading R19
+ * (S3) is the Qwen3-MoE block:
+ *     xn   = RMSNorm(x; w_ln1)
+ *     qkv  = xn . W_qkv^T                 W_qkv [(Hq + 2 Hkv) d, H]: q rows, then k, then v
+ *     q_h  = RoPE(RMSNorm(q_h; w_qn)), k_g = RoPE(RMSNorm(k_g; w_kn))   (per head of d)
+ *     o    = causal softmax(q k^T / sqrt(d)) v per prompt, query head h reads kv head
+ *            h / (Hq / Hkv) (grouped-query attention); positions restart at 0 per prompt
+ *     x'   = x + o . W_o^T                W_o [H, Hq d]
+ *     xn2  = RMSNorm(x'; w_ln2)           (the input of the MoE layer's router and experts)
+ * Rotary embedding: rotate-half, inv_freq_i = theta^(-2i/d).  All tensors bf16, row-major,
+ * device, caller-owned; fp32 accumulation.  Nothing is stored beyond the call (no KV cache).
+ * Prompts are packed: prompt b holds tokens [cu_seqlens[b], cu_seqlens[b+1]).
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+  int32_t hidden;      /* H (multiple of 256)                                   */
+  int32_t q_heads;     /* Hq (multiple of kv_heads)                             */
+  int32_t kv_heads;    /* Hkv                                                   */
+  int32_t head_dim;    /* d: must be 128                                        */
+  int64_t max_tokens;  /* workspace sizing                                      */
+  int64_t max_prompts; /* workspace sizing (0 = max_tokens)                     */
+  double eps;          /* RMSNorm epsilon (Qwen3: 1e-6)                         */
+  double rope_theta;   /* Qwen3: 1e6                                            */
+} asyncep_attn_config;
+
+/* Workspace bytes asyncep_attn_layer needs (xn, qkv, q, k, V^T, o, projection output, counters). */
+ASYNCEP_API size_t asyncep_attn_workspace_size(const asyncep_attn_config* cfg);
+
+/*
+ * The attention core alone (step 4 of the layer above), on `stream`:
+ *  q  [T, Hq, d], k [T, Hkv, d] bf16 device;  cu_seqlens [B+1] int32 device, non-decreasing,
+ *  cu_seqlens[0] = 0, cu_seqlens[B] = T;  vt [Hkv, d, ldv] bf16 device = V transposed per kv
+ *  head, prompt b's keys at columns [vt_cu[b], vt_cu[b] + len_b) (vt_cu [B+1] int32 device,
+ *  every vt_cu[b] a multiple of 8 -- the TMA start along the contiguous dimension must be
+ *  16-B aligned; columns outside the prompts must hold finite values); ldv % 8 == 0;
+ *  o [T, Hq, d] bf16 output.
+ * Causal within each prompt.  T == 0 is a no-op.  Errors: INVALID_ARG (d != 128, Hq % Hkv,
+ * alignment), CUDA.
+ */
+ASYNCEP_API asyncep_status asyncep_attention(const asyncep_attn_config* cfg, const void* q, const void* k,
+                                             const void* vt, int64_t ldv, const int32_t* vt_cu,
+                                             const int32_t* cu_seqlens, int32_t B, int64_t T, void* o,
+                                             void* stream);
+
+/*
+ * One full attention layer (the formulas above), on `stream`.
+ *  x [T, H] bf16 device; cu_seqlens [B+1] int32 device; weights bf16 device: w_ln1 [H],
+ *  w_qkv [(Hq + 2 Hkv) d, H], w_qn [d], w_kn [d], w_o [H, Hq d], w_ln2 [H];
+ *  x_out [T, H] = x' and xn2_out [T, H] = RMSNorm(x'; w_ln2) (both bf16 device outputs,
+ *  neither may alias x); workspace of asyncep_attn_workspace_size bytes, 256-B aligned.
+ * T > max_tokens or B > max_prompts -> WORKSPACE; T == 0 is a no-op.
+ */
+ASYNCEP_API asyncep_status asyncep_attn_layer(const asyncep_attn_config* cfg, const void* x, int64_t T,
+                                              const int32_t* cu_seqlens, int32_t B, const void* w_ln1,
+                                              const void* w_qkv, const void* w_qn, const void* w_kn, const void* w_o,
+                                              const void* w_ln2, void* x_out, void* xn2_out, void* workspace,
+                                              size_t workspace_bytes, void* stream);
+
 /* Number of kernels the library launched since context creation (host-side counter). */
 ASYNCEP_API int64_t asyncep_kernel_launches(const asyncep_ctx* ctx);
 

@@ -51,6 +51,18 @@ def make_config(num_layers, num_experts, top_k, hidden, ffn, *, expert_dtype=BF1
                   replicate_layer0, norm_topk, max_tokens, gamma, flags)
 
 
+class AttnConfig(ctypes.Structure):
+    """asyncep_attn_config (NEXT-3 attention layer, reading R19)."""
+    _fields_ = [("hidden", ctypes.c_int32), ("q_heads", ctypes.c_int32), ("kv_heads", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("max_tokens", ctypes.c_int64), ("max_prompts", ctypes.c_int64),
+                ("eps", ctypes.c_double), ("rope_theta", ctypes.c_double)]
+
+
+def make_attn_config(hidden, q_heads, kv_heads, head_dim=128, *, max_tokens=1, max_prompts=0, eps=1e-6,
+                     rope_theta=1e6) -> AttnConfig:
+    return AttnConfig(hidden, q_heads, kv_heads, head_dim, max_tokens, max_prompts, eps, rope_theta)
+
+
 _lib = None
 
 
@@ -94,6 +106,10 @@ def lib() -> ctypes.CDLL:
             "asyncep_ep_plan": ([CP, P, P, P, P, P, P, P, ctypes.POINTER(I64)], I32),
             "asyncep_ep_workspace_size": ([CP, I64], SZ),
             "asyncep_ep_forward": ([P, I32, P, I64, P, P, P, I64], I32),
+            "asyncep_attn_workspace_size": ([ctypes.POINTER(AttnConfig)], SZ),
+            "asyncep_attention": ([ctypes.POINTER(AttnConfig), P, P, P, I64, P, P, I32, I64, P, P], I32),
+            "asyncep_attn_layer": ([ctypes.POINTER(AttnConfig), P, I64, P, I32, P, P, P, P, P, P, P, P, P, SZ, P],
+                                   I32),
             "asyncep_destroy": ([P], I32),
         }
         for name, (args, res) in sig.items():
@@ -299,6 +315,31 @@ def nccl_comm_ptr(pg=None) -> int:
     import torch.distributed as dist
     pg = pg or dist.group.WORLD
     return pg._get_backend(torch.device("cuda"))._comm_ptr()
+
+
+# ------------------------------------------------------------------------------ NEXT-3 attention
+def asyncep_attn_workspace_size(cfg: AttnConfig) -> int:
+    n = lib().asyncep_attn_workspace_size(ctypes.byref(cfg))
+    if n == 0:
+        _check(ERR_INVALID_ARG)
+    return n
+
+
+def asyncep_attention(cfg: AttnConfig, q, k, vt, ldv: int, vt_cu, cu_seqlens, o, stream=None) -> None:
+    """Causal GQA attention core: q [T,Hq,d], k [T,Hkv,d], vt [Hkv,d,ldv] with prompt b at columns
+    vt_cu[b] (multiples of 8), cu_seqlens int32 [B+1]."""
+    T = q.shape[0]
+    _check(lib().asyncep_attention(ctypes.byref(cfg), _p(q), _p(k), _p(vt), ldv, _p(vt_cu), _p(cu_seqlens),
+                                   cu_seqlens.shape[0] - 1, T, _p(o),
+                                   _stream(stream or torch.cuda.current_stream())))
+
+
+def asyncep_attn_layer(cfg: AttnConfig, x, cu_seqlens, weights, x_out, xn2_out, workspace, stream=None) -> None:
+    """One DP attention layer; weights = (w_ln1, w_qkv, w_qn, w_kn, w_o, w_ln2)."""
+    _check(lib().asyncep_attn_layer(ctypes.byref(cfg), _p(x), x.shape[0], _p(cu_seqlens), cu_seqlens.shape[0] - 1,
+                                    *[_p(w) for w in weights], _p(x_out), _p(xn2_out), _p(workspace),
+                                    workspace.numel() * workspace.element_size(),
+                                    _stream(stream or torch.cuda.current_stream())))
 
 
 # ------------------------------------------------------------------------------ NEXT-4 admission

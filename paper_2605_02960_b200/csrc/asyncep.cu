@@ -878,6 +878,125 @@ asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double
   return ASYNCEP_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-3 attention layer
+namespace {
+struct AttnWs {
+  size_t xn, qkv, q, k, vt, vcu, o, ao, cnt, total;
+  int64_t ldv;
+};
+AttnWs attn_layout(const asyncep_attn_config& c) {
+  AttnWs L{};
+  const int64_t T = c.max_tokens, H = c.hidden, d = c.head_dim;
+  const int64_t nqkv = (int64_t)(c.q_heads + 2 * c.kv_heads) * d;
+  const int64_t P = c.max_prompts > 0 ? c.max_prompts : T;
+  L.ldv = (T + 7 * P + 7) / 8 * 8;  // every prompt's V^T columns start on a multiple of 8
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += (bytes + 255) / 256 * 256;
+    return at;
+  };
+  L.xn = take((size_t)T * H * 2);
+  L.qkv = take((size_t)T * nqkv * 2);
+  L.q = take((size_t)T * c.q_heads * d * 2);
+  L.k = take((size_t)T * c.kv_heads * d * 2);
+  L.vt = take((size_t)c.kv_heads * d * L.ldv * 2);
+  L.vcu = take((size_t)(P + 1) * 4);
+  L.o = take((size_t)T * c.q_heads * d * 2);
+  L.ao = take((size_t)T * H * 2);
+  L.cnt = take(256);
+  L.total = o;
+  return L;
+}
+asyncep_status attn_check(const asyncep_attn_config* c) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "attn config is NULL");
+  if (c->head_dim != 128) return fail(ASYNCEP_ERR_INVALID_ARG, "head_dim must be 128 (got %d)", c->head_dim);
+  if (c->q_heads <= 0 || c->kv_heads <= 0 || c->q_heads % c->kv_heads)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "q_heads must be a positive multiple of kv_heads");
+  if (c->hidden <= 0 || c->hidden % 256) return fail(ASYNCEP_ERR_INVALID_ARG, "hidden must be a multiple of 256");
+  if (((int64_t)(c->q_heads + 2 * c->kv_heads) * c->head_dim) % 256)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "(q_heads + 2 kv_heads) * head_dim must be a multiple of 256");
+  if (c->max_tokens < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "max_tokens < 0");
+  return ASYNCEP_OK;
+}
+int device_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+}  // namespace
+
+size_t asyncep_attn_workspace_size(const asyncep_attn_config* c) {
+  if (attn_check(c) != ASYNCEP_OK) return 0;
+  return attn_layout(*c).total;
+}
+
+asyncep_status asyncep_attention(const asyncep_attn_config* c, const void* q, const void* k, const void* vt,
+                                 int64_t ldv, const int32_t* vt_cu, const int32_t* cu, int32_t B, int64_t T, void* o,
+                                 void* stream) {
+  if (asyncep_status st = attn_check(c)) return st;
+  if (T == 0) return ASYNCEP_OK;
+  if (!q || !k || !vt || !vt_cu || !cu || !o || B <= 0 || T < 0 || ldv < T || ldv % 8)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attention: bad pointers / B / T / ldv");
+  if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)vt | (uintptr_t)o) % 16)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attention: tensors must be 16-B aligned");
+  if (!aep::launch_flash_attn((const bf16*)q, (const bf16*)k, (const bf16*)vt, ldv, cu, vt_cu, B, T, c->q_heads,
+                              c->kv_heads, (bf16*)o, (cudaStream_t)stream))
+    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (attention maps)");
+  CUDA_TRY(cudaGetLastError());
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_attn_layer(const asyncep_attn_config* c, const void* x, int64_t T, const int32_t* cu,
+                                  int32_t B, const void* w_ln1, const void* w_qkv, const void* w_qn,
+                                  const void* w_kn, const void* w_o, const void* w_ln2, void* x_out, void* xn2_out,
+                                  void* workspace, size_t ws_bytes, void* stream) {
+  if (asyncep_status st = attn_check(c)) return st;
+  if (T == 0) return ASYNCEP_OK;
+  if (T < 0 || T > c->max_tokens) return fail(ASYNCEP_ERR_WORKSPACE, "T=%lld > max_tokens", (long long)T);
+  if (c->max_prompts > 0 && B > c->max_prompts) return fail(ASYNCEP_ERR_WORKSPACE, "B=%d > max_prompts", B);
+  if (!x || !cu || B <= 0 || !w_ln1 || !w_qkv || !w_qn || !w_kn || !w_o || !w_ln2 || !x_out || !xn2_out ||
+      !workspace)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attn_layer: null argument");
+  const AttnWs L = attn_layout(*c);
+  if (ws_bytes < L.total || (uintptr_t)workspace % 256)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attn_layer: workspace too small or misaligned");
+  if (x_out == x || xn2_out == x) return fail(ASYNCEP_ERR_INVALID_ARG, "outputs may not alias x");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* ws = (uint8_t*)workspace;
+  const int H = c->hidden, Hq = c->q_heads, Hkv = c->kv_heads, d = c->head_dim;
+  const int nqkv = (Hq + 2 * Hkv) * d;
+  const float eps = (float)c->eps;
+  int* cnt = (int*)(ws + L.cnt);
+  CUDA_TRY(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
+  bf16* xn = (bf16*)(ws + L.xn);
+  bf16* qkv = (bf16*)(ws + L.qkv);
+  bf16* qb = (bf16*)(ws + L.q);
+  bf16* kb = (bf16*)(ws + L.k);
+  bf16* vt = (bf16*)(ws + L.vt);
+  bf16* ob = (bf16*)(ws + L.o);
+  bf16* ao = (bf16*)(ws + L.ao);
+  aep::launch_rmsnorm((const bf16*)x, (const bf16*)w_ln1, T, H, eps, xn, st);
+  if (!aep::launch_dense_gemm_tc(xn, T, H, (const bf16*)w_qkv, nqkv, qkv, cnt, device_sms(), st))
+    return fail(ASYNCEP_ERR_CUDA, "QKV projection: tensor map encoding failed");
+  aep::launch_qk_rope(qkv, T, Hq, Hkv, cu, B, (const bf16*)w_qn, (const bf16*)w_kn, eps, (float)c->rope_theta, qb, kb,
+                      st);
+  int32_t* vcu = (int32_t*)(ws + L.vcu);
+  const int64_t ldv = (T + 7 * (int64_t)B + 7) / 8 * 8;
+  aep::launch_v_transpose(qkv, T, Hq, Hkv, cu, B, vcu, ldv, vt, st);
+  if (!aep::launch_flash_attn(qb, kb, vt, ldv, cu, vcu, B, T, Hq, Hkv, ob, st))
+    return fail(ASYNCEP_ERR_CUDA, "attention: tensor map encoding failed");
+  if (!aep::launch_dense_gemm_tc(ob, T, Hq * d, (const bf16*)w_o, H, ao, cnt + 1, device_sms(), st))
+    return fail(ASYNCEP_ERR_CUDA, "O projection: tensor map encoding failed");
+  aep::launch_residual_rmsnorm((const bf16*)x, ao, (const bf16*)w_ln2, T, H, eps, (bf16*)x_out, (bf16*)xn2_out, st);
+  CUDA_TRY(cudaGetLastError());
+  return ASYNCEP_OK;
+}
+
 int64_t asyncep_kernel_launches(const asyncep_ctx* c) { return c ? c->launches : 0; }
 
 asyncep_status asyncep_destroy(asyncep_ctx* c) {

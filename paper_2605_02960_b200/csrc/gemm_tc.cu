@@ -772,6 +772,52 @@ void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
                    nullptr, true);
 }
 
+// ------------------------------------------------------------------ dense GEMM (NEXT-3 projections)
+bool launch_dense_gemm_tc(const bf16* A, int64_t M, int K, const bf16* W, int N, bf16* out, int* sched, int num_sms,
+                          cudaStream_t s) {
+  if (M <= 0) return true;
+  if (K % 64 || N % 256) return false;
+  CUtensorMap ma, mb, mo;
+  {
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)M};
+    const uint64_t strides[1] = {(uint64_t)K * 2};
+    const uint32_t box[2] = {BK, BM};
+    if (!encode_tmap(&ma, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, A, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  {
+    const uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, 1};
+    const uint64_t strides[2] = {(uint64_t)K * 2, (uint64_t)K * 2 * N};
+    const uint32_t box[3] = {BK, 128, 1};  // 256-row W tile, half per CTA of the pair
+    if (!encode_tmap(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  {
+    const uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
+    const uint64_t strides[1] = {(uint64_t)N * 2};
+    const uint32_t box[2] = {64, 32};
+    if (!encode_tmap(&mo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+  }
+  TcArgs a{};
+  a.E = 1;
+  a.dense_rows = (int)M;
+  a.K = K;
+  a.BN = 256;
+  a.n_tiles = N / 256;
+  a.n_out = N;
+  a.ts_scale = 1;
+  a.raster = 0;
+  a.pol_a = 0;
+  a.pol_b = 1;  // the weight tile is reused by every row tile
+  a.sched = sched;
+  const int units = num_sms / 2;
+  const int64_t total = (M + 255) / 256 * a.n_tiles;
+  const int grid = 2 * (int)(total < units ? total : units);
+  launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s);
+  return true;
+}
+
 // ------------------------------------------------------------------ router on tcgen05
 // Logits tile = 128 tokens x E_pad experts (M=128, N=E_pad, K=H, 1-CTA) in TMEM, fp32;
 // the epilogue threads (one per token) do the top-k straight out of TMEM.

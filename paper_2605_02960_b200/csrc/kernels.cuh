@@ -125,6 +125,22 @@ void launch_pack_fp8(const uint8_t* gate, const uint8_t* up, const uint8_t* down
 // One thread spinning on %globaltimer for `ns` nanoseconds (link-bandwidth emulation).
 void launch_spin_ns(uint64_t ns, cudaStream_t s);
 
+// ---- NEXT-3 attention layer (attn.cu) ----
+void launch_rmsnorm(const bf16* x, const bf16* w, int64_t rows, int n, float eps, bf16* out, cudaStream_t s);
+void launch_residual_rmsnorm(const bf16* x, const bf16* a, const bf16* w, int64_t rows, int n, float eps, bf16* xo,
+                             bf16* xn, cudaStream_t s);
+void launch_qk_rope(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32_t* cu, int B, const bf16* w_qn,
+                    const bf16* w_kn, float eps, float theta, bf16* q, bf16* k, cudaStream_t s);
+// vcu [B+1] (output): per-prompt V^T column offsets, each prompt padded to 8 columns
+void launch_v_transpose(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32_t* cu, int B, int32_t* vcu,
+                        int64_t ldv, bf16* vt, cudaStream_t s);
+bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv, const int32_t* cu,
+                       const int32_t* vcu, int B, int64_t T, int Hq, int Hkv, bf16* o, cudaStream_t s);
+// dense out[M, N] = A[M, K] . W[N, K]^T on the tcgen05 GEMM (CTA pairs, N % 256 == 0,
+// K % 64 == 0); sched: a zeroed int for the dynamic tile scheduler (nullable)
+bool launch_dense_gemm_tc(const bf16* A, int64_t M, int K, const bf16* W, int N, bf16* out, int* sched, int num_sms,
+                          cudaStream_t s);
+
 // Driver entry point for cuTensorMapEncodeTiled (resolved once through the runtime).
 bool encode_tmap(CUtensorMap* map, CUtensorMapDataType dtype, int rank, const void* base, const uint64_t* dims,
                  const uint64_t* strides_bytes /* rank-1 entries */, const uint32_t* box, CUtensorMapSwizzle sw);
