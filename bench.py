@@ -29,6 +29,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -36,6 +38,7 @@ METRIC = "tokens/s and MFU per B200, Qwen3-235B MoE layers, 1/2/4/8 GPUs; expose
 L_, E_, K_, H_, h_ = 8, 128, 8, 4096, 1536
 T_LOC = 32768
 FLOPS_TOK_LAYER = 2 * H_ * E_ + 6 * K_ * H_ * h_          # 303,038,464 (router + experts)
+ATT_HQ, ATT_HKV = 64, 4                                    # Qwen3-235B-A22B attention (NEXT-3, R19)
 GEMM1_FLOPS_TOK = 4 * K_ * H_ * h_                        # gate/up: 2 * k * H * 2h
 GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
 SPEC_BF16 = 2.25e15
@@ -204,6 +207,11 @@ def main():
                     help="NEXT-2: expert shards in pinned host memory, a W-deep device window filled over PCIe")
     ap.add_argument("--zipf", type=float, default=0.0, metavar="S",
                     help="Zipf-skewed routing (reading R14, BASELINE config 5 uses S=0.35)")
+    ap.add_argument("--attn", action="store_true",
+                    help="NEXT-3: decoder layers = DP attention (KV-cache-free, Qwen3-235B heads) + MoE; the "
+                         "gather of layer l+1 overlaps both")
+    ap.add_argument("--prompt", type=int, default=4096,
+                    help="prompt length of the packed batch with --attn (tokens/GPU split into prompts)")
     ap.add_argument("--fp8", action="store_true",
                     help="FP8 e4m3 experts (BASELINE config 4) instead of BF16 (config 3)")
     args = ap.parse_args()
@@ -240,10 +248,19 @@ def main():
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8, offload_window=args.offload)
     local_shards = stack.peer_shards() if emu > 1 else None
+    cu = None
+    attn_flops_layer = 0.0
+    if args.attn:
+        lengths = synth.prompt_lengths(T, args.prompt, seed, spread=0.0)
+        cu = torch.tensor([0] + list(np.cumsum(lengths)), dtype=torch.int32, device=dev)
+        stack.enable_attention(lambda l: synth.attn_weights(H_, ATT_HQ, ATT_HKV, 128, seed, l, device=dev),
+                               ATT_HQ, ATT_HKV, max_prompts=len(lengths))
+        pairs = sum(n * (n + 1) // 2 for n in lengths)
+        attn_flops_layer = 4.0 * 128 * ATT_HQ * pairs + 2.0 * T * H_ * ((ATT_HQ + 2 * ATT_HKV) * 128 + ATT_HQ * 128)
     if args.ep:  # contrast layer: every rank keeps its shard; tokens travel instead of weights
         _run = lambda xin, out: stack.run_ep(xin, out=out)
     else:
-        _run = lambda xin, out: stack.run(xin, out=out, local_shards=local_shards)
+        _run = lambda xin, out: stack.run(xin, out=out, local_shards=local_shards, cu_seqlens=cu)
     if emu > 1 and args.link_gbs > 0:
         A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
     # tokens: DP -- every rank its own batch
@@ -281,7 +298,7 @@ def main():
     ms_step = ms_max / args.steps
     value = world * T * args.steps / (ms_max / 1e3)     # whole-job tokens/s
     per_gpu = value / world
-    mfu_flops = per_gpu * L * FLOPS_TOK_LAYER
+    mfu_flops = per_gpu * L * FLOPS_TOK_LAYER + (per_gpu / T) * L * attn_flops_layer
 
     # ---------------- e2e: public API with host buffers (pinned), copies in the timed region
     xh = x.cpu().pin_memory()
@@ -305,6 +322,24 @@ def main():
     if world > 1:
         dist.all_reduce(t2, op=dist.ReduceOp.MAX)
     e2e_value = world * T * args.steps / (t2.item() / 1e3)
+
+    attn_info = None
+    if args.attn:  # attention half alone (outside the timed region), for the layer breakdown
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        stack.attention(0, x, cu)
+        barrier()
+        a0.record(cs)
+        for l in range(L):
+            stack.attention(l, x, cu)
+        a1.record(cs)
+        barrier()
+        a_ms = a0.elapsed_time(a1) / L
+        attn_info = {"ms_per_layer": a_ms, "prompt_len": args.prompt, "prompts": int(cu.numel() - 1),
+                     "q_heads": ATT_HQ, "kv_heads": ATT_HKV, "head_dim": 128,
+                     "flops_per_layer": attn_flops_layer, "tflops": attn_flops_layer / (a_ms / 1e3) / 1e12,
+                     "note": "RMSNorm + QKV GEMM + QK-norm/RoPE + causal flash attention + O GEMM + "
+                             "residual/RMSNorm (reading R19); timed separately, included in the step"}
 
     peaks, peak_src = load_peaks()
     # dominant kernel: GEMM1 (gate/up + SwiGLU), stage-timed with CUDA events on the
@@ -335,7 +370,9 @@ def main():
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp8_e4m3" if args.fp8 else "bf16", "data": "synthetic",
-        "config": {"workload": f"qwen3-235b-a22b moe-layer stack, {L} layers, E=128 k=8 H=4096 h=1536, "
+        "config": {"workload": (f"qwen3-235b-a22b decoder-layer stack (DP attention Hq=64 Hkv=4 d=128, KV-cache-free, "
+                                f"{args.prompt}-token prompts + MoE), " if args.attn else
+                                "qwen3-235b-a22b moe-layer stack, ") + f"{L} layers, E=128 k=8 H=4096 h=1536, "
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
@@ -354,6 +391,7 @@ def main():
                 "vs_measured_sustained": mfu_flops / (peak_tf * 1e12),
                 "flops_per_token_layer": FLOPS_TOK_LAYER},
         "stage_ms_per_layer": per_layer_ms,
+        "attention": attn_info,
         "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
                          "flops_per_s": f_gemm, "ag_bytes_per_s": bw,
                          "note": "Eq. 1 per layer, F = measured grouped-GEMM rate of this run"},

@@ -61,11 +61,35 @@ class MoEStack:
         self.ctx = A.asyncep_init(self.cfg, nccl_comm, self.compute_stream, self.comm_stream, self.router_w,
                                   self.shards, self.slots[0], self.slots[1], self.workspace)
         self._bufs = None
+        self.attn_w = None
         if offload_window:
             nb = A.asyncep_slot_bytes(self.cfg) if world_size == 1 else A.asyncep_shard_bytes(self.cfg)
             self.window = [torch.empty(nb, dtype=torch.uint8, device=self.device) for _ in range(offload_window)]
             self.h2d_stream = torch.cuda.Stream(self.device)
             A.asyncep_enable_offload(self.ctx, self.host_shards, self.window, offload_window, self.h2d_stream)
+
+    def enable_attention(self, attn_fn, q_heads: int, kv_heads: int, head_dim: int = 128, max_prompts: int = 0,
+                         eps: float = 1e-6, rope_theta: float = 1e6) -> None:
+        """NEXT-3: run each layer as a decoder layer, DP attention (KV-cache-free) then MoE:
+        x' = x + Attn_l(x);  x_{l+1} = x' + MoE_l(RMSNorm(x'))  (reading R19).
+        attn_fn(l) -> (w_ln1, w_qkv, w_qn, w_kn, w_o, w_ln2) bf16 tensors (replicated on
+        every rank).  The gather of layer l+1 then overlaps attention and MoE."""
+        self.attn_cfg = A.make_attn_config(self.H, q_heads, kv_heads, head_dim, max_tokens=self.cfg.max_tokens,
+                                           max_prompts=max_prompts, eps=eps, rope_theta=rope_theta)
+        self.attn_w = [tuple(t.to(self.device, torch.bfloat16).contiguous() for t in attn_fn(l))
+                       for l in range(self.L)]
+        self.attn_ws = torch.empty(A.asyncep_attn_workspace_size(self.attn_cfg), dtype=torch.uint8,
+                                   device=self.device)
+        self._abufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
+                       for _ in range(2)]
+
+    def attention(self, l, x, cu_seqlens):
+        """Attention half of decoder layer l: returns (x', RMSNorm(x'; w_ln2)) views."""
+        T = x.shape[0]
+        xa, xn = self._abufs[0][:T], self._abufs[1][:T]
+        A.asyncep_attn_layer(self.attn_cfg, x, cu_seqlens, self.attn_w[l], xa, xn, self.attn_ws,
+                             stream=self.compute_stream)
+        return xa, xn
 
     def pack(self, l: int, experts: range) -> torch.Tensor:
         """Packed blobs of ``experts`` of layer l (the shard format of asyncep.h)."""
@@ -113,8 +137,10 @@ class MoEStack:
         return A.asyncep_moe_forward(self.ctx, l, x, residual=residual, y=y, topk_ids_out=ids,
                                      topk_w_out=w, expert_counts_out=counts)
 
-    def run(self, x, residual=True, out=None, local_shards=None, record=None):
-        """One pass of the whole stack: x_{l+1} = x_l + MoE_l(x_l) (reading R9).
+    def run(self, x, residual=True, out=None, local_shards=None, record=None, cu_seqlens=None):
+        """One pass of the whole stack: x_{l+1} = x_l + MoE_l(x_l) (reading R9), or with
+        attention enabled the decoder layer x' = x + Attn_l(x), x_{l+1} = x' + MoE_l(RMSNorm(x'))
+        over the packed prompts cu_seqlens (int32 device [B+1]).
         Returns the final activations (a ping-pong buffer unless ``out`` is given).
         ``record(l, x_l)`` (optional) sees each layer's input before it runs."""
         T = x.shape[0]
@@ -132,7 +158,11 @@ class MoEStack:
             if record is not None:
                 record(l, cur)
             dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
-            self.forward(l, cur, residual=cur if residual else None, y=dst)
+            if self.attn_w is not None:
+                xa, xn = self.attention(l, cur, cu_seqlens)
+                self.forward(l, xn, residual=xa, y=dst)
+            else:
+                self.forward(l, cur, residual=cur if residual else None, y=dst)
             cur = dst
         return cur
 
