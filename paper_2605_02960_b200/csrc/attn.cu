@@ -17,10 +17,11 @@
 //            one block ahead of PV_j = P_j V_j (A = P from smem, B = V^T_j) accumulated in a
 //            TMEM O (accumulate flag off for j = 0)
 //   warp 2   TMEM allocator (512 columns: S0, S1, O)
-//   warps 4-7 softmax, thread = query row: S row from TMEM (4 x 32 columns), scale to the
-//            log2 domain, causal / prompt-end mask on the diagonal block, row max, p =
-//            exp2(s - m), row sum in fp32, P as bf16 into the 128-B-swizzled smem tile the
-//            MMA reads.  The running max is only moved (and O rescaled in TMEM) when it grows
+//   warps 4-7 softmax, thread = query row: S row from TMEM (4 x 32 columns), causal /
+//            prompt-end mask on the diagonal block, row max, p = exp2(s * scale - m) (one FFMA
+//            + ex2), P as bf16 into the 128-B-swizzled smem tile the MMA reads.  The row sums
+//            come from the tensor core: V^T carries 16 rows of ones, so PV (N = 144) writes
+//            sum_j p_j next to O.  The running max is only moved (and O rescaled in TMEM) when it grows
 //            by more than 8 (log2 units): the final O / l uses the same stale max in both, so
 //            the result is exact, and O is rarely touched.
 // The rows of a tile past the end of its prompt are computed but never stored.
@@ -29,6 +30,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -42,6 +44,11 @@ constexpr int FA_BN = 128;  // keys per block
 constexpr int FA_D = 128;   // head dim
 constexpr int FA_KB = 16 * 1024;       // one [128 rows x 128 B] swizzled k-block
 constexpr int FA_TILE = 2 * FA_KB;     // a 128 x 128 bf16 operand tile (2 k-blocks of 64)
+// V^T k-blocks carry 16 extra rows of ones after the 128 d rows: PV with N = 144 also
+// yields the row sums of P (columns 128..143 of O), so the softmax warps never add up p.
+constexpr int FA_VN = FA_D + 16;
+constexpr int FA_VKB = FA_VN * 128;    // 18 KB
+constexpr int FA_VTILE = 2 * FA_VKB;
 constexpr int FA_NTHREADS = 256;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 
@@ -50,7 +57,7 @@ struct FaSmem {
   static constexpr int Q = 0;
   static constexpr int K0 = Q + FA_TILE;
   static constexpr int V0 = K0 + 2 * FA_TILE;
-  static constexpr int P = V0 + 2 * FA_TILE;
+  static constexpr int P = V0 + 2 * FA_VTILE;
   static constexpr int BAR = P + FA_TILE;
   static constexpr int BYTES = BAR + 256;
   static constexpr int ALLOC = BYTES + 1024;  // alignment slack
@@ -136,6 +143,12 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  for (int i = threadIdx.x; i < 4 * 16 * 128 / 16; i += FA_NTHREADS) {  // 4 k-blocks x 2 KB of bf16 1.0
+    const int kb = i / 128, off = (i % 128) * 16;
+    const uint32_t one2 = 0x3F803F80u;
+    st_shared_v4(smem_u32(smem + FaSmem::V0 + kb * FA_VKB + FA_KB + off), one2, one2, one2, one2);
+  }
+  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -162,18 +175,19 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
         mbar_wait(&v_empty[st], ph);
         mbar_arrive_expect_tx(&v_full[st], FA_TILE);
         for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + FaSmem::V0 + st * FA_TILE + c * FA_KB, &map_vt, &v_full[st],
+          tma_load_3d_nohint(smem + FaSmem::V0 + st * FA_VTILE + c * FA_VKB, &map_vt, &v_full[st],
                              vstart + j * FA_BN + c * 64, 0, kvh);
       }
     }
     __syncwarp();
   } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);  // M = 128, N = 128 (keys or d)
+    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);     // S: M = 128, N = 128 keys
+    constexpr uint32_t idesc_pv = make_idesc(FA_BM, FA_VN, true);  // PV: N = 128 d + 16 sum columns
     const uint64_t dq = make_smem_desc_sw128(smem_u32(smem + FaSmem::Q));
     const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + FaSmem::K0));
     const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + FaSmem::V0));
     const uint64_t dp = make_smem_desc_sw128(smem_u32(smem + FaSmem::P));
-    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4;
+    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4, kVkb = FA_VKB >> 4, kVtile = FA_VTILE >> 4;
     mbar_wait(q_full, 0);
     auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j & 1]
       const int st = j & 1;
@@ -202,7 +216,8 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {  // keys = 128 = 2 k-blocks x 4 steps of 16
           const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
-          mma_bf16(t_o, dp + off, dv + st * kTile + off, idesc, (j > 0 || k > 0) ? 1u : 0u);
+          const uint64_t voff = (uint64_t)(k >> 2) * kVkb + (uint64_t)(k & 3) * 2;
+          mma_bf16(t_o, dp + off, dv + st * kVtile + voff, idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
         }
         tc_commit(pv_done);
         tc_commit(&v_empty[st]);
@@ -214,7 +229,8 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
     const int r = ew * 32 + lane;           // query row in the tile
     const int qpos = q0 + r;                // position in the prompt
     const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    float m_used = -1e30f, l = 0.f;
+    float m_used = -1e30f;  // running max in scaled log2 units (moved only by > 8)
+    const float scl = p.scale_log2;
     const uint32_t p_base = smem_u32(smem + FaSmem::P) + (uint32_t)r * 128;
     for (int j = 0; j < nblk; ++j) {
       const int st = j & 1;
@@ -227,41 +243,36 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[st]);
-      // scale to log2 units, mask, row max
-      const bool diag = (j == nblk - 1);
-      const int kpos0 = j * FA_BN;
+      // causal / prompt-end mask (diagonal block only), raw row max
+      if (j == nblk - 1) {
+        const int lim = min(qpos, len - 1) - j * FA_BN;  // keys c <= lim are visible
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > lim) s[c] = __float_as_uint(-INFINITY);
+      }
       float mx = -1e30f;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
-        float v = __uint_as_float(s[c]) * p.scale_log2;
-        if (diag && (kpos0 + c > qpos || kpos0 + c >= len)) v = -INFINITY;
-        s[c] = __float_as_uint(v);
-        mx = fmaxf(mx, v);
-      }
+      for (int c = 0; c < 128; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
+      mx *= scl;
       float alpha = 1.f;
       const bool resc = mx > m_used + kRescaleThresh;
       if (resc) {
         alpha = fast_exp2(m_used - mx);
         m_used = mx;
-        l *= alpha;
       }
-      // p = exp2(s - m), row sum, bf16 pack (64 words)
+      // p = exp2(s * scale - m): one FFMA + ex2 per element, bf16 pack (64 words)
       uint32_t pk[64];
-      float sum = 0.f;
+      const float nm = -m_used;
 #pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float a = fast_exp2(__uint_as_float(s[2 * c]) - m_used);
-        const float b = fast_exp2(__uint_as_float(s[2 * c + 1]) - m_used);
-        sum += a + b;
-        pk[c] = pack_bf16x2(a, b);
-      }
-      l += sum;
-      // PV_{j-1} done: the P buffer is free and O is final for blocks < j
+      for (int c = 0; c < 64; ++c)
+        pk[c] = pack_bf16x2(fast_exp2(fmaf(__uint_as_float(s[2 * c]), scl, nm)),
+                            fast_exp2(fmaf(__uint_as_float(s[2 * c + 1]), scl, nm)));
+      // PV_{j-1} done: the P buffer is free and O (with its sum columns) is final for blocks < j
       if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
       tc_fence_after();
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {  // rare: rescale this warp's O rows in TMEM
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {  // rare: rescale this warp's O rows (+ sums)
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 5; ++c) {
           uint32_t o[32];
           tmem_ld32(t_o + lane_off + c * 32, o);
           tmem_ld_wait();
@@ -284,10 +295,13 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
     }
-    // epilogue: O / l -> bf16 -> o[start + qpos, head, :]
+    // epilogue: O / l -> bf16 -> o[start + qpos, head, :]; l = O column 128 (P . ones)
     mbar_wait(pv_done, (nblk - 1) & 1);
     tc_fence_after();
-    const float inv = 1.f / l;
+    uint32_t lsum[8];
+    tmem_ld8(t_o + lane_off + FA_D, lsum);
+    tmem_ld_wait();
+    const float inv = 1.f / __uint_as_float(lsum[0]);
     const bool valid = qpos < len;
     __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
 #pragma unroll 1
@@ -311,6 +325,277 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ flash attention, two query tiles
+// v2: one CTA per (query head, pair of 128-query tiles of a prompt) = 256 queries sharing every
+// K / V^T block (half the operand traffic per FLOP of v1).  320 threads:
+//   warps 0-3  softmax of tile A (rows 0-127), warps 4-7 softmax of tile B (rows 128-255):
+//              two softmax warps per SMSP, so one's exp / pack / max latency hides the other's
+//   warp 8     TMA producer (Q_A, Q_B once; K and V^T blocks in a 2-stage ring)
+//   warp 9     TMEM allocator + MMA issuer
+// TMEM (512 columns): per tile t, S_t at [256t, 256t + 128) and O_t at [256t + 128, 256t + 256).
+// P_t is written by the softmax threads (tcgen05.st, bf16 pairs) over the first 64 columns of
+// S_t and read from TMEM by PV_t (A operand in TMEM, "ts" MMA) -- no smem round trip, no proxy
+// fence.  Issue order per key block j: PV_A(j), S_A(j+1), PV_B(j), S_B(j+1); the tensor pipe
+// executes one thread's MMAs in order, so S_t(j+1) overwrites S/P_t only after PV_t(j) read it,
+// and each softmax group has the other tile's PV + S time to produce its next P.
+constexpr int FA2_NTHREADS = 320;
+struct Fa2Smem {
+  static constexpr int QA = 0;
+  static constexpr int QB = QA + FA_TILE;
+  static constexpr int K0 = QB + FA_TILE;
+  static constexpr int V0 = K0 + 2 * FA_TILE;
+  static constexpr int BAR = V0 + 2 * FA_TILE;
+  static constexpr int BYTES = BAR + 256;
+  static constexpr int ALLOC = BYTES + 1024;
+};
+
+// (prompt, tile pair) of linear index u: prompts in order, each prompt's pairs heaviest first
+__device__ bool fa2_pair(const int32_t* cu, int B, int u, int& b, int& pair, int& start, int& len) {
+  int acc = 0;
+  for (int i = 0; i < B; ++i) {
+    const int s = cu[i], L = cu[i + 1] - s;
+    const int np = (L + 2 * FA_BM - 1) / (2 * FA_BM);
+    if (u < acc + np) {
+      b = i;
+      start = s;
+      len = L;
+      pair = np - 1 - (u - acc);
+      return true;
+    }
+    acc += np;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(FA2_NTHREADS, 1)
+    flash_attn2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Fa2Smem::BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;    // [2]
+  uint64_t* k_empty = bars + 3;   // [2]
+  uint64_t* v_full = bars + 5;    // [2]
+  uint64_t* v_empty = bars + 7;   // [2]
+  uint64_t* s_full = bars + 9;    // [tile]
+  uint64_t* p_full = bars + 11;   // [tile]
+  uint64_t* pv_done = bars + 13;  // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  __shared__ int s_job[4];
+
+  const int warp = warp_id(), lane = lane_id();
+  const int head = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int b = 0, pair = 0, start = 0, len = 0;
+    const bool ok = fa2_pair(p.cu, p.B, blockIdx.y, b, pair, start, len);
+    s_job[0] = ok ? pair : -1;
+    s_job[1] = start;
+    s_job[2] = len;
+    s_job[3] = ok ? p.vcu[b] : 0;
+  }
+  __syncthreads();
+  const int pair = s_job[0];
+  if (pair < 0) return;
+  const int start = s_job[1], len = s_job[2], vstart = s_job[3];
+  const int q0 = pair * 2 * FA_BM;           // first query position of tile A
+  const int nA = 2 * pair + 1, nB = 2 * pair + 2;  // causal key blocks of tiles A and B
+  const int kvh = head / (p.Hq / p.Hkv);
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&map_q);
+      tma_prefetch_desc(&map_k);
+      tma_prefetch_desc(&map_vt);
+      mbar_arrive_expect_tx(q_full, 2 * FA_TILE);
+      for (int c = 0; c < 2; ++c) {
+        tma_load_3d_nohint(smem + Fa2Smem::QA + c * FA_KB, &map_q, q_full, c * 64, head, start + q0);
+        tma_load_3d_nohint(smem + Fa2Smem::QB + c * FA_KB, &map_q, q_full, c * 64, head, start + q0 + FA_BM);
+      }
+      for (int j = 0; j < nB; ++j) {
+        const int st = j & 1;
+        const uint32_t ph = ((j >> 1) & 1) ^ 1;
+        mbar_wait(&k_empty[st], ph);
+        mbar_arrive_expect_tx(&k_full[st], FA_TILE);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d_nohint(smem + Fa2Smem::K0 + st * FA_TILE + c * FA_KB, &map_k, &k_full[st], c * 64, kvh,
+                             start + j * FA_BN);
+        mbar_wait(&v_empty[st], ph);
+        mbar_arrive_expect_tx(&v_full[st], FA_TILE);
+        for (int c = 0; c < 2; ++c)
+          tma_load_3d_nohint(smem + Fa2Smem::V0 + st * FA_TILE + c * FA_KB, &map_vt, &v_full[st],
+                             vstart + j * FA_BN + c * 64, 0, kvh);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);  // M = 128, N = 128 (keys or d)
+    const uint64_t dq[2] = {make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QA)),
+                            make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QB))};
+    const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::K0));
+    const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::V0));
+    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4;
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int t, int j, bool release_k) {  // S_t(j) = Q_t K_j^T
+      const int st = j & 1;
+      if (t == 0 || j >= nA) mbar_wait(&k_full[st], (j >> 1) & 1);  // first user of K_j waits for it
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
+          mma_bf16(tmem + 256 * t, dq[t] + off, dk + st * kTile + off, idesc, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[t]);
+        if (release_k) tc_commit(&k_empty[st]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int t, int j, bool release_v) {  // O_t += P_t(j) V_j
+      const int st = j & 1;
+      mbar_wait(&p_full[t], j & 1);
+      if (t == 0 || j >= nA) mbar_wait(&v_full[st], (j >> 1) & 1);
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {  // 128 keys = 8 x 16: P columns advance by 8 (2 bf16 each)
+          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
+          mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, dv + st * kTile + off, idesc,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&pv_done[t]);
+        if (release_v) tc_commit(&v_empty[st]);
+      }
+      __syncwarp();
+    };
+    issue_s(0, 0, false);
+    issue_s(1, 0, true);
+    for (int j = 0; j < nB; ++j) {
+      if (j < nA) {
+        issue_pv(0, j, false);
+        if (j + 1 < nA) issue_s(0, j + 1, false);
+      }
+      issue_pv(1, j, true);
+      if (j + 1 < nB) issue_s(1, j + 1, true);
+    }
+  } else {
+    // softmax: warps 0-3 tile A, 4-7 tile B; thread = query row (TMEM lane)
+    const int t = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const int qpos = q0 + t * FA_BM + r;
+    const int nblk = t == 0 ? nA : nB;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + 256 * t + lane_off, t_o = t_s + 128;
+    const float scl = p.scale_log2;
+    float m_used = -1e30f, l0 = 0.f, l1 = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      uint32_t s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * c));
+      tmem_ld_wait();
+      if (j == nblk - 1 || (t == 1 && j == nblk - 2)) {  // blocks that can hold masked keys
+        const int lim = min(qpos, len - 1) - j * FA_BN;
+#pragma unroll
+        for (int c = 0; c < 128; ++c)
+          if (c > lim) s[c] = __float_as_uint(-INFINITY);
+      }
+      float mx = -1e30f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
+      mx *= scl;
+      float alpha = 1.f;
+      const bool resc = mx > m_used + kRescaleThresh;
+      if (resc) {
+        alpha = fast_exp2(m_used - mx);
+        m_used = mx;
+        l0 *= alpha;
+        l1 *= alpha;
+      }
+      const float nm = -m_used;
+      // p = exp2(s * scale - m) -> bf16 pairs into the first 64 columns of S_t (P_t)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float a = fast_exp2(fmaf(__uint_as_float(s[64 * c + 2 * i]), scl, nm));
+          const float b = fast_exp2(fmaf(__uint_as_float(s[64 * c + 2 * i + 1]), scl, nm));
+          add2(l0, l1, l0, l1, a, b);
+          pk[i] = pack_bf16x2(a, b);
+        }
+        tmem_st32(t_s + 32 * c, pk);
+      }
+      // O_t is final for blocks < j once PV_t(j-1) is done; rescale it (rare) before PV_t(j)
+      if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
+      tc_fence_after();
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld32(t_o + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(t_o + c * 32, o);
+        }
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[t]);
+    }
+    mbar_wait(&pv_done[t], (nblk - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / (l0 + l1);
+    const bool valid = qpos < len;
+    __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t o[32];
+      tmem_ld32(t_o + c * 32, o);
+      tmem_ld_wait();
+      if (valid) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+          v.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          v.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+          v.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -392,8 +677,9 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(const __nv_bfloat
 }
 
 // q / k heads of the fused QKV rows: per-head RMSNorm (d = 128) then rotate-half RoPE at the
-// token's position in its prompt.  One warp per (token, head); lane holds elements
-// lane, lane+32, lane+64, lane+96 (pairs (i, i+64)).
+// token's position in its prompt.  One warp per token: lane l owns the rotation pairs
+// (e, e + 64) for e = 2l, 2l + 1, computes their cos / sin once, and walks the token's
+// Hq + Hkv heads with 4-byte (bf16x2) loads and stores.
 __global__ void __launch_bounds__(256) qk_rope_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t T, int Hq,
                                                       int Hkv, const int32_t* __restrict__ cu, int B,
                                                       const __nv_bfloat16* __restrict__ w_qn,
@@ -401,12 +687,8 @@ __global__ void __launch_bounds__(256) qk_rope_kernel(const __nv_bfloat16* __res
                                                       float log2_theta, __nv_bfloat16* __restrict__ q_out,
                                                       __nv_bfloat16* __restrict__ k_out) {
   const int lane = threadIdx.x & 31;
-  const int nh = Hq + Hkv;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (gw >= T * nh) return;
-  const int64_t t = gw / nh;
-  const int hh = (int)(gw - t * nh);
-  // position of t in its prompt (binary search over cu)
+  const int64_t t = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
   int lo = 0, hi = B;  // cu[lo] <= t < cu[hi]
   while (hi - lo > 1) {
     const int mid = (lo + hi) >> 1;
@@ -414,31 +696,33 @@ __global__ void __launch_bounds__(256) qk_rope_kernel(const __nv_bfloat16* __res
     else hi = mid;
   }
   const float pos = (float)(t - cu[lo]);
-  const __nv_bfloat16* src = qkv + t * (int64_t)(Hq + 2 * Hkv) * FA_D + (int64_t)hh * FA_D;
-  const __nv_bfloat16* w = hh < Hq ? w_qn : w_kn;
-  float v[4], g[4];
+  float cs[2], sn[2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    v[i] = __bfloat162float(src[lane + 32 * i]);
-    g[i] = __bfloat162float(w[lane + 32 * i]);
+  for (int i = 0; i < 2; ++i) {
+    const int e = 2 * lane + i;
+    sincosf(pos * exp2f(-(2.0f * e / FA_D) * log2_theta), &sn[i], &cs[i]);
   }
-  float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+  const uint32_t* wq = reinterpret_cast<const uint32_t*>(w_qn);
+  const uint32_t* wk = reinterpret_cast<const uint32_t*>(w_kn);
+  const uint32_t gq0 = wq[lane], gq1 = wq[32 + lane], gk0 = wk[lane], gk1 = wk[32 + lane];
+  const uint32_t* row = reinterpret_cast<const uint32_t*>(qkv + t * (int64_t)(Hq + 2 * Hkv) * FA_D);
+  for (int hh = 0; hh < Hq + Hkv; ++hh) {
+    const uint32_t a2 = row[hh * 64 + lane], b2 = row[hh * 64 + 32 + lane];  // (2l, 2l+1), (64+2l, 64+2l+1)
+    float v[4] = {bf16_lo(a2), bf16_hi(a2), bf16_lo(b2), bf16_hi(b2)};
+    float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const float rs = rsqrtf(ss / FA_D + eps);
-  // the normalised head is rounded to bf16 (as a separate norm kernel would store it)
-#pragma unroll
-  for (int i = 0; i < 4; ++i) v[i] = __bfloat162float(__float2bfloat16_rn(v[i] * rs * g[i]));
-  __nv_bfloat16* dst = hh < Hq ? q_out + (t * Hq + hh) * FA_D : k_out + (t * Hkv + (hh - Hq)) * FA_D;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {  // pair (e, e + 64), e = lane + 32 i
-    const int e = lane + 32 * i;
-    const float inv_freq = exp2f(-(2.0f * e / FA_D) * log2_theta);
-    float sn, cs;
-    sincosf(pos * inv_freq, &sn, &cs);
-    const float a = v[i], b = v[i + 2];
-    dst[e] = __float2bfloat16_rn(a * cs - b * sn);
-    dst[e + 64] = __float2bfloat16_rn(b * cs + a * sn);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const float rs = rsqrtf(ss / FA_D + eps);
+    const bool isq = hh < Hq;
+    const uint32_t g0 = isq ? gq0 : gk0, g1 = isq ? gq1 : gk1;
+    // the normalised head is rounded to bf16 (as a separate norm kernel would store it)
+    const uint32_t n0 = pack_bf16x2(v[0] * rs * bf16_lo(g0), v[1] * rs * bf16_hi(g0));
+    const uint32_t n1 = pack_bf16x2(v[2] * rs * bf16_lo(g1), v[3] * rs * bf16_hi(g1));
+    const float x0 = bf16_lo(n0), x1 = bf16_hi(n0), y0 = bf16_lo(n1), y1 = bf16_hi(n1);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(isq ? q_out + (t * Hq + hh) * FA_D
+                                                    : k_out + (t * Hkv + (hh - Hq)) * FA_D);
+    dst[lane] = pack_bf16x2(x0 * cs[0] - y0 * sn[0], x1 * cs[1] - y1 * sn[1]);
+    dst[32 + lane] = pack_bf16x2(y0 * cs[0] + x0 * sn[0], y1 * cs[1] + x1 * sn[1]);
   }
 }
 
@@ -522,8 +806,7 @@ void launch_residual_rmsnorm(const bf16* x, const bf16* a, const bf16* w, int64_
 void launch_qk_rope(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32_t* cu, int B, const bf16* w_qn,
                     const bf16* w_kn, float eps, float theta, bf16* q, bf16* k, cudaStream_t s) {
   if (T <= 0) return;
-  const int64_t warps = T * (Hq + Hkv);
-  qk_rope_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(qkv, T, Hq, Hkv, cu, B, w_qn, w_kn, eps, log2f(theta),
+  qk_rope_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(qkv, T, Hq, Hkv, cu, B, w_qn, w_kn, eps, log2f(theta),
                                                              q, k);
 }
 
@@ -564,7 +847,9 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(flash_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FaSmem::ALLOC);
+    cudaFuncSetAttribute(flash_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
   });
+  static const bool v1 = getenv("ASYNCEP_FA_V1") && atoi(getenv("ASYNCEP_FA_V1")) != 0;
   FaArgs a{};
   a.cu = cu;
   a.vcu = vcu;
@@ -573,9 +858,14 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   a.Hkv = Hkv;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)FA_D));
   a.o = o;
-  const int64_t tiles_upper = (T + FA_BM - 1) / FA_BM + B;  // sum_b ceil(L_b / 128) <= this
-  dim3 grid((unsigned)Hq, (unsigned)tiles_upper);
-  flash_attn_kernel<<<grid, FA_NTHREADS, FaSmem::ALLOC, s>>>(mq, mk, mv, a);
+  if (v1) {
+    const int64_t tiles_upper = (T + FA_BM - 1) / FA_BM + B;  // sum_b ceil(L_b / 128) <= this
+    flash_attn_kernel<<<dim3((unsigned)Hq, (unsigned)tiles_upper), FA_NTHREADS, FaSmem::ALLOC, s>>>(mq, mk, mv, a);
+  } else {
+    const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
+    flash_attn2_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv,
+                                                                                                      a);
+  }
   return true;
 }
 
