@@ -330,6 +330,24 @@ __global__ void __launch_bounds__(FA_NTHREADS, 1)
   }
 }
 
+// 2^x on the FMA / ALU pipes (FA-style SFU offload): x = n + f with n = rint(x) by the 1.5 * 2^23
+// magic add, 2^f on [-1/2, 1/2] by a cubic (rel. err 7.7e-5, far below the bf16 rounding of P),
+// and 2^n added to the exponent bits.  x is clamped at -125 (masked -inf -> 2^-125 ~ 0; the
+// exponent field then stays >= 1).
+__device__ __forceinline__ float poly_exp2(float x) {
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.05508877f, f, 0.24260466f);
+  p = fmaf(p, f, 0.69327628f);
+  p = fmaf(p, f, 0.9999289f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+#ifndef FA_POLY_EVERY
+#define FA_POLY_EVERY 4  // one exp2 in FA_POLY_EVERY pairs on the FMA pipe (0: all on the SFU)
+#endif
+
 // ------------------------------------------------------------------ flash attention, two query tiles
 // v2: one CTA per (query head, pair of 128-query tiles of a prompt) = 256 queries sharing every
 // K / V^T block (half the operand traffic per FLOP of v1).  320 threads:
@@ -544,8 +562,11 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
         uint32_t pk[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          const float a = fast_exp2(fmaf(__uint_as_float(s[64 * c + 2 * i]), scl, nm));
-          const float b = fast_exp2(fmaf(__uint_as_float(s[64 * c + 2 * i + 1]), scl, nm));
+          const float xa = fmaf(__uint_as_float(s[64 * c + 2 * i]), scl, nm);
+          const float xb = fmaf(__uint_as_float(s[64 * c + 2 * i + 1]), scl, nm);
+          const bool poly = FA_POLY_EVERY > 0 && (i % (FA_POLY_EVERY > 0 ? FA_POLY_EVERY : 1)) == 0;
+          const float a = poly ? poly_exp2(xa) : fast_exp2(xa);
+          const float b = poly ? poly_exp2(xb) : fast_exp2(xb);
           add2(l0, l1, l0, l1, a, b);
           pk[i] = pack_bf16x2(a, b);
         }
