@@ -41,7 +41,6 @@ int env_int(const char* name, int dflt) {
 }
 constexpr int BM = kTileM;          // 128 rows per CTA (per-CTA UMMA M slice)
 constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
-constexpr int NTHREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int SCL_BYTES = 256 * 4;             // per epilogue warp: the tile's 256 FP8 weight scales
@@ -49,15 +48,29 @@ constexpr int TMEM_COLS = 512;
 constexpr int RING = 4;
   // tile ids in flight between the scheduler and the consumers
 
-template <int NCTA>
+enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
+
+#ifndef PLAIN_NSTG
+#define PLAIN_NSTG 1
+#endif
+#ifndef EPI8
+#define EPI8 0  // 1: 8 epilogue warps on CTA-pair GEMMs (two per TMEM lane quadrant, split columns)
+#endif
+// Shared memory plan per (CTA group, epilogue mode).  With PLAIN_NSTG = 2 the plain epilogue
+// (GEMM2: four 64-column stores per tile) double-buffers its staging; its FP8 scales are then
+// read as warp-broadcast vector loads instead of an smem copy (the space goes to staging).
+template <int NCTA, int MODE>
 struct Cfg {
   static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
   static constexpr int STAGES = NCTA == 2 ? 6 : 4;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + 4 * STG_BYTES +
-                                 4 * SCL_BYTES + 512 + (kMaxExperts + 1) * sizeof(int32_t);
+  static constexpr int EW = (EPI8 && NCTA == 2 && (MODE == EPI_PLAIN || MODE == EPI_SWIGLU)) ? 8 : 4;
+  static constexpr int NTHR = 128 + 32 * EW;  // warps 0-3 roles, then EW epilogue warps
+  static constexpr int NSTG = (MODE == EPI_PLAIN && NCTA == 2 && EW == 4) ? PLAIN_NSTG : 1;
+  static constexpr int NSCL = ((MODE == EPI_PLAIN && NSTG == 2) || EW == 8) ? 0 : SCL_BYTES;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + EW * NSTG * STG_BYTES +
+                                 EW * NSCL + 512 + (kMaxExperts + 1) * sizeof(int32_t);
+  static_assert(SMEM <= 232448, "shared memory budget");
 };
-
-enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
 
 struct TcArgs {
   const int32_t* tile_start;  // grouped mode: [E+1] prefix of row tiles (rows padded to 128*NCTA)
@@ -178,9 +191,14 @@ __device__ __forceinline__ void router_epilogue(uint32_t tb, int E, int k, int n
 // Epilogue store of 64 bf16 columns (32 packed words) of this thread's row through the
 // warp's 32 x 128 B staging buffer (128-B swizzle: 16-B chunk j of row r at chunk
 // j ^ (r & 7), conflict-free) and one TMA bulk tensor store of the {64 x 32} box.
+// With NSTG = 2 buffers (chunk parity picks one) only the store before last must have been read.
+template <int NSTG>
 __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t* stg, int lane,
                                                 const CUtensorMap* map_out, int col0, int row0) {
-  if (lane == 0) bulk_wait_read0();  // previous store has finished reading the buffer
+  if (lane == 0) {  // the store that last used this buffer has finished reading it
+    if (NSTG == 2) bulk_wait_read1();
+    else bulk_wait_read0();
+  }
   __syncwarp();
   const uint32_t base = smem_u32(stg) + lane * 128;
 #pragma unroll
@@ -245,18 +263,18 @@ __device__ __forceinline__ const float* stage_scales(float* dst, const float* sr
 }
 
 template <int MODE, int NCTA, bool F8>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
-  using C = Cfg<NCTA>;
+  using C = Cfg<NCTA, MODE>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
   uint8_t* sStg = sB + STAGES * C::B_BYTES_MAX;
-  float* sScl = reinterpret_cast<float*>(sStg + 4 * STG_BYTES);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + 4 * STG_BYTES + 4 * SCL_BYTES);
+  float* sScl = reinterpret_cast<float*>(sStg + C::EW * C::NSTG * STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EW * C::NSTG * STG_BYTES + C::EW * C::NSCL);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -280,7 +298,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       s_ts[1] = (p.dense_rows + TM - 1) / TM;
     }
   } else {
-    for (int i = threadIdx.x; i <= p.E; i += NTHREADS) s_ts[i] = p.tile_start[i] * p.ts_scale;
+    for (int i = threadIdx.x; i <= p.E; i += C::NTHR) s_ts[i] = p.tile_start[i] * p.ts_scale;
   }
   const bool gather = p.gather_rows != nullptr;
   if (warp == 0 && lane == 0) {
@@ -295,13 +313,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * NCTA);  // one arrive per epilogue warp of each CTA
+      mbar_init(&tempty[a], C::EW * NCTA);  // one arrive per epilogue warp of each CTA
     }
     for (int r = 0; r < RING; ++r) {
       mbar_init(&sfull[r], 1);
       // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue
       // warps}; fused dispatch adds the 2 gather warps of each CTA and the peer's forwarder
-      mbar_init(&sempty[r], 5 * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0));
+      mbar_init(&sempty[r], (1 + C::EW) * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0));
     }
     fence_barrier_init();
   }
@@ -463,8 +481,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     __syncwarp();
   } else if (warp >= 4) {
-    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew+32)
-    uint8_t* stg = sStg + ew * STG_BYTES;
+    const int ew = warp - 4;           // epilogue warp index (staging / scale buffers)
+    const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad+32): this warp's rows
+    const int ch = ew >> 2;            // EW == 8: column half of the tile this warp stores
+    uint8_t* stg = sStg + ew * C::NSTG * STG_BYTES;
+    uint32_t chunk = 0;  // stores issued by this warp (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int seq = 0;; ++seq) {
@@ -474,10 +495,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (t >= total) break;
       int mt, nt;
       decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
-      const int wrow0 = mt * TM + (int)rank * BM + ew * 32;  // first row of this warp's slice
+      const int wrow0 = mt * TM + (int)rank * BM + quad * 32;  // first row of this warp's slice
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tb = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(acc * 256);
+      const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
       if (MODE == EPI_ROUTER || MODE == EPI_ROUTER16) {
         const int row = wrow0 + lane;
         router_epilogue<MODE == EPI_ROUTER ? 8 : 16>(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows,
@@ -490,12 +511,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sa = p.a_scale[gather ? __ldg(p.gather_rows + wrow0 + lane) : wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = stage_scales(sScl + ew * 256,
-                            reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256, 256,
-                            lane);
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256;
+          if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, 256, lane);
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 64) {
+        for (int c0 = C::EW == 8 ? 64 * ch : 0; c0 < (C::EW == 8 ? 64 * ch + 64 : 128); c0 += 64) {
           uint32_t o[32];
           uint32_t amax2 = 0;  // |bf16| bit patterns of both halves: unsigned order = magnitude order
 #pragma unroll
@@ -513,8 +533,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 uv[j] = __uint_as_float(u[4 * q + j]);
               }
               if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
-                const uint32_t sc = smem_u32(sb) + 4 * (c0 + 32 * half + 4 * q);
-                const float4 sg = ld_shared_f4(sc), su = ld_shared_f4(sc + 512);
+                const int cc = c0 + 32 * half + 4 * q;
+                float4 sg, su;
+                if (C::NSCL > 0) {
+                  sg = ld_shared_f4(smem_u32(sb) + 4 * cc);
+                  su = ld_shared_f4(smem_u32(sb) + 4 * cc + 512);
+                } else {
+                  sg = __ldg(reinterpret_cast<const float4*>(sb + cc));
+                  su = __ldg(reinterpret_cast<const float4*>(sb + 128 + cc));
+                }
                 float s0, s1, s2, s3, t0, t1, t2, t3;
                 mul2(s0, s1, sa, sa, sg.x, sg.y);
                 mul2(s2, s3, sa, sa, sg.z, sg.w);
@@ -535,7 +562,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-          stage_and_store(o, stg, lane, &map_out, nt * 128 + c0, wrow0);
+          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * 128 + c0, wrow0);
           if (F8) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
         }
         if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
@@ -546,12 +573,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           sa = p.a_scale[wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = stage_scales(sScl + ew * 256,
-                            reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN,
-                            p.BN, lane);
+          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN;
+          if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < p.BN; c0 += 64) {
+        for (int c0 = C::EW == 8 ? 128 * ch : 0; c0 < (C::EW == 8 ? min(128 * ch + 128, p.BN) : p.BN); c0 += 64) {
           if (nt * p.BN + c0 >= p.n_out) break;
           uint32_t o[32];
 #pragma unroll
@@ -565,7 +591,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
               for (int j = 0; j < 4; ++j) v[j] = __uint_as_float(r[4 * q + j]);
               if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
-                const float4 sv = ld_shared_f4(smem_u32(sb) + 4 * (c0 + 32 * half + 4 * q));
+                const int cc = c0 + 32 * half + 4 * q;
+                const float4 sv = C::NSCL > 0 ? ld_shared_f4(smem_u32(sb) + 4 * cc)
+                                              : __ldg(reinterpret_cast<const float4*>(sb + cc));
                 float s0, s1, s2, s3;
                 mul2(s0, s1, sa, sa, sv.x, sv.y);
                 mul2(s2, s3, sa, sa, sv.z, sv.w);
@@ -576,7 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               o[16 * half + 2 * q + 1] = pack_bf16x2(v[2], v[3]);
             }
           }
-          stage_and_store(o, stg, lane, &map_out, nt * p.BN + c0, wrow0);
+          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * p.BN + c0, wrow0);
         }
       }
       tc_fence_before();
@@ -606,12 +634,12 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg<NCTA>::SMEM);
+                         (int)Cfg<NCTA, MODE>::SMEM);
   });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = Cfg<NCTA>::SMEM;
+  cfg.blockDim = dim3(Cfg<NCTA, MODE>::NTHR);
+  cfg.dynamicSmemBytes = Cfg<NCTA, MODE>::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
