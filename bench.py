@@ -200,6 +200,9 @@ def main():
     ap.add_argument("--link-gbs", type=float, default=0.0,
                     help="with --emulate-gather: pace the peer-shard copies at this GB/s (NVLink receive "
                          "bandwidth; B200_PROFILING.md measured peer copy: 770)")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="N>1: the weight gather over NVLink copy engines on CUDA-IPC-mapped peer shards "
+                         "(default; leaves every SM to the persistent GEMMs) or ncclAllGather")
     ap.add_argument("--ep", action="store_true",
                     help="contrast baseline: the same stack as synchronous DP x EP (two on-path AllToAlls "
                          "per layer, PAPER.md:196-199) instead of AsyncEP")
@@ -241,6 +244,8 @@ def main():
     seed = 0
     flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0) | (A.FLAG_XPERM if args.xperm else 0)
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
+    if world > 1 and args.gather == "nccl":  # NCCL's SM-based AllGather needs SMs the GEMMs leave free
+        os.environ.setdefault("ASYNCEP_RESERVE_SMS", "16")
     emu = args.emulate_gather if world == 1 else 0
     stack = MoEStack(L, E_, K_, H_, h_, T,
                      lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf),
@@ -248,6 +253,13 @@ def main():
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8, offload_window=args.offload)
     local_shards = stack.peer_shards() if emu > 1 else None
+    gather_mode = "emulated" if emu > 1 else ("none" if world == 1 else args.gather)
+    if world > 1 and args.gather == "p2p" and not args.ep:
+        try:
+            stack.enable_p2p_gather()
+        except Exception as e:  # fall back to NCCL (recorded in the JSON line)
+            gather_mode = f"nccl (p2p setup failed: {type(e).__name__}: {str(e)[:120]})"
+            A.asyncep_set_peer_shards(stack.ctx, None)
     cu = None
     attn_flops_layer = 0.0
     if args.attn:
@@ -410,6 +422,7 @@ def main():
                                    if emu > 1 else "dp1 (all experts resident)") +
                                   (f", shards offloaded to pinned host memory, {args.offload}-deep device window "
                                    "(NEXT-2)" if args.offload else ""),
+                   "gather": gather_mode,
                    "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,

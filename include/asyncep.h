@@ -168,6 +168,18 @@ ASYNCEP_API asyncep_status asyncep_enable_offload(asyncep_ctx* ctx, const void* 
 ASYNCEP_API asyncep_status asyncep_stage_layer(asyncep_ctx* ctx, int32_t layer);
 
 /*
+ * Copy-engine gather (the alternative to NCCL for step 5): `shards` [num_layers * world_size]
+ * holds, for every layer l and rank r, a device pointer (in this process's address space:
+ * CUDA-IPC-mapped for r != rank) to rank r's shard of layer l (entries of resident layers are
+ * ignored).  From then on asyncep_prefetch_layer fills the slot with cudaMemcpyAsync copies over
+ * NVLink on the comm stream -- copy engines, no SMs, so the gather overlaps the persistent GEMMs
+ * that occupy every SM (an SM-based NCCL AllGather can only run in their gaps, or on SMs left free
+ * with ASYNCEP_RESERVE_SMS).  Same slot layout, events and ordering rules as the NCCL path.
+ * NULL reverts to NCCL.  The pointed-to shards must stay mapped while the context is used.
+ */
+ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void* const* shards);
+
+/*
  * Test / measurement hook for asyncep_prefetch_layer_local: pace the copies of the OTHER
  * ranks' shards at `bytes_per_s` (0 = unpaced) to emulate the NVLink receive bandwidth of
  * an N-rank AllGather on one GPU.  Each 64 MiB chunk is preceded on the comm stream by a

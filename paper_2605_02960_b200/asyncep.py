@@ -93,6 +93,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
+            "asyncep_set_peer_shards": ([P, P], I32),
             "asyncep_enable_offload": ([P, P, P, I32, P], I32),
             "asyncep_stage_layer": ([P, I32], I32),
             "asyncep_cost_delta": ([P, I64, I64, I64], D),
@@ -245,6 +246,19 @@ def asyncep_enable_offload(ctx: Context, host_shards, window, w: int, h2d_stream
 
 def asyncep_stage_layer(ctx: Context, layer: int) -> None:
     _check(lib().asyncep_stage_layer(ctx.handle, layer))
+
+
+def asyncep_set_peer_shards(ctx: Context, shards) -> None:
+    """shards: [layer][rank] tensors (peer ones CUDA-IPC-mapped) or None to revert to NCCL."""
+    if shards is None:
+        _check(lib().asyncep_set_peer_shards(ctx.handle, None))
+        return
+    L, N = ctx.cfg.num_layers, ctx.cfg.world_size
+    flat = [(_p(shards[l][r]) if shards[l] is not None and shards[l][r] is not None else None)
+            for l in range(L) for r in range(N)]
+    arr = (ctypes.c_void_p * (L * N))(*flat)
+    _check(lib().asyncep_set_peer_shards(ctx.handle, arr))
+    ctx.keep.append(shards)
 
 
 def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:

@@ -187,6 +187,7 @@ struct asyncep_ctx {
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   int64_t launches = 0;
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
+  std::vector<const void*> peer;  // P2P gather: [layer * N + rank] peer-mapped shard pointers (empty: NCCL)
   std::vector<aep::GemmMaps> ep_maps;  // EP contrast: maps over this rank's shard of each layer
   std::vector<char> ep_maps_ok;
   // NEXT-2 offload: host backing store + w-deep device window
@@ -304,6 +305,11 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   c->cs = (cudaStream_t)compute_stream;
   c->ms = (cudaStream_t)comm_stream;
   c->num_sms = prop.multiProcessorCount;
+  if (cfg->world_size > 1) {  // leave SMs to NCCL's AllGather kernels (persistent GEMMs fill every SM)
+    const char* rs = getenv("ASYNCEP_RESERVE_SMS");
+    const int reserve = rs && *rs ? atoi(rs) : 0;
+    if (reserve > 0 && reserve < c->num_sms - 2) c->num_sms -= reserve & ~1;
+  }
   c->router_w.assign(router_w, router_w + L);
   c->shard.assign(expert_shard, expert_shard + L);
   c->ws = (uint8_t*)workspace;
@@ -384,9 +390,14 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     CUDA_TRY(cudaStreamWaitEvent(c->ms, c->h2d_done[wi], 0));
     own = c->window[wi];
   }
+  if (!shards && !c->peer.empty()) shards = c->peer.data() + (size_t)layer * c->cfg.world_size;  // P2P gather
   if (shards) {
+    // copy-engine gather: the N - 1 peer shards (then the own one), each rank starting at its
+    // right-hand neighbour so that the N readers of a shard are spread over time
     constexpr size_t kChunk = (size_t)64 << 20;
-    for (int r = 0; r < c->cfg.world_size; ++r) {
+    const int N = c->cfg.world_size;
+    for (int i = 1; i <= N; ++i) {
+      const int r = (c->cfg.rank + i) % N;
       if (!shards[r]) return fail(ASYNCEP_ERR_INVALID_ARG, "null shard %d", r);
       uint8_t* dst = (uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes;
       const uint8_t* src = (const uint8_t*)(r == c->cfg.rank && c->offload ? own : shards[r]);
@@ -477,6 +488,22 @@ asyncep_status asyncep_prefetch_layer_local(asyncep_ctx* c, int32_t layer, const
   if (c->cfg.world_size < 2) return fail(ASYNCEP_ERR_INVALID_ARG, "prefetch_layer_local needs world_size > 1");
   if (!shards) return fail(ASYNCEP_ERR_INVALID_ARG, "shards is NULL");
   return prefetch_common(c, layer, shards);
+}
+
+asyncep_status asyncep_set_peer_shards(asyncep_ctx* c, const void* const* shards) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  const int L = c->cfg.num_layers, N = c->cfg.world_size;
+  if (!shards) {
+    c->peer.clear();
+    return ASYNCEP_OK;
+  }
+  if (N < 2) return fail(ASYNCEP_ERR_INVALID_ARG, "peer shards need world_size > 1");
+  for (int l = 0; l < L; ++l)
+    for (int r = 0; r < N; ++r)
+      if (!layer_resident(c, l) && (!shards[(size_t)l * N + r] || ((uintptr_t)shards[(size_t)l * N + r] & 15)))
+        return fail(ASYNCEP_ERR_INVALID_ARG, "peer shard (layer %d, rank %d) is null or misaligned", l, r);
+  c->peer.assign(shards, shards + (size_t)L * N);
+  return ASYNCEP_OK;
 }
 
 asyncep_status asyncep_set_link_emulation(asyncep_ctx* c, double bytes_per_s) {

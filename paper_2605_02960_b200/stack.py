@@ -123,6 +123,38 @@ class MoEStack:
                         for r in range(self.N)]
         return lambda l: table[l]
 
+    def enable_p2p_gather(self, pg=None) -> None:
+        """Copy-engine gather across real ranks (asyncep_set_peer_shards): every rank shares its
+        shard buffers through CUDA IPC (torch's tensor IPC, exchanged with all_gather_object) and
+        maps the peers'; asyncep_prefetch_layer then copies them over NVLink with copy engines,
+        leaving every SM to the persistent GEMMs.  Collective over the process group."""
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+        mine = [None if self.layer_resident(l) else reduce_tensor(self.shards[l]) for l in range(self.L)]
+        allh = [None] * self.N
+        dist.all_gather_object(allh, mine, group=pg)
+        table = [None] * self.L
+        for l in range(self.L):
+            if self.layer_resident(l):
+                continue
+            row = []
+            for r in range(self.N):
+                if r == self.rank:
+                    row.append(self.shards[l])
+                else:
+                    fn, args = allh[r][l]
+                    row.append(fn(*args))  # peer memory mapped into this process
+            table[l] = row
+        self._peer_table = table
+        A.asyncep_set_peer_shards(self.ctx, table)
+        dist.barrier(group=pg)
+
+    def set_peer_table(self, table) -> None:
+        """Install a [layer][rank] shard table for the copy-engine gather (1-GPU emulation in
+        tests: local tensors stand in for the IPC-mapped peers)."""
+        self._peer_table = table
+        A.asyncep_set_peer_shards(self.ctx, table)
+
     def layer_resident(self, l: int) -> bool:
         return layer_resident(l, self.N, bool(self.cfg.replicate_layer0))
 

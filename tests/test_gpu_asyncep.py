@@ -9,6 +9,7 @@ import pytest
 import torch
 
 from gpu_helpers import Workload
+from paper_2605_02960_b200 import asyncep as A
 
 pytestmark = pytest.mark.gpu
 
@@ -217,3 +218,23 @@ def test_offload_window_bitwise_equals_resident(N, w):
         out = st.run(x, local_shards=sh).clone()
         torch.cuda.synchronize()
         assert torch.equal(_bits(out), _bits(ref))
+
+
+@pytest.mark.parametrize("N", [2, 4])
+def test_copy_engine_gather_bitwise_equals_resident(N):
+    """asyncep_set_peer_shards (the copy-engine gather used across real ranks with IPC-mapped
+    peer shards) through the plain asyncep_prefetch_layer: bitwise = resident, two passes."""
+    wl = Workload(L=4, E=16, k=4, H=256, h=256, seed=31)
+    T = 1200
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    st = wl.stack(max_tokens=T, world_size=N, rank=N - 1)
+    sh = st.peer_shards()
+    st.set_peer_table([None if st.layer_resident(l) else sh(l) for l in range(wl.L)])
+    for _ in range(2):
+        out = st.run(x).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(_bits(out), _bits(ref))
+    with pytest.raises(A.AsyncEPError):  # a gathered layer without a peer entry is rejected
+        bad = [None] * wl.L
+        A.asyncep_set_peer_shards(st.ctx, bad)
