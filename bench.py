@@ -39,6 +39,7 @@ L_, E_, K_, H_, h_ = 8, 128, 8, 4096, 1536
 T_LOC = 32768
 FLOPS_TOK_LAYER = 2 * H_ * E_ + 6 * K_ * H_ * h_          # 303,038,464 (router + experts)
 ATT_HQ, ATT_HKV = 64, 4                                    # Qwen3-235B-A22B attention (NEXT-3, R19)
+COMBINE_BYTES_TOK = K_ * H_ * 2 + 2 * H_ * 2               # read k rows + residual, write y
 GEMM1_FLOPS_TOK = 4 * K_ * H_ * h_                        # gate/up: 2 * k * H * 2h
 GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
 SPEC_BF16 = 2.25e15
@@ -430,6 +431,13 @@ def main():
                 "vs_measured_sustained": mfu_flops / (peak_tf * 1e12),
                 "flops_per_token_layer": FLOPS_TOK_LAYER},
         "stage_ms_per_layer": per_layer_ms,
+        "hbm": {  # achieved HBM bandwidth of the memory-bound steps (algorithmic bytes / stage time)
+            "combine_gbs": (T * COMBINE_BYTES_TOK / (per_layer_ms["combine"] / 1e3) / 1e9
+                            if per_layer_ms.get("combine") else None),
+            "combine_bytes_per_token": COMBINE_BYTES_TOK,
+            "peak_gbs": peaks.get("hbm_gbs"),
+            "note": "combine reads k bf16 expert rows + the residual and writes y (81,920 B/token); the dispatch "
+                    "writes only the row maps (the row copy is fused into GEMM1's A load)"},
         "attention": attn_info,
         "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
                          "flops_per_s": f_gemm, "ag_bytes_per_s": bw,
