@@ -10,20 +10,9 @@
 // residual_rmsnorm (x + attn -> x', RMSNorm(x')).  The two projections run on the tcgen05
 // GEMM (gemm_tc.cu, dense mode).
 //
-// flash_attn: one CTA per (query head, 128-query tile of one prompt); 256 threads:
-//   warp 0   TMA producer: Q tile once, then per 128-key block K_j and V^T_j into a 2-stage
-//            ring (K and V released separately: K after S_j, V after PV_j)
-//   warp 1   MMA issuer: S_j = Q K_j^T (M=128, N=128, K=d) into a double-buffered TMEM S,
-//            one block ahead of PV_j = P_j V_j (A = P from smem, B = V^T_j) accumulated in a
-//            TMEM O (accumulate flag off for j = 0)
-//   warp 2   TMEM allocator (512 columns: S0, S1, O)
-//   warps 4-7 softmax, thread = query row: S row from TMEM (4 x 32 columns), causal /
-//            prompt-end mask on the diagonal block, row max, p = exp2(s * scale - m) (one FFMA
-//            + ex2), P as bf16 into the 128-B-swizzled smem tile the MMA reads.  The row sums
-//            come from the tensor core: V^T carries 16 rows of ones, so PV (N = 144) writes
-//            sum_j p_j next to O.  The running max is only moved (and O rescaled in TMEM) when it grows
-//            by more than 8 (log2 units): the final O / l uses the same stale max in both, so
-//            the result is exact, and O is rarely touched.
+// flash_attn2 (default) and flash_attn3 (64-key variant) are described above each kernel.
+// (A first single-tile version -- P through smem, row sums from a ones block appended to V^T --
+// reached 620-850 TFLOP/s and was replaced by the two-tile kernel.)
 // The rows of a tile past the end of its prompt are computed but never stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -44,24 +33,7 @@ constexpr int FA_BN = 128;  // keys per block
 constexpr int FA_D = 128;   // head dim
 constexpr int FA_KB = 16 * 1024;       // one [128 rows x 128 B] swizzled k-block
 constexpr int FA_TILE = 2 * FA_KB;     // a 128 x 128 bf16 operand tile (2 k-blocks of 64)
-// V^T k-blocks carry 16 extra rows of ones after the 128 d rows: PV with N = 144 also
-// yields the row sums of P (columns 128..143 of O), so the softmax warps never add up p.
-constexpr int FA_VN = FA_D + 16;
-constexpr int FA_VKB = FA_VN * 128;    // 18 KB
-constexpr int FA_VTILE = 2 * FA_VKB;
-constexpr int FA_NTHREADS = 256;
 constexpr float kRescaleThresh = 8.0f;  // log2 units
-
-struct FaSmem {
-  // operand tiles (each 1024-B aligned, [k-block][128 rows][128 B])
-  static constexpr int Q = 0;
-  static constexpr int K0 = Q + FA_TILE;
-  static constexpr int V0 = K0 + 2 * FA_TILE;
-  static constexpr int P = V0 + 2 * FA_VTILE;
-  static constexpr int BAR = P + FA_TILE;
-  static constexpr int BYTES = BAR + 256;
-  static constexpr int ALLOC = BYTES + 1024;  // alignment slack
-};
 
 struct FaArgs {
   const int32_t* cu;   // [B+1] prompt offsets (tokens)
@@ -72,263 +44,6 @@ struct FaArgs {
   float scale_log2;  // softmax scale * log2(e)
   __nv_bfloat16* o;  // [T, Hq, d]
 };
-
-// (prompt, q tile) of linear tile u: prompts in order, each prompt's tiles heaviest first
-__device__ bool fa_tile(const int32_t* cu, int B, int u, int& b, int& tile, int& start, int& len) {
-  // linear scan over the prompts (one thread per CTA)
-  int acc = 0;
-  for (int i = 0; i < B; ++i) {
-    const int s = cu[i], L = cu[i + 1] - s;
-    const int nt = (L + FA_BM - 1) / FA_BM;
-    if (u < acc + nt) {
-      b = i;
-      start = s;
-      len = L;
-      tile = nt - 1 - (u - acc);
-      return true;
-    }
-    acc += nt;
-  }
-  return false;
-}
-
-__global__ void __launch_bounds__(FA_NTHREADS, 1)
-    flash_attn_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                      const __grid_constant__ CUtensorMap map_vt, const FaArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FaSmem::BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;   // [2]
-  uint64_t* k_empty = bars + 3;  // [2]
-  uint64_t* v_full = bars + 5;   // [2]
-  uint64_t* v_empty = bars + 7;  // [2]
-  uint64_t* s_full = bars + 9;   // [2]
-  uint64_t* s_empty = bars + 11; // [2]
-  uint64_t* p_full = bars + 13;
-  uint64_t* pv_done = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  __shared__ int s_tile[4];
-
-  const int warp = warp_id(), lane = lane_id();
-  const int head = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int b = 0, tile = 0, start = 0, len = 0;
-    const bool ok = fa_tile(p.cu, p.B, blockIdx.y, b, tile, start, len);
-    s_tile[0] = ok ? tile : -1;
-    s_tile[1] = start;
-    s_tile[2] = len;
-    s_tile[3] = ok ? p.vcu[b] : 0;
-  }
-  __syncthreads();
-  const int tile = s_tile[0];
-  if (tile < 0) return;  // past the last tile of the batch (grid is an upper bound)
-  const int start = s_tile[1], len = s_tile[2], vstart = s_tile[3];
-  const int q0 = tile * FA_BM;        // first query position in the prompt
-  const int nblk = tile + 1;          // causal: key blocks 0..tile
-  const int kvh = head / (p.Hq / p.Hkv);
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);
-    }
-    mbar_init(p_full, 4);
-    mbar_init(pv_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  for (int i = threadIdx.x; i < 4 * 16 * 128 / 16; i += FA_NTHREADS) {  // 4 k-blocks x 2 KB of bf16 1.0
-    const int kb = i / 128, off = (i % 128) * 16;
-    const uint32_t one2 = 0x3F803F80u;
-    st_shared_v4(smem_u32(smem + FaSmem::V0 + kb * FA_VKB + FA_KB + off), one2, one2, one2, one2);
-  }
-  fence_proxy_async_smem();
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s[2] = {tmem, tmem + 128};
-  const uint32_t t_o = tmem + 256;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      tma_prefetch_desc(&map_q);
-      tma_prefetch_desc(&map_k);
-      tma_prefetch_desc(&map_vt);
-      mbar_arrive_expect_tx(q_full, FA_TILE);
-      for (int c = 0; c < 2; ++c)
-        tma_load_3d_nohint(smem + FaSmem::Q + c * FA_KB, &map_q, q_full, c * 64, head, start + q0);
-      for (int j = 0; j < nblk; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = ((j >> 1) & 1) ^ 1;
-        const int key0 = start + j * FA_BN;
-        mbar_wait(&k_empty[st], ph);
-        mbar_arrive_expect_tx(&k_full[st], FA_TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + FaSmem::K0 + st * FA_TILE + c * FA_KB, &map_k, &k_full[st], c * 64, kvh, key0);
-        mbar_wait(&v_empty[st], ph);
-        mbar_arrive_expect_tx(&v_full[st], FA_TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + FaSmem::V0 + st * FA_VTILE + c * FA_VKB, &map_vt, &v_full[st],
-                             vstart + j * FA_BN + c * 64, 0, kvh);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);     // S: M = 128, N = 128 keys
-    constexpr uint32_t idesc_pv = make_idesc(FA_BM, FA_VN, true);  // PV: N = 128 d + 16 sum columns
-    const uint64_t dq = make_smem_desc_sw128(smem_u32(smem + FaSmem::Q));
-    const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + FaSmem::K0));
-    const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + FaSmem::V0));
-    const uint64_t dp = make_smem_desc_sw128(smem_u32(smem + FaSmem::P));
-    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4, kVkb = FA_VKB >> 4, kVtile = FA_VTILE >> 4;
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int j) {  // S_j = Q K_j^T into S[j & 1]
-      const int st = j & 1;
-      mbar_wait(&k_full[st], (j >> 1) & 1);
-      mbar_wait(&s_empty[st], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // d = 128 = 2 k-blocks x 4 steps of 16
-          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
-          mma_bf16(t_s[st], dq + off, dk + st * kTile + off, idesc, k > 0 ? 1u : 0u);
-        }
-        tc_commit(&s_full[st]);
-        tc_commit(&k_empty[st]);
-      }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int j = 0; j < nblk; ++j) {
-      if (j + 1 < nblk) issue_s(j + 1);
-      const int st = j & 1;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // keys = 128 = 2 k-blocks x 4 steps of 16
-          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
-          const uint64_t voff = (uint64_t)(k >> 2) * kVkb + (uint64_t)(k & 3) * 2;
-          mma_bf16(t_o, dp + off, dv + st * kVtile + voff, idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-        }
-        tc_commit(pv_done);
-        tc_commit(&v_empty[st]);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    const int ew = warp - 4;
-    const int r = ew * 32 + lane;           // query row in the tile
-    const int qpos = q0 + r;                // position in the prompt
-    const uint32_t lane_off = (uint32_t)(ew * 32) << 16;
-    float m_used = -1e30f;  // running max in scaled log2 units (moved only by > 8)
-    const float scl = p.scale_log2;
-    const uint32_t p_base = smem_u32(smem + FaSmem::P) + (uint32_t)r * 128;
-    for (int j = 0; j < nblk; ++j) {
-      const int st = j & 1;
-      mbar_wait(&s_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(t_s[st] + lane_off + c * 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * c));
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[st]);
-      // causal / prompt-end mask (diagonal block only), raw row max
-      if (j == nblk - 1) {
-        const int lim = min(qpos, len - 1) - j * FA_BN;  // keys c <= lim are visible
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > lim) s[c] = __float_as_uint(-INFINITY);
-      }
-      float mx = -1e30f;
-#pragma unroll
-      for (int c = 0; c < 128; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
-      mx *= scl;
-      float alpha = 1.f;
-      const bool resc = mx > m_used + kRescaleThresh;
-      if (resc) {
-        alpha = fast_exp2(m_used - mx);
-        m_used = mx;
-      }
-      // p = exp2(s * scale - m): one FFMA + ex2 per element, bf16 pack (64 words)
-      uint32_t pk[64];
-      const float nm = -m_used;
-#pragma unroll
-      for (int c = 0; c < 64; ++c)
-        pk[c] = pack_bf16x2(fast_exp2(fmaf(__uint_as_float(s[2 * c]), scl, nm)),
-                            fast_exp2(fmaf(__uint_as_float(s[2 * c + 1]), scl, nm)));
-      // PV_{j-1} done: the P buffer is free and O (with its sum columns) is final for blocks < j
-      if (j > 0) mbar_wait(pv_done, (j - 1) & 1);
-      tc_fence_after();
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {  // rare: rescale this warp's O rows (+ sums)
-#pragma unroll 1
-        for (int c = 0; c < 5; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + lane_off + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + lane_off + c * 32, o);
-        }
-        tmem_st_wait();
-      }
-      // P row -> smem: 2 k-blocks of 64 keys, 16-B chunk q of row r at (q ^ (r & 7))
-#pragma unroll
-      for (int kb = 0; kb < 2; ++kb)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int w0 = kb * 32 + q * 4;
-          st_shared_v4(p_base + kb * FA_KB + ((q ^ (r & 7)) << 4), pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
-        }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
-    }
-    // epilogue: O / l -> bf16 -> o[start + qpos, head, :]; l = O column 128 (P . ones)
-    mbar_wait(pv_done, (nblk - 1) & 1);
-    tc_fence_after();
-    uint32_t lsum[8];
-    tmem_ld8(t_o + lane_off + FA_D, lsum);
-    tmem_ld_wait();
-    const float inv = 1.f / __uint_as_float(lsum[0]);
-    const bool valid = qpos < len;
-    __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + lane_off + c * 32, o);
-      tmem_ld_wait();
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
 
 // 2^x on the FMA / ALU pipes (FA-style SFU offload): x = n + f with n = rint(x) by the 1.5 * 2^23
 // magic add, 2^f on [-1/2, 1/2] by a cubic (rel. err 7.7e-5, far below the bf16 rounding of P),
@@ -1128,13 +843,11 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   }
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(flash_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FaSmem::ALLOC);
     cudaFuncSetAttribute(flash_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
     cudaFuncSetAttribute(flash_attn3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa3Smem::ALLOC);
   });
   // v2 by default (same-box A/B, profiles/r01/ab_attn_v2_v3.log: v3 is 6 % slower on 4K / 32K prompts)
   static const int ver = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 2;
-  const bool v1 = ver == 1;
   FaArgs a{};
   a.cu = cu;
   a.vcu = vcu;
@@ -1143,10 +856,7 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   a.Hkv = Hkv;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)FA_D));
   a.o = o;
-  if (v1) {
-    const int64_t tiles_upper = (T + FA_BM - 1) / FA_BM + B;  // sum_b ceil(L_b / 128) <= this
-    flash_attn_kernel<<<dim3((unsigned)Hq, (unsigned)tiles_upper), FA_NTHREADS, FaSmem::ALLOC, s>>>(mq, mk, mv, a);
-  } else if (ver == 2) {
+  if (ver != 3) {
     const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
     flash_attn2_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv,
                                                                                                       a);

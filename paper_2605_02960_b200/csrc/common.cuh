@@ -238,24 +238,6 @@ AEP_DEV void tma_load_3d_nohint(void* dst, const void* tmap, uint64_t* bar, int 
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
-// TMA gather4: 4 rows (r0..r3) x box-width columns starting at column c0 -> 4 consecutive
-// 128-B smem rows.  The tensor map's box is {width, 1}.
-AEP_DEV void tma_gather4(void* dst, const void* tmap, uint64_t* bar, int c0, int4 rows) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(rows.x), "r"(rows.y), "r"(rows.z),
-      "r"(rows.w)
-      : "memory");
-}
-AEP_DEV void tma_gather4_pair(void* dst, const void* tmap, uint64_t* bar, int c0, int4 rows) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.cta_group::2"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(rows.x), "r"(rows.y),
-      "r"(rows.z), "r"(rows.w)
-      : "memory");
-}
 AEP_DEV void tma_load_2d_pair(void* dst, const void* tmap, uint64_t* bar, int c0, int c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
