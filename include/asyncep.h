@@ -179,6 +179,13 @@ ASYNCEP_API asyncep_status asyncep_stage_layer(asyncep_ctx* ctx, int32_t layer);
  */
 ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void* const* shards);
 
+/* The gather's transport primitive, exposed for measurement: a device-to-device (or NVLink
+ * peer) copy of `bytes` on `stream` by a copy kernel of small CTAs that co-reside with the
+ * persistent GEMM CTAs (the driver's D2D memcpy and NCCL kernels cannot start beside them).
+ * ASYNCEP_GATHER_COPY=ce selects cudaMemcpyBatchAsync with the copy-engine hint, =memcpy
+ * cudaMemcpyAsync. */
+ASYNCEP_API asyncep_status asyncep_gather_copy(void* dst, const void* src, size_t bytes, void* stream);
+
 /*
  * Test / measurement hook for asyncep_prefetch_layer_local: pace the copies of the OTHER
  * ranks' shards at `bytes_per_s` (0 = unpaced) to emulate the NVLink receive bandwidth of

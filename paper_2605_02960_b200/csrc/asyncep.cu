@@ -31,6 +31,45 @@ asyncep_status fail(asyncep_status st, const char* fmt, ...) {
   return st;
 }
 
+// The gather's transport primitive.  Default: aep::launch_gather_copy, a copy kernel whose small
+// CTAs co-reside with the persistent GEMM CTAs (measured: the driver's D2D memcpy -- also with the
+// copy-engine hint -- stalls for the whole duration of a persistent GEMM, profiles/copy_timeline.py).
+// ASYNCEP_GATHER_COPY=ce: cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute;
+// =memcpy: cudaMemcpyAsync.
+cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0) {
+  static const int mode = [] {
+    const char* e = getenv("ASYNCEP_GATHER_COPY");
+    if (e && !strcmp(e, "ce")) return 1;
+    if (e && !strcmp(e, "memcpy")) return 2;
+    return 0;
+  }();
+  static const int ctas = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  if (mode == 0 && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
+    aep::launch_gather_copy(dst, src, n, ctas, st, min_ns);
+    return cudaGetLastError();
+  }
+  if (min_ns) aep::launch_spin_ns(min_ns, st);  // other transports: link time, then the copy
+  if (mode == 1) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    void* dsts[1] = {dst};
+    void* srcs[1] = {const_cast<void*>(src)};
+    size_t sizes[1] = {n};
+    size_t idx[1] = {0};
+    size_t fail_idx = 0;
+    if (cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &attr, idx, 1, &fail_idx, st) == cudaSuccess)
+      return cudaSuccess;
+    cudaGetLastError();  // clear, fall back
+  }
+  return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st);
+}
+
 #define CUDA_TRY(expr)                                                                              \
   do {                                                                                              \
     cudaError_t _e = (expr);                                                                        \
@@ -404,11 +443,8 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       const bool paced = c->link_bps > 0 && r != c->cfg.rank;  // own shard is a local copy
       for (size_t o = 0; o < c->shard_bytes; o += kChunk) {
         const size_t n = std::min(kChunk, c->shard_bytes - o);
-        if (paced) {
-          aep::launch_spin_ns((uint64_t)((double)n / c->link_bps * 1e9), c->ms);
-          c->launches += 1;
-        }
-        CUDA_TRY(cudaMemcpyAsync(dst + o, src + o, n, cudaMemcpyDeviceToDevice, c->ms));
+        CUDA_TRY(gather_copy(dst + o, src + o, n, c->ms, paced ? (uint64_t)((double)n / c->link_bps * 1e9) : 0));
+        c->launches += 1;
       }
     }
   } else {
@@ -503,6 +539,13 @@ asyncep_status asyncep_set_peer_shards(asyncep_ctx* c, const void* const* shards
       if (!layer_resident(c, l) && (!shards[(size_t)l * N + r] || ((uintptr_t)shards[(size_t)l * N + r] & 15)))
         return fail(ASYNCEP_ERR_INVALID_ARG, "peer shard (layer %d, rank %d) is null or misaligned", l, r);
   c->peer.assign(shards, shards + (size_t)L * N);
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_gather_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((!dst || !src) && bytes) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
+  if (!bytes) return ASYNCEP_OK;
+  CUDA_TRY(gather_copy(dst, src, bytes, (cudaStream_t)stream));
   return ASYNCEP_OK;
 }
 

@@ -71,9 +71,46 @@ __global__ void spin_ns_kernel(uint64_t ns) {
     __nanosleep(1000);
   }
 }
+
+// The gather transport on SMs that the persistent GEMMs leave room on: small CTAs (128 threads,
+// no shared memory, few registers) that co-reside with a GEMM CTA on every SM, so the copy
+// progresses DURING the GEMMs instead of waiting for SMs to drain (the driver's D2D memcpy and
+// NCCL's kernels do not fit beside a ~220 KB-smem GEMM CTA).  Streaming 16-B loads / stores
+// (evict-first: the slot is read once, by the next layer); works on NVLink peer pointers too.
+// min_ns > 0 (1-GPU link emulation): block 0 holds the kernel open until min_ns after it started,
+// so a chunk takes max(copy time, link time) -- the copy overlaps the emulated link time.
+__global__ void __launch_bounds__(128) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                          size_t n16, uint64_t min_ns) {
+  uint64_t t0 = 0;
+  if (min_ns && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  const size_t stride = (size_t)gridDim.x * 128;
+  size_t i = (size_t)blockIdx.x * 128 + threadIdx.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
+                d = __ldcs(src + i + 3 * stride);
+    __stcs(dst + i, a);
+    __stcs(dst + i + stride, b);
+    __stcs(dst + i + 2 * stride, c);
+    __stcs(dst + i + 3 * stride, d);
+  }
+  for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
+  if (min_ns && blockIdx.x == 0 && threadIdx.x == 0)
+    for (;;) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 >= min_ns) break;
+      __nanosleep(500);
+    }
+}
 }  // namespace
 
 void launch_spin_ns(uint64_t ns, cudaStream_t s) { spin_ns_kernel<<<1, 1, 0, s>>>(ns); }
+
+void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns) {
+  if (!bytes) return;
+  gather_copy_kernel<<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16,
+                                         min_ns);
+}
 
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
                     int64_t T, int H, int k, cudaStream_t s) {

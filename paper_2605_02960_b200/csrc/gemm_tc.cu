@@ -262,8 +262,12 @@ __device__ __forceinline__ const float* stage_scales(float* dst, const float* sr
   return dst;
 }
 
+// Register cap: every GEMM CTA leaves >= 4K registers free on its SM, so the gather transport's
+// copy CTAs (128 threads x 32 registers) co-reside with it and the next layer's gather makes
+// progress during the GEMM (without the cap the FP8 SwiGLU kernel took 250 registers/thread,
+// the whole register file, and the gather stalled for its entire duration).
 template <int MODE, int NCTA, bool F8>
-__global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1)
+__global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCTA, MODE>::NTHR == 256 ? 224 : 168))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
   using C = Cfg<NCTA, MODE>;
