@@ -45,6 +45,19 @@ GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
 SPEC_BF16 = 2.25e15
 
 
+def set_shape(name: str) -> None:
+    """--shape 30b: BASELINE config 2 (Qwen3-30B-A3B MoE layer, H=2048, h=768, one layer,
+    16K tokens, no sharding) instead of the headline Qwen3-235B stack."""
+    global L_, H_, h_, T_LOC, FLOPS_TOK_LAYER, COMBINE_BYTES_TOK, GEMM1_FLOPS_TOK, GEMM2_FLOPS_TOK, ATT_HQ, ATT_HKV
+    if name == "30b":
+        L_, H_, h_, T_LOC = 1, 2048, 768, 16384
+        ATT_HQ, ATT_HKV = 32, 4
+    FLOPS_TOK_LAYER = 2 * H_ * E_ + 6 * K_ * H_ * h_
+    COMBINE_BYTES_TOK = K_ * H_ * 2 + 2 * H_ * 2
+    GEMM1_FLOPS_TOK = 4 * K_ * H_ * h_
+    GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -184,7 +197,12 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------ GPU arm
 def main():
+    pre = argparse.ArgumentParser(add_help=False)
+    pre.add_argument("--shape", choices=["235b", "30b"], default="235b")
+    set_shape(pre.parse_known_args()[0].shape)
     ap = argparse.ArgumentParser()
+    ap.add_argument("--shape", choices=["235b", "30b"], default="235b",
+                    help="235b: headline Qwen3-235B 8-layer stack (config 3/4); 30b: Qwen3-30B layer (config 2)")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -405,13 +423,14 @@ def main():
                          world_size=n_for_T, max_tokens=T, gamma=1.2)
     t_tok, t_flops = A.asyncep_saturation_T(tcfg, f_gemm, bw) if f_gemm > 0 else (None, None)
     step_layer_ms = ms_step / L
+    model = "qwen3-30b-a3b (config 2)" if args.shape == "30b" else "qwen3-235b-a22b"
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp8_e4m3" if args.fp8 else "bf16", "data": "synthetic",
-        "config": {"workload": (f"qwen3-235b-a22b decoder-layer stack (DP attention Hq=64 Hkv=4 d=128, KV-cache-free, "
+        "config": {"workload": (f"{model} decoder-layer stack (DP attention Hq=64 Hkv=4 d=128, KV-cache-free, "
                                 f"{args.prompt}-token prompts + MoE), " if args.attn else
-                                "qwen3-235b-a22b moe-layer stack, ") + f"{L} layers, E=128 k=8 H=4096 h=1536, "
+                                f"{model} moe-layer stack, ") + f"{L} layers, E=128 k=8 H={H_} h={h_}, "
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,

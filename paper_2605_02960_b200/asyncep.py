@@ -94,6 +94,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
             "asyncep_set_peer_shards": ([P, P], I32),
+            "asyncep_gather_copy": ([P, P, SZ, P], I32),
             "asyncep_enable_offload": ([P, P, P, I32, P], I32),
             "asyncep_stage_layer": ([P, I32], I32),
             "asyncep_cost_delta": ([P, I64, I64, I64], D),
@@ -259,6 +260,10 @@ def asyncep_set_peer_shards(ctx: Context, shards) -> None:
     arr = (ctypes.c_void_p * (L * N))(*flat)
     _check(lib().asyncep_set_peer_shards(ctx.handle, arr))
     ctx.keep.append(shards)
+
+
+def asyncep_gather_copy(dst, src, nbytes: int, stream=None) -> None:
+    _check(lib().asyncep_gather_copy(_p(dst), _p(src), nbytes, _stream(stream or torch.cuda.current_stream())))
 
 
 def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:

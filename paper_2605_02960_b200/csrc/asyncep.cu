@@ -43,11 +43,11 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
     if (e && !strcmp(e, "memcpy")) return 2;
     return 0;
   }();
-  static const int ctas = [] {
-    int dev = 0, n = 148;
+  static const int ctas = [] {  // two 128-thread CTAs per SM: both fit beside any GEMM CTA (<= 224
+    int dev = 0, n = 148;         // registers/thread) and keep more NVLink reads in flight
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
+    return 2 * n;
   }();
   if (mode == 0 && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
     aep::launch_gather_copy(dst, src, n, ctas, st, min_ns);
