@@ -337,6 +337,267 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------ flash attention v4 (persistent v2)
+// v2's CTA (two query tiles, P in TMEM, two softmax warpgroups), made persistent: one CTA per SM
+// walks the (pair, head) work items heaviest-first (item w: head = w % Hq, pair list index
+// w / Hq), and the per-item fixed costs overlap the neighbouring items: the producer loads the
+// next item's Q as soon as the current item's last S has read Q (q_empty), the MMA starts the
+// next item's S while the softmax warps finish the current item, and the next PV waits only
+// for the softmax warps to have read O out of TMEM (o_empty).  All barrier phases run on
+// counters that continue across items.
+__device__ __forceinline__ bool fa4_item(const FaArgs& p, int w, int& head, int& start, int& len, int& vstart,
+                                         int& pair) {
+  head = w % p.Hq;
+  int b = 0;
+  if (!fa2_pair(p.cu, p.B, w / p.Hq, b, pair, start, len)) return false;  // past the last pair
+  vstart = p.vcu[b];
+  return true;
+}
+
+__global__ void __launch_bounds__(FA2_NTHREADS, 1)
+    flash_attn4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p, int n_items) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Fa2Smem::BAR);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;    // [2]
+  uint64_t* k_empty = bars + 4;   // [2]
+  uint64_t* v_full = bars + 6;    // [2]
+  uint64_t* v_empty = bars + 8;   // [2]
+  uint64_t* s_full = bars + 10;   // [tile]
+  uint64_t* p_full = bars + 12;   // [tile]
+  uint64_t* pv_done = bars + 14;  // [tile]
+  uint64_t* o_empty = bars + 16;  // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+
+  const int warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0) {
+      tma_prefetch_desc(&map_q);
+      tma_prefetch_desc(&map_k);
+      tma_prefetch_desc(&map_vt);
+      int g = 0;  // K/V blocks loaded so far (ring position)
+      int it = 0;
+      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+        int head, start, len, vstart, pair;
+        if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+        const int q0 = pair * 2 * FA_BM, nB = 2 * pair + 2, kvh = head / (p.Hq / p.Hkv);
+        mbar_wait(q_empty, (it & 1) ^ 1);  // the previous item's S MMAs are done with Q
+        mbar_arrive_expect_tx(q_full, 2 * FA_TILE);
+        for (int c = 0; c < 2; ++c) {
+          tma_load_3d_nohint(smem + Fa2Smem::QA + c * FA_KB, &map_q, q_full, c * 64, head, start + q0);
+          tma_load_3d_nohint(smem + Fa2Smem::QB + c * FA_KB, &map_q, q_full, c * 64, head, start + q0 + FA_BM);
+        }
+        for (int j = 0; j < nB; ++j, ++g) {
+          const int st = g & 1;
+          const uint32_t ph = ((g >> 1) & 1) ^ 1;
+          mbar_wait(&k_empty[st], ph);
+          mbar_arrive_expect_tx(&k_full[st], FA_TILE);
+          for (int c = 0; c < 2; ++c)
+            tma_load_3d_nohint(smem + Fa2Smem::K0 + st * FA_TILE + c * FA_KB, &map_k, &k_full[st], c * 64, kvh,
+                               start + j * FA_BN);
+          mbar_wait(&v_empty[st], ph);
+          mbar_arrive_expect_tx(&v_full[st], FA_TILE);
+          for (int c = 0; c < 2; ++c)
+            tma_load_3d_nohint(smem + Fa2Smem::V0 + st * FA_TILE + c * FA_KB, &map_vt, &v_full[st],
+                               vstart + j * FA_BN + c * 64, 0, kvh);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);
+    const uint64_t dq[2] = {make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QA)),
+                            make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QB))};
+    const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::K0));
+    const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::V0));
+    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4;
+    int g = 0;                   // K/V ring position
+    int ns[2] = {0, 0}, np[2] = {0, 0};  // S issued / PV issued per tile (barrier phases)
+    int it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      int head, start, len, vstart, pair;
+      if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+      const int nA = 2 * pair + 1, nB = 2 * pair + 2;
+      mbar_wait(q_full, it & 1);
+      auto issue_s = [&](int t, int j, bool last) {
+        const int gg = g + j, st = gg & 1;
+        if (t == 0 || j >= nA) mbar_wait(&k_full[st], (gg >> 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
+            mma_bf16(tmem + 256 * t, dq[t] + off, dk + st * kTile + off, idesc, k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[t]);
+          if (t == 1) tc_commit(&k_empty[st]);
+          if (last) tc_commit(q_empty);  // the item's last read of Q
+        }
+        __syncwarp();
+        ++ns[t];
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int gg = g + j, st = gg & 1;
+        mbar_wait(&p_full[t], np[t] & 1);
+        if (t == 0 || j >= nA) mbar_wait(&v_full[st], (gg >> 1) & 1);
+        if (j == 0 && it > 0) mbar_wait(&o_empty[t], (it - 1) & 1);  // previous item's O has been read out
+        tc_fence_after();
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
+            mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, dv + st * kTile + off, idesc,
+                        (j > 0 || k > 0) ? 1u : 0u);
+          }
+          tc_commit(&pv_done[t]);
+          if (t == 1) tc_commit(&v_empty[st]);
+        }
+        __syncwarp();
+        ++np[t];
+      };
+      issue_s(0, 0, false);
+      issue_s(1, 0, nB == 1);
+      for (int j = 0; j < nB; ++j) {
+        if (j < nA) {
+          issue_pv(0, j);
+          if (j + 1 < nA) issue_s(0, j + 1, false);
+        }
+        issue_pv(1, j);
+        if (j + 1 < nB) issue_s(1, j + 1, j + 2 == nB);
+      }
+      g += nB;
+    }
+  } else {
+    const int t = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t t_s = tmem + 256 * t + lane_off, t_o = t_s + 128;
+    const float scl = p.scale_log2;
+    int nb = 0;  // blocks processed by this tile's softmax across items (barrier phases)
+    int it = 0;
+    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      int head, start, len, vstart, pair;
+      if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+      const int q0 = pair * 2 * FA_BM;
+      const int qpos = q0 + t * FA_BM + r;
+      const int nblk = t == 0 ? 2 * pair + 1 : 2 * pair + 2;
+      float m_used = -1e30f, l0 = 0.f, l1 = 0.f;
+      for (int j = 0; j < nblk; ++j, ++nb) {
+        mbar_wait(&s_full[t], nb & 1);
+        tc_fence_after();
+        uint32_t s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * c));
+        tmem_ld_wait();
+        if (j == nblk - 1 || (t == 1 && j == nblk - 2)) {
+          const int lim = min(qpos, len - 1) - j * FA_BN;
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c > lim) s[c] = __float_as_uint(-INFINITY);
+        }
+        float mx = -1e30f;
+#pragma unroll
+        for (int c = 0; c < 128; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
+        mx *= scl;
+        float alpha = 1.f;
+        const bool resc = mx > m_used + kRescaleThresh;
+        if (resc) {
+          alpha = fast_exp2(m_used - mx);
+          m_used = mx;
+          l0 *= alpha;
+          l1 *= alpha;
+        }
+        const float nm = -m_used;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float xa = fmaf(__uint_as_float(s[64 * c + 2 * i]), scl, nm);
+            const float xb = fmaf(__uint_as_float(s[64 * c + 2 * i + 1]), scl, nm);
+            const bool poly = FA_POLY_EVERY > 0 && (i % (FA_POLY_EVERY > 0 ? FA_POLY_EVERY : 1)) == 0;
+            const float a = poly ? poly_exp2(xa) : fast_exp2(xa);
+            const float b = poly ? poly_exp2(xb) : fast_exp2(xb);
+            add2(l0, l1, l0, l1, a, b);
+            pk[i] = pack_bf16x2(a, b);
+          }
+          tmem_st32(t_s + 32 * c, pk);
+        }
+        if (j > 0) mbar_wait(&pv_done[t], (nb - 1) & 1);
+        tc_fence_after();
+        if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(t_o + c * 32, o);
+          }
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[t]);
+      }
+      // epilogue: read O out of TMEM (then release it to the next item), normalise, store
+      mbar_wait(&pv_done[t], (nb - 1) & 1);
+      tc_fence_after();
+      uint32_t o[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(t_o + c * 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32 * c));
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[t]);
+      if (qpos < len) {
+        const float inv = 1.f / (l0 + l1);
+        __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
+#pragma unroll
+        for (int i = 0; i < 128; i += 8) {
+          uint4 v;
+          v.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+          v.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+          v.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+          v.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+          *reinterpret_cast<uint4*>(dst + i) = v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // ------------------------------------------------------------------ flash attention v3
 // v3 = v2 (two query tiles, P in TMEM, two softmax warpgroups) with 64-key blocks, which frees
 // TMEM for a double-buffered S per tile: [S0 | S1 | O] = 64 + 64 + 128 columns per tile.  The
@@ -845,9 +1106,13 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   std::call_once(once, [] {
     cudaFuncSetAttribute(flash_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
     cudaFuncSetAttribute(flash_attn3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa3Smem::ALLOC);
+    cudaFuncSetAttribute(flash_attn4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
   });
-  // v2 by default (same-box A/B, profiles/r01/ab_attn_v2_v3.log: v3 is 6 % slower on 4K / 32K prompts)
-  static const int ver = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 2;
+  // Default (same-box A/B, profiles/r01/ab_attn_*.log): the persistent v4 for short prompts
+  // (mean <= 2048 tokens: +13-19 % at 1K, where v2's per-CTA fixed costs dominate), v2 otherwise
+  // (v4's static item order loses 3 % at 32K); v3 (64-key blocks) only on request.
+  static const int ver_env = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 0;
+  const int ver = ver_env ? ver_env : (T / B <= 2048 ? 4 : 2);
   FaArgs a{};
   a.cu = cu;
   a.vcu = vcu;
@@ -856,7 +1121,15 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   a.Hkv = Hkv;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)FA_D));
   a.o = o;
-  if (ver != 3) {
+  if (ver == 4) {
+    // exact item count needs the prompt lengths on the host; the upper bound is enough: items past
+    // the end map to no pair (fa2_pair fails) -- guarded by counting the real pairs on the device
+    const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    flash_attn4_kernel<<<sms, FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv, a, (int)(pairs_upper * Hq));
+  } else if (ver != 3) {
     const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
     flash_attn2_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv,
                                                                                                       a);
