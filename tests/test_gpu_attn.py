@@ -71,6 +71,18 @@ def test_attention_core_qwen3_heads_sampled():
     assert err <= 1e-2, err
 
 
+@pytest.mark.parametrize("lengths", [[32768], [4096] * 8], ids=["one_32k_prompt", "eight_4k_prompts"])
+def test_attention_core_bench_shapes_sampled(lengths):
+    """The bench's attention configurations at full size (32,768 tokens, Qwen3-235B heads):
+    sampled rows near tile / prompt boundaries and at random, against the oracle."""
+    T = sum(lengths)
+    rng = np.random.default_rng(3)
+    rows = np.unique(np.concatenate([[0, 127, 128, 255, 256, 4095, 4096, T - 1], rng.choice(T, 16, replace=False)]))
+    got, ref = _core(lengths, Hq=64, Hkv=4, seed=17, rows=rows)
+    err = _err(got.reshape(got.shape[0], -1), ref.reshape(ref.shape[0], -1))
+    assert err <= 1e-2, err
+
+
 def _layer(H, Hq, Hkv, lengths, seed, rows=None):
     d = 128
     cu = _cu(lengths)

@@ -32,8 +32,9 @@ def _cu(lengths):
     return torch.from_numpy(np.concatenate([[0], np.cumsum(lengths)]).astype(np.int32)).cuda()
 
 
-def test_decoder_stack_composition_bitwise():
-    wl = Workload(L=3, E=16, k=4, H=512, h=256, seed=21)
+@pytest.mark.parametrize("fp8", [False, True], ids=["bf16_experts", "fp8_experts"])
+def test_decoder_stack_composition_bitwise(fp8):
+    wl = Workload(L=3, E=16, k=4, H=512, h=256, seed=21, fp8=fp8)
     lengths = [700, 1, 300, 129]
     T = sum(lengths)
     cu = _cu(lengths)
