@@ -503,6 +503,18 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
+      // hand the accumulator back to the MMA as soon as the warp's last tcgen05.ld has landed
+      // (before the final chunk's math and store), not after the stores
+      bool released = false;
+      auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (NCTA == 2) mbar_arrive_cluster(&tempty[acc], 0);
+          else mbar_arrive(&tempty[acc]);
+        }
+        released = true;
+      };
       if (MODE == EPI_ROUTER || MODE == EPI_ROUTER16) {
         const int row = wrow0 + lane;
         router_epilogue<MODE == EPI_ROUTER ? 8 : 16>(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows,
@@ -522,12 +534,18 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         for (int c0 = C::EW == 8 ? 64 * ch : 0; c0 < (C::EW == 8 ? 64 * ch + 64 : 128); c0 += 64) {
           uint32_t o[32];
           uint32_t amax2 = 0;  // |bf16| bit patterns of both halves: unsigned order = magnitude order
+          uint32_t gg[2][32], uu[2][32];  // the chunk's 64 gate + 64 up columns, one wait
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            uint32_t g[32], u[32];
-            tmem_ld32(tb + c0 + 32 * half, g);
-            tmem_ld32(tb + 128 + c0 + 32 * half, u);
-            tmem_ld_wait();
+            tmem_ld32(tb + c0 + 32 * half, gg[half]);
+            tmem_ld32(tb + 128 + c0 + 32 * half, uu[half]);
+          }
+          tmem_ld_wait();
+          if (c0 + 64 >= (C::EW == 8 ? 64 * ch + 64 : 128)) release();  // last TMEM read of the tile
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const uint32_t(&g)[32] = gg[half];
+            const uint32_t(&u)[32] = uu[half];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {  // 4 columns per step
               float gv[4], uv[4];
@@ -580,15 +598,19 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN;
           if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
         }
+        const int cbeg = C::EW == 8 ? 128 * ch : 0;
+        const int cend = min(C::EW == 8 ? min(128 * ch + 128, p.BN) : p.BN, max(p.n_out - nt * p.BN, 0));
 #pragma unroll 1
-        for (int c0 = C::EW == 8 ? 128 * ch : 0; c0 < (C::EW == 8 ? min(128 * ch + 128, p.BN) : p.BN); c0 += 64) {
-          if (nt * p.BN + c0 >= p.n_out) break;
+        for (int c0 = cbeg; c0 < cend; c0 += 64) {
           uint32_t o[32];
+          uint32_t rr[2][32];  // the chunk's 64 columns, one wait
+          tmem_ld32(tb + c0, rr[0]);
+          tmem_ld32(tb + c0 + 32, rr[1]);
+          tmem_ld_wait();
+          if (c0 + 64 >= cend) release();  // last TMEM read of the tile: the MMA may reuse it
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            uint32_t r[32];
-            tmem_ld32(tb + c0 + 32 * half, r);
-            tmem_ld_wait();
+            const uint32_t(&r)[32] = rr[half];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {  // 4 columns per step
               float v[4];
@@ -611,12 +633,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * p.BN + c0, wrow0);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (NCTA == 2) mbar_arrive_cluster(&tempty[acc], 0);
-        else mbar_arrive(&tempty[acc]);
-      }
+      if (!released) release();  // router epilogue, or no stored columns
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
