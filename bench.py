@@ -252,13 +252,23 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # Test hooks for running N ranks on ONE GPU (NCCL refuses that): ASYNCEP_BENCH_DEVICE pins every
+    # rank to one device, ASYNCEP_BENCH_BACKEND=gloo runs the control plane (barrier, max-over-ranks)
+    # on gloo; the gather then must be the peer-copy transport (CUDA IPC works within one GPU).
+    backend = os.environ.get("ASYNCEP_BENCH_BACKEND", "nccl")
+    dev_idx = int(os.environ.get("ASYNCEP_BENCH_DEVICE", local))
+    torch.cuda.set_device(dev_idx)
+    dev = torch.device("cuda", dev_idx)
     comm = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        dist.all_reduce(torch.ones(1, device=dev))  # eager comm init
-        comm = A.nccl_comm_ptr()
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+            dist.all_reduce(torch.ones(1, device=dev))  # eager comm init
+            comm = A.nccl_comm_ptr()
+        else:
+            dist.init_process_group(backend)
+            if args.gather == "nccl" or args.ep:
+                raise SystemExit("--gather nccl / --ep need the NCCL backend")
     L, T = args.layers, args.tokens
     seed = 0
     flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0) | (A.FLAG_XPERM if args.xperm else 0)
@@ -300,16 +310,27 @@ def main():
     cs = stack.compute_stream
 
     def barrier():
-        if world > 1:
-            dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
+        if world > 1:
+            if backend == "nccl":
+                dist.barrier(device_ids=[dev_idx])
+            else:
+                dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
 
     for _ in range(args.warmup):
         _run(x, out)
     barrier()
     A.asyncep_reset_stage_times(stack.ctx)
     launches0 = A.asyncep_kernel_launches(stack.ctx)
-    clocks = ClockSampler(local).start()
+    clocks = ClockSampler(dev_idx).start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -322,10 +343,7 @@ def main():
     ms = e0.elapsed_time(e1)
     launches = A.asyncep_kernel_launches(stack.ctx) - launches0
     stages, nfwd = A.asyncep_stage_times(stack.ctx)
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = t.item()
+    ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     value = world * T * args.steps / (ms_max / 1e3)     # whole-job tokens/s
     per_gpu = value / world
@@ -375,10 +393,7 @@ def main():
     e2e_steps(args.steps)
     f1.record(cs)
     barrier()
-    t2 = torch.tensor([f0.elapsed_time(f1)], device=dev)
-    if world > 1:
-        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    e2e_value = world * T * args.steps / (t2.item() / 1e3)
+    e2e_value = world * T * args.steps / (max_over_ranks(f0.elapsed_time(f1)) / 1e3)
 
     attn_info = None
     if args.attn:  # attention half alone (outside the timed region), for the layer breakdown
