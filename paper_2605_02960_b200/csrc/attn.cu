@@ -354,9 +354,22 @@ __device__ __forceinline__ bool fa4_item(const FaArgs& p, int w, int& head, int&
   return true;
 }
 
+constexpr int FA4_RING = 4;
+// consumer side of the work-item ring: lane 0 waits for item number seq and releases its slot
+__device__ __forceinline__ int fa4_next(uint64_t* r_full, uint64_t* r_empty, const int32_t* ring, int seq, int lane) {
+  int w = 0;
+  if (lane == 0) {
+    const int slot = seq % FA4_RING;
+    mbar_wait(&r_full[slot], (uint32_t)(seq / FA4_RING) & 1u);
+    w = ring[slot];
+    mbar_arrive(&r_empty[slot]);
+  }
+  return __shfl_sync(0xffffffffu, w, 0);
+}
+
 __global__ void __launch_bounds__(FA2_NTHREADS, 1)
     flash_attn4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p, int n_items) {
+                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p, int n_items, int* sched) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Fa2Smem::BAR);
@@ -370,10 +383,17 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
   uint64_t* p_full = bars + 12;   // [tile]
   uint64_t* pv_done = bars + 14;  // [tile]
   uint64_t* o_empty = bars + 16;  // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* r_full = bars + 18;   // [FA4_RING] work-item ring: published
+  uint64_t* r_empty = bars + 22;  // [FA4_RING]                 consumed (MMA + 8 softmax warps)
+  int32_t* ring = reinterpret_cast<int32_t*>(bars + 26);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + FA4_RING);
 
   const int warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 0) {
+    for (int i = 0; i < FA4_RING; ++i) {
+      mbar_init(&r_full[i], 1);
+      mbar_init(&r_empty[i], 9);
+    }
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
@@ -400,10 +420,16 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
       tma_prefetch_desc(&map_k);
       tma_prefetch_desc(&map_vt);
       int g = 0;  // K/V blocks loaded so far (ring position)
-      int it = 0;
-      for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+      for (int it = 0;; ++it) {
+        // scheduler: take the next work item from the global counter and publish it to the
+        // MMA and softmax warps through the ring (heavier items come first in the item order)
+        const int slot = it % FA4_RING;
+        mbar_wait(&r_empty[slot], ((uint32_t)(it / FA4_RING) & 1u) ^ 1u);
+        const int w = atomicAdd(sched, 1);
+        ring[slot] = w;
+        mbar_arrive(&r_full[slot]);
         int head, start, len, vstart, pair;
-        if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+        if (w >= n_items || !fa4_item(p, w, head, start, len, vstart, pair)) break;
         const int q0 = pair * 2 * FA_BM, nB = 2 * pair + 2, kvh = head / (p.Hq / p.Hkv);
         mbar_wait(q_empty, (it & 1) ^ 1);  // the previous item's S MMAs are done with Q
         mbar_arrive_expect_tx(q_full, 2 * FA_TILE);
@@ -437,10 +463,10 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
     constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4;
     int g = 0;                   // K/V ring position
     int ns[2] = {0, 0}, np[2] = {0, 0};  // S issued / PV issued per tile (barrier phases)
-    int it = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int w = fa4_next(r_full, r_empty, ring, it, lane);
       int head, start, len, vstart, pair;
-      if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+      if (w >= n_items || !fa4_item(p, w, head, start, len, vstart, pair)) break;
       const int nA = 2 * pair + 1, nB = 2 * pair + 2;
       mbar_wait(q_full, it & 1);
       auto issue_s = [&](int t, int j, bool last) {
@@ -498,10 +524,10 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
     const uint32_t t_s = tmem + 256 * t + lane_off, t_o = t_s + 128;
     const float scl = p.scale_log2;
     int nb = 0;  // blocks processed by this tile's softmax across items (barrier phases)
-    int it = 0;
-    for (int w = blockIdx.x; w < n_items; w += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
+      const int w = fa4_next(r_full, r_empty, ring, it, lane);
       int head, start, len, vstart, pair;
-      if (!fa4_item(p, w, head, start, len, vstart, pair)) break;
+      if (w >= n_items || !fa4_item(p, w, head, start, len, vstart, pair)) break;
       const int q0 = pair * 2 * FA_BM;
       const int qpos = q0 + t * FA_BM + r;
       const int nblk = t == 0 ? 2 * pair + 1 : 2 * pair + 2;
@@ -1108,11 +1134,9 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
     cudaFuncSetAttribute(flash_attn3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa3Smem::ALLOC);
     cudaFuncSetAttribute(flash_attn4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
   });
-  // Default (same-box A/B, profiles/r01/ab_attn_*.log): the persistent v4 for short prompts
-  // (mean <= 2048 tokens: +13-19 % at 1K, where v2's per-CTA fixed costs dominate), v2 otherwise
-  // (v4's static item order loses 3 % at 32K); v3 (64-key blocks) only on request.
-  static const int ver_env = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 0;
-  const int ver = ver_env ? ver_env : (T / B <= 2048 ? 4 : 2);
+  // Default: the persistent, dynamically scheduled v4 (same-box A/B, profiles/r01/ab_attn_v2_v4*.log:
+  // +4 % on 4K prompts, +10 % on 1K, equal on 32K against v2); v2 / v3 on request.
+  static const int ver = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 4;
   FaArgs a{};
   a.cu = cu;
   a.vcu = vcu;
@@ -1128,7 +1152,10 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    flash_attn4_kernel<<<sms, FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv, a, (int)(pairs_upper * Hq));
+    static int* sched = nullptr;  // the dynamic scheduler's counter (one per process / device)
+    if (!sched && cudaMalloc(&sched, sizeof(int)) != cudaSuccess) return false;
+    cudaMemsetAsync(sched, 0, sizeof(int), s);
+    flash_attn4_kernel<<<sms, FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv, a, (int)(pairs_upper * Hq), sched);
   } else if (ver != 3) {
     const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
     flash_attn2_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv,
