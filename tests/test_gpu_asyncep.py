@@ -238,3 +238,33 @@ def test_copy_engine_gather_bitwise_equals_resident(N):
     with pytest.raises(A.AsyncEPError):  # a gathered layer without a peer entry is rejected
         bad = [None] * wl.L
         A.asyncep_set_peer_shards(st.ctx, bad)
+
+
+def test_gather_copy_transport():
+    """asyncep_gather_copy: the co-resident copy kernel for 16-B aligned sizes, cudaMemcpyAsync
+    otherwise -- both byte-exact; zero bytes is a no-op."""
+    src = torch.randint(0, 256, (3 * (1 << 20) + 48,), dtype=torch.uint8, device="cuda")
+    for off, n in ((0, src.numel()), (16, 1 << 20), (1, 12345), (0, 0)):
+        dst = torch.zeros_like(src)
+        A.asyncep_gather_copy(dst[off:], src[off:], n)
+        torch.cuda.synchronize()
+        assert torch.equal(dst[off:off + n], src[off:off + n])
+        assert int(dst[:off].sum()) == 0 and int(dst[off + n:].sum()) == 0
+
+
+def test_attention_abi_errors():
+    cfg = A.make_attn_config(256, 8, 2, 128, max_tokens=64)
+    q = torch.zeros((64, 8, 128), dtype=torch.bfloat16, device="cuda")
+    k = torch.zeros((64, 2, 128), dtype=torch.bfloat16, device="cuda")
+    vt = torch.zeros((2, 128, 64), dtype=torch.bfloat16, device="cuda")
+    cu = torch.tensor([0, 64], dtype=torch.int32, device="cuda")
+    o = torch.empty_like(q)
+    with pytest.raises(A.AsyncEPError):  # ldv not a multiple of 8
+        A.asyncep_attention(cfg, q, k, vt, 63, cu, cu, o)
+    with pytest.raises(A.AsyncEPError):  # head_dim must be 128
+        A.asyncep_attention(A.make_attn_config(256, 8, 2, 64, max_tokens=64), q, k, vt, 64, cu, cu, o)
+    with pytest.raises(A.AsyncEPError):  # q_heads not a multiple of kv_heads
+        A.asyncep_attention(A.make_attn_config(256, 6, 4, 128, max_tokens=64), q, k, vt, 64, cu, cu, o)
+    A.asyncep_attention(cfg, q, k, vt, 64, cu, cu, o)  # all-zero inputs: uniform attention over v = 0
+    torch.cuda.synchronize()
+    assert int(torch.count_nonzero(o)) == 0
