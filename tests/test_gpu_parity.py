@@ -228,3 +228,32 @@ def test_fused_dispatch_bitwise(T):
         outs.append(run_layer(wl, st, 0, x)[0])
         del st
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+def test_qwen3_235b_eight_layer_stack_sampled():
+    """The bench's exact workload: the 8-layer Qwen3-235B stack at 32,768 tokens through
+    MoEStack.run (the launch configuration bench.py times).  Every layer's input is recorded
+    (R9: layer l reads the GPU's bf16 output of layer l-1) and 32 sampled tokens per layer are
+    checked against the oracle (output tolerance of R7; the routing of these tokens is the
+    oracle's -- per-token router parity is covered by the single-layer tests)."""
+    T = 32768
+    wl = Workload(L=8, E=128, k=8, H=4096, h=1536, seed=0)
+    st = wl.stack(max_tokens=T)
+    x = wl.tokens(T)
+    rng = np.random.default_rng(7)
+    idx = np.unique(np.concatenate([[0, T - 1], rng.choice(T, 30, replace=False)]))
+    ins = {}
+    out = st.run(x, record=lambda l, xl: ins.__setitem__(l, f32(xl)[idx])).clone()
+    torch.cuda.synchronize()
+    outs = {l: ins[l + 1] for l in range(wl.L - 1)}
+    outs[wl.L - 1] = f32(out)[idx]
+    del st
+    torch.cuda.empty_cache()
+    for l in range(wl.L):
+        wr, g, u, d = wl.host_layer(l)
+        xl = ins[l]
+        # the oracle's routing of the sampled tokens, then the acceptance check with the GPU output
+        orc = oracle.router(xl, wr, wl.k)
+        rep = check_layer(xl, wr, g, u, d, wl.k, outs[l], orc["ids"], orc["w"], None)
+        print(l, rep)
+        del wr, g, u, d
