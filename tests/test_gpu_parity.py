@@ -3,6 +3,8 @@
 Tolerances (north_star): ids / counts bit-exact outside near ties (gap < 1e-4), routing
 weights 1e-5, BF16 outputs err <= 2e-2 with err = max|y - y*| / max|y*| (R7).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -230,14 +232,17 @@ def test_fused_dispatch_bitwise(T):
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
 
 
-def test_qwen3_235b_eight_layer_stack_sampled():
+@pytest.mark.parametrize("fp8", [False, pytest.param(True, marks=pytest.mark.skipif(
+    not os.environ.get("ASYNCEP_LONG_TESTS"), reason="4 min (host dequantisation of 8 FP8 layers); "
+    "ASYNCEP_LONG_TESTS=1 runs it, log in profiles/r01/parity_8layer_stack_sampled_fp8.log"))], ids=["bf16", "fp8"])
+def test_qwen3_235b_eight_layer_stack_sampled(fp8):
     """The bench's exact workload: the 8-layer Qwen3-235B stack at 32,768 tokens through
     MoEStack.run (the launch configuration bench.py times).  Every layer's input is recorded
     (R9: layer l reads the GPU's bf16 output of layer l-1) and 32 sampled tokens per layer are
     checked against the oracle (output tolerance of R7; the routing of these tokens is the
     oracle's -- per-token router parity is covered by the single-layer tests)."""
     T = 32768
-    wl = Workload(L=8, E=128, k=8, H=4096, h=1536, seed=0)
+    wl = Workload(L=8, E=128, k=8, H=4096, h=1536, seed=0, fp8=fp8)
     st = wl.stack(max_tokens=T)
     x = wl.tokens(T)
     rng = np.random.default_rng(7)
@@ -254,6 +259,6 @@ def test_qwen3_235b_eight_layer_stack_sampled():
         xl = ins[l]
         # the oracle's routing of the sampled tokens, then the acceptance check with the GPU output
         orc = oracle.router(xl, wr, wl.k)
-        rep = check_layer(xl, wr, g, u, d, wl.k, outs[l], orc["ids"], orc["w"], None)
+        rep = check_layer(xl, wr, g, u, d, wl.k, outs[l], orc["ids"], orc["w"], None, tol=6e-2 if fp8 else 2e-2)
         print(l, rep)
         del wr, g, u, d
