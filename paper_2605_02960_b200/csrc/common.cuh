@@ -184,6 +184,17 @@ AEP_DEV void cluster_sync_all() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster
+// remote arrive with the default semantics (release at CTA scope, as CUTLASS's ClusterBarrier):
+// orders this thread's prior operations without the cluster-scope memory barrier of
+// .release.cluster (which cost the GEMM epilogue a MEMBAR.ALL + ERRBAR per tile)
+AEP_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
 AEP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"

@@ -510,7 +510,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if (NCTA == 2) mbar_arrive_cluster(&tempty[acc], 0);
+          if (NCTA == 2) mbar_arrive_remote(&tempty[acc], 0);
           else mbar_arrive(&tempty[acc]);
         }
         released = true;
