@@ -349,9 +349,19 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
+      // With the fused gather the scheduler publishes one tile ahead, so the gather warps can
+      // fetch the next tile's row indices while they copy the current tile (and, in the peer CTA,
+      // a gather warp is the consumer that arms the ring slot for the st.async).
+      int t_next = (leader && gather) ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
       for (int seq = 0;; ++seq) {
-        const int t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
-                             : sched_consume<NCTA>(ring, seq, false, true);
+        int t;
+        if (leader && gather) {
+          t = t_next;
+          if (t < total) t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits);
+        } else {
+          t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
+                     : sched_consume<NCTA>(ring, seq, false, !gather);
+        }
         if (t >= total) break;
         int mt, nt;
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
@@ -392,18 +402,31 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     const uint32_t dst0 = smem_u32(sA) + (uint32_t)(rr * 128 + ((ch ^ (rr & 7)) << 4));
     int stage = 0;
     uint32_t phase = 0;
-    for (int seq = 0;; ++seq) {
+    const bool arm = NCTA == 2 && !leader && warp == 2;  // peer: this warp arms the ring slots
+    auto next_tile = [&](int seq) {
       int t = 0;
-      if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false);
-      t = __shfl_sync(0xffffffffu, t, 0);
-      if (t >= total) break;
+      if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, arm);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    auto load_rows = [&](int t, int32_t (&tok)[16]) {  // the tile's 16 row indices of this thread
+      if (t >= total) return;
       int mt, nt;
       decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
       const int row0 = mt * TM + (int)rank * BM;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tok[i] = __ldg(p.gather_rows + row0 + rr + 8 * i);
+    };
+    int t = next_tile(0);
+    int32_t tok[16];
+    load_rows(t, tok);
+    for (int seq = 0;; ++seq) {
+      if (t >= total) break;
+      const int tn = next_tile(seq + 1);  // published one tile ahead: prefetch its row indices
+      int32_t tok_n[16];
+      load_rows(tn, tok_n);
       const uint8_t* src[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        src[i] = p.gather_src + (int64_t)__ldg(p.gather_rows + row0 + rr + 8 * i) * p.gather_ld + ch * 16;
+      for (int i = 0; i < 16; ++i) src[i] = p.gather_src + (int64_t)tok[i] * p.gather_ld + ch * 16;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&empty[stage], phase ^ 1);
         const uint32_t dst = dst0 + (uint32_t)(stage * A_BYTES);
@@ -412,6 +435,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         cp_async_mbar_arrive_noinc(&afull[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      t = tn;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tok[i] = tok_n[i];
     }
     __syncwarp();
   } else if (warp == 1) {
