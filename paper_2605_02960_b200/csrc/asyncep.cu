@@ -214,6 +214,7 @@ struct asyncep_ctx {
   // tcgen05 tensor maps
   aep::ActMaps act_maps;
   std::vector<aep::GemmMaps> layer_maps;  // per resident layer (index l), valid if resident[l]
+  std::vector<aep::GemmMaps> own_maps;    // per gathered layer: maps over this rank's own shard
   std::vector<char> resident;
   aep::GemmMaps slot_maps[2];
   std::vector<aep::RouterTc> router_maps;  // per layer
@@ -397,6 +398,14 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
                                cfg->ffn, c->act_maps.bn2, fp8))
       return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (layer %d)", l));
   }
+  // gathered layers: the GEMMs read this rank's own experts straight from its shard
+  c->own_maps.resize(L);
+  for (int l = 0; l < L; ++l) {
+    if (layer_resident(c, l) || !c->shard[l]) continue;
+    if (!aep::make_weight_maps(c->own_maps[l], c->shard[l], c->expert_bytes, cfg->num_experts / cfg->world_size,
+                               cfg->hidden, cfg->ffn, c->act_maps.bn2, fp8))
+      return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (own shard %d)", l));
+  }
   c->router_maps.resize(L);
   for (int l = 0; l < L; ++l)
     if (!aep::make_router_wmap(c->router_maps[l], (const bf16*)c->router_w[l], cfg->hidden, cfg->num_experts))
@@ -438,6 +447,8 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     for (int i = 1; i <= N; ++i) {
       const int r = (c->cfg.rank + i) % N;
       if (!shards[r]) return fail(ASYNCEP_ERR_INVALID_ARG, "null shard %d", r);
+      // the tcgen05 GEMMs read the own shard in place (the SIMT debug GEMM reads the whole slot)
+      if (r == c->cfg.rank && !c->offload && !(c->cfg.flags & ASYNCEP_FLAG_SIMT_GEMM)) continue;
       uint8_t* dst = (uint8_t*)c->slot[s] + (size_t)r * c->shard_bytes;
       const uint8_t* src = (const uint8_t*)(r == c->cfg.rank && c->offload ? own : shards[r]);
       const bool paced = c->link_bps > 0 && r != c->cfg.rank;  // own shard is a local copy
@@ -653,6 +664,14 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (3) grouped GEMM: gate/up + SwiGLU, then down.  Y_perm overwrites X_perm.
   const uint8_t* wl = (const uint8_t*)(from_window ? c->window[wi] : res ? c->shard[layer] : c->slot[s]);
   const aep::GemmMaps& wm = from_window ? c->win_maps[wi] : res ? c->layer_maps[layer] : c->slot_maps[s];
+  // gathered layer: this rank's experts come from its own shard (the slot's copy of it is skipped)
+  aep::OwnShard own_sh;
+  const bool use_own = !from_window && !res && !c->offload && c->shard[layer];
+  if (use_own) {
+    const int per = E / cf.world_size;
+    own_sh = aep::OwnShard{&c->own_maps[layer], (const uint8_t*)c->shard[layer], cf.rank * per, (cf.rank + 1) * per};
+  }
+  const aep::OwnShard* own = use_own ? &own_sh : nullptr;
   aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
@@ -665,16 +684,17 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   } else if (fp8) {
     f8.layer = wl;
     aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const void*)(ws + c->L.xq) : nullptr, T, src_tok,
-                         c->num_sms, st, &f8);
+                         c->num_sms, st, &f8, own);
     aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
                           (float*)(ws + c->L.ascale), st);
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
-    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8);
+    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8, own);
     c->launches += 3;
   } else {
-    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? x : nullptr, T, src_tok, c->num_sms, st);
+    aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? x : nullptr, T, src_tok, c->num_sms, st, nullptr,
+                         own);
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
-    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st);
+    aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, nullptr, own);
     c->launches += 2;
   }
   if (timing && (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS)) CUDA_TRY(cudaEventRecord(ev[4], st));

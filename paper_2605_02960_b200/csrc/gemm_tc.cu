@@ -97,6 +97,9 @@ struct TcArgs {
   const int32_t* gather_rows;
   const uint8_t* gather_src;
   int64_t gather_ld;
+  // experts [own_lo, own_hi) are read through map_b2 (this rank's own shard, local index e - own_lo)
+  int own_lo, own_hi;
+  const uint8_t* b_scale_base_own;
   // router epilogue
   int top_k, norm_topk;
   int32_t* ids;
@@ -269,7 +272,8 @@ __device__ __forceinline__ const float* stage_scales(float* dst, const float* sr
 template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCTA, MODE>::NTHR == 256 ? 224 : 168))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   const __grid_constant__ CUtensorMap map_out, const TcArgs p) {
+                   const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_b2,
+                   const TcArgs p) {
   using C = Cfg<NCTA, MODE>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -308,6 +312,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   if (warp == 0 && lane == 0) {
     if (!gather) tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (p.own_hi > p.own_lo) tma_prefetch_desc(&map_b2);
     if (MODE == EPI_PLAIN || MODE == EPI_SWIGLU) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
       // leader: own expect_tx arrive + peer producer's arrive (+ peer's gathered-A forward)
@@ -367,6 +372,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
         int e = find_expert(s_ts, G, mt);
         if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
+        const bool own_e = e >= p.own_lo && e < p.own_hi;
+        const CUtensorMap* mb = own_e ? &map_b2 : &map_b;
+        if (own_e) e -= p.own_lo;
         const int row0 = mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -378,14 +386,14 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           } else {
             mbar_arrive_expect_tx(&full[stage], tx);
             if (!gather) {
               if (p.pol_a == 3) tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            tma_load_3d(sB + stage * C::B_BYTES_MAX, &map_b, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+            tma_load_3d(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -553,7 +561,10 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           sa = p.a_scale[gather ? __ldg(p.gather_rows + wrow0 + lane) : wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256;
+          sb = reinterpret_cast<const float*>(
+                   (ge >= p.own_lo && ge < p.own_hi ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
+                                                    : p.b_scale_base + (size_t)ge * p.expert_bytes)) +
+               nt * 256;
           if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, 256, lane);
         }
 #pragma unroll 1
@@ -621,7 +632,10 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           sa = p.a_scale[wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
-          sb = reinterpret_cast<const float*>(p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * p.BN;
+          sb = reinterpret_cast<const float*>(
+                   (ge >= p.own_lo && ge < p.own_hi ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
+                                                    : p.b_scale_base + (size_t)ge * p.expert_bytes)) +
+               nt * p.BN;
           if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
         }
         const int cbeg = C::EW == 8 ? 128 * ch : 0;
@@ -677,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 
 template <int MODE, int NCTA, bool F8 = false>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
-                 cudaStream_t s) {
+                 cudaStream_t s, const CUtensorMap* mb2 = nullptr) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -695,7 +709,7 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, a);
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, mb2 ? *mb2 : mb, a);
 }
 
 // Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
@@ -712,7 +726,7 @@ int grouped_raster() {
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
                     const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false,
-                    const void* gather_src = nullptr, int64_t gather_ld = 0) {
+                    const void* gather_src = nullptr, int64_t gather_ld = 0, const OwnShard* own = nullptr) {
   static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
@@ -729,6 +743,13 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.gather_rows = gather_rows;
   a.gather_src = static_cast<const uint8_t*>(gather_src);
   a.gather_ld = gather_ld;
+  const CUtensorMap* mb2 = nullptr;
+  if (own && own->maps && own->hi > own->lo) {
+    a.own_lo = own->lo;
+    a.own_hi = own->hi;
+    mb2 = gemm2 ? &own->maps->wd : &own->maps->wgu;
+    if (f8) a.b_scale_base_own = own->base + (gemm2 ? f8->sd_off : f8->sgu_off);
+  }
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
   a.group_mod = g.group_mod;
   if (f8) {
@@ -741,14 +762,14 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
   const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
   if (f8) {  // FP8 experts: CTA pairs only
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s);
-    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2);
   } else if (ncta == 2) {
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s);
-    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s, mb2);
   } else {
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 1>(a, ma, mb, mo, grid, s);
-    else launch_mode<EPI_PLAIN, 1>(a, ma, mb, mo, grid, s);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 1>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 1>(a, ma, mb, mo, grid, s, mb2);
   }
 }
 }  // namespace
@@ -824,27 +845,23 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
                      const void* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
-                     const F8Args* f8) {
+                     const F8Args* f8, const OwnShard* own) {
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns.
   // x_gather != nullptr: dispatch fused into the A load (rows gathered from the token-major
   // x / x_q through src_tok); the A map is then unused.
   const int64_t ld = (int64_t)H * (f8 ? 1 : 2);
   const CUtensorMap& ma = f8 ? am.xq : am.xperm;
   launch_grouped(g, ma, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s,
-                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld);
+                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own);
   (void)T;
   return true;
 }
 
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
-                     int num_sms, cudaStream_t s, const F8Args* f8) {
+                     int num_sms, cudaStream_t s, const F8Args* f8, const OwnShard* own) {
   const int bn = am.bn2;
-  if (f8)
-    launch_grouped(g, am.aq, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s, nullptr, f8,
-                   true);
-  else
-    launch_grouped(g, am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s, nullptr,
-                   nullptr, true);
+  launch_grouped(g, f8 ? am.aq : am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s,
+                 nullptr, f8, true, nullptr, 0, own);
 }
 
 // ------------------------------------------------------------------ dense GEMM (NEXT-3 projections)

@@ -80,6 +80,14 @@ struct GemmMaps {
   CUtensorMap wd;    // 3D {h, H, E},  box {128 B, BN2/NCTA rows, 1}
   bool fp8 = false;
 };
+// Gathered layers: experts [lo, hi) (this rank's own shard) are read by the GEMMs straight from
+// the rank's resident shard (maps over its hi - lo experts), so the copy transports never copy
+// the own shard into the slot.
+struct OwnShard {
+  const GemmMaps* maps = nullptr;
+  const uint8_t* base = nullptr;  // own shard base (FP8 scales)
+  int lo = 0, hi = 0;
+};
 // FP8 experts (R6): where the GEMMs find their scales.
 struct F8Args {
   const float* x_scale;    // [R] per permuted row (per token), from the permute quantisation
@@ -108,9 +116,9 @@ int gemm2_bn(int H);
 // into the GEMM and X_perm is never written.
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
                      const void* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
-                     const F8Args* f8 = nullptr);
+                     const F8Args* f8 = nullptr, const OwnShard* own = nullptr);
 void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* yperm,
-                     int num_sms, cudaStream_t s, const F8Args* f8 = nullptr);
+                     int num_sms, cudaStream_t s, const F8Args* f8 = nullptr, const OwnShard* own = nullptr);
 
 // Step (4): weighted combine (+ residual).
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,

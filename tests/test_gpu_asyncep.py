@@ -48,7 +48,16 @@ def test_slot_holds_the_unsharded_layer_bytes():
     from paper_2605_02960_b200 import asyncep as A
     A.asyncep_prefetch_layer_local(s0.ctx, 1, [ranks[r].shards[1] for r in range(N)])
     torch.cuda.synchronize()
-    assert torch.equal(s0.slots[1], full.shards[1])
+    # rank-major slot = the unsharded layer, except rank 0's own region: the copy transport does
+    # not copy the own shard (the GEMMs read it in place from the rank's resident shard)
+    sb = s0.slots[1].numel() // N
+    assert torch.equal(s0.slots[1][sb:], full.shards[1][sb:])
+    assert torch.equal(ranks[0].shards[1], full.shards[1][:sb])
+    # with the SIMT debug GEMM (which reads the whole slot) the own shard is copied too
+    s1 = wl.stack(max_tokens=64, world_size=N, rank=0, flags=A.FLAG_SIMT_GEMM)
+    A.asyncep_prefetch_layer_local(s1.ctx, 1, [ranks[r].shards[1] for r in range(N)])
+    torch.cuda.synchronize()
+    assert torch.equal(s1.slots[1], full.shards[1])
 
 
 def test_prefetch_ordering_errors():
