@@ -26,6 +26,7 @@
 // tile_start (permute scan; expert rows padded to 256), no host sync.  Every output tile
 // is produced by one CTA (pair) in a fixed K order: bitwise deterministic results that do
 // not depend on the grid size.
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -45,13 +46,23 @@ constexpr int A_BYTES = BM * BK * 2;           // 16 KB
 constexpr int STG_BYTES = 32 * 128;            // per epilogue warp: 32 rows x 64 bf16 (SW128)
 constexpr int SCL_BYTES = 256 * 4;             // per epilogue warp: the tile's 256 FP8 weight scales
 constexpr int TMEM_COLS = 512;
-constexpr int RING = 4;
+constexpr int RING = 8;
   // tile ids in flight between the scheduler and the consumers
 
 enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
 
 #ifndef PLAIN_NSTG
 #define PLAIN_NSTG 1
+#endif
+#ifndef GEMM_WAITPROF
+#define GEMM_WAITPROF 0  // 1: the MMA / gather / producer threads printf their barrier-wait cycles (A/B only)
+#endif
+#if GEMM_WAITPROF
+#define WP_DECL(n) long long n = 0;
+#define WP_WAIT(acc, stmt) { const long long c_ = clock64(); stmt; acc += clock64() - c_; }
+#else
+#define WP_DECL(n)
+#define WP_WAIT(acc, stmt) stmt;
 #endif
 #ifndef EPI8
 #define EPI8 0  // 1: 8 epilogue warps on CTA-pair GEMMs (two per TMEM lane quadrant, split columns)
@@ -195,12 +206,27 @@ __device__ __forceinline__ void router_epilogue(uint32_t tb, int E, int k, int n
 // warp's 32 x 128 B staging buffer (128-B swizzle: 16-B chunk j of row r at chunk
 // j ^ (r & 7), conflict-free) and one TMA bulk tensor store of the {64 x 32} box.
 // With NSTG = 2 buffers (chunk parity picks one) only the store before last must have been read.
+#if GEMM_WAITPROF
+#define g_wp_store wp_store_acc
+#else
+#define g_wp_store 0
+#endif
 template <int NSTG>
 __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t* stg, int lane,
-                                                const CUtensorMap* map_out, int col0, int row0) {
+                                                const CUtensorMap* map_out, int col0, int row0
+#if GEMM_WAITPROF
+                                                , long long& wp_store_acc
+#endif
+                                                ) {
   if (lane == 0) {  // the store that last used this buffer has finished reading it
+#if GEMM_WAITPROF
+    const long long c_ = clock64();
+#endif
     if (NSTG == 2) bulk_wait_read1();
     else bulk_wait_read0();
+#if GEMM_WAITPROF
+    wp_store_acc += clock64() - c_;
+#endif
   }
   __syncwarp();
   const uint32_t base = smem_u32(stg) + lane * 128;
@@ -354,18 +380,24 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      // With the fused gather the scheduler publishes one tile ahead, so the gather warps can
-      // fetch the next tile's row indices while they copy the current tile (and, in the peer CTA,
-      // a gather warp is the consumer that arms the ring slot for the st.async).
-      int t_next = (leader && gather) ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
+      WP_DECL(wp_e) WP_DECL(wp_s)
+#if GEMM_WAITPROF
+      const long long wp_t0 = clock64();
+#endif
+      // The scheduler publishes one tile ahead: the global atomic that fetches tile seq+1 is in
+      // flight while tile seq's loads are issued (on short-K tiles its latency otherwise sat
+      // between two tiles' loads), and with the fused gather the gather warps fetch the next
+      // tile's row indices while they copy the current tile (in the peer CTA a gather warp is
+      // then the consumer that arms the ring slot for the st.async; without the gather the peer
+      // producer arms it -- a complete_tx that lands before the arm leaves the phase pending).
+      int t_next = leader ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
       for (int seq = 0;; ++seq) {
         int t;
-        if (leader && gather) {
+        if (leader) {
           t = t_next;
-          if (t < total) t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits);
+          if (t < total) WP_WAIT(wp_s, t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits))
         } else {
-          t = leader ? sched_publish<NCTA>(ring, p.sched, seq, unit, nunits)
-                     : sched_consume<NCTA>(ring, seq, false, !gather);
+          WP_WAIT(wp_s, t = sched_consume<NCTA>(ring, seq, false, !gather))
         }
         if (t >= total) break;
         int mt, nt;
@@ -378,7 +410,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         const int row0 = mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
           if (NCTA == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], tx);
             else mbar_arrive_cluster_relaxed(&full[stage], 0);
@@ -398,6 +430,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+#if GEMM_WAITPROF
+      printf("WPP %d %d %lld %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_e, wp_s);
+#endif
     }
     __syncwarp();
   } else if (gather && (warp == 2 || warp == 3)) {
@@ -424,6 +459,10 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #pragma unroll
       for (int i = 0; i < 16; ++i) tok[i] = __ldg(p.gather_rows + row0 + rr + 8 * i);
     };
+    WP_DECL(wp_e)
+#if GEMM_WAITPROF
+    const long long wp_t0 = clock64();
+#endif
     int t = next_tile(0);
     int32_t tok[16];
     load_rows(t, tok);
@@ -436,7 +475,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #pragma unroll
       for (int i = 0; i < 16; ++i) src[i] = p.gather_src + (int64_t)tok[i] * p.gather_ld + ch * 16;
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
+        WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
         const uint32_t dst = dst0 + (uint32_t)(stage * A_BYTES);
 #pragma unroll
         for (int i = 0; i < 16; ++i) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
@@ -447,6 +486,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #pragma unroll
       for (int i = 0; i < 16; ++i) tok[i] = tok_n[i];
     }
+#if GEMM_WAITPROF
+    if (lane == 0 && warp == 2) printf("WPG %d %d %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_e);
+#endif
     __syncwarp();
   } else if (warp == 1) {
     if (gather && NCTA == 2 && !leader) {
@@ -476,16 +518,20 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      WP_DECL(wp_f) WP_DECL(wp_a) WP_DECL(wp_t) WP_DECL(wp_s)
+#if GEMM_WAITPROF
+      const long long wp_t0 = clock64();
+#endif
       for (int seq = 0;; ++seq) {
         int t = 0;
-        if (lane == 0) t = sched_consume<NCTA>(ring, seq, true, false);
+        WP_WAIT(wp_s, if (lane == 0) t = sched_consume<NCTA>(ring, seq, true, false))
         if (__shfl_sync(0xffffffffu, t, 0) >= total) break;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        WP_WAIT(wp_t, mbar_wait(&tempty[acc], acc_phase ^ 1))
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          if (gather) mbar_wait(&afull[stage], phase);  // own gathered A half
+          WP_WAIT(wp_f, mbar_wait(&full[stage], phase))
+          WP_WAIT(wp_a, if (gather) mbar_wait(&afull[stage], phase))  // own gathered A half
           tc_fence_after();
           // descriptor start address field is addr >> 4: a stage / a 32-B K step are plain adds
           const uint64_t ad = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
@@ -516,6 +562,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#if GEMM_WAITPROF
+      if (lane == 0) printf("WPM %d %lld %lld %lld %lld %lld\n", (int)blockIdx.x, clock64() - wp_t0, wp_f, wp_a, wp_t, wp_s);
+#endif
     }
     __syncwarp();
   } else if (warp >= 4) {
@@ -526,15 +575,19 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     uint32_t chunk = 0;  // stores issued by this warp (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
+    WP_DECL(wp_f) WP_DECL(wp_s) WP_DECL(wp_store_acc)
+#if GEMM_WAITPROF
+    const long long wp_t0 = clock64();
+#endif
     for (int seq = 0;; ++seq) {
       int t = 0;
-      if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false);
+      WP_WAIT(wp_s, if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false))
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= total) break;
       int mt, nt;
       decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
       const int wrow0 = mt * TM + (int)rank * BM + quad * 32;  // first row of this warp's slice
-      mbar_wait(&tfull[acc], acc_phase);
+      WP_WAIT(wp_f, mbar_wait(&tfull[acc], acc_phase))
       tc_fence_after();
       const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * 256);
       // hand the accumulator back to the MMA as soon as the warp's last tcgen05.ld has landed
@@ -621,7 +674,11 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               }
             }
           }
-          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * 128 + c0, wrow0);
+          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * 128 + c0, wrow0
+#if GEMM_WAITPROF
+                                  , wp_store_acc
+#endif
+                                  );
           if (F8) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
         }
         if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
@@ -670,13 +727,20 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               o[16 * half + 2 * q + 1] = pack_bf16x2(v[2], v[3]);
             }
           }
-          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * p.BN + c0, wrow0);
+          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * p.BN + c0, wrow0
+#if GEMM_WAITPROF
+                                  , wp_store_acc
+#endif
+                                  );
         }
       }
       if (!released) release();  // router epilogue, or no stored columns
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+#if GEMM_WAITPROF
+    if (lane == 0 && warp == 4) printf("WPE %d %d %lld %lld %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_f, wp_s, g_wp_store);
+#endif
     if ((MODE == EPI_PLAIN || MODE == EPI_SWIGLU) && lane == 0) bulk_wait0();  // this warp's stores done
     __syncwarp();
   }
