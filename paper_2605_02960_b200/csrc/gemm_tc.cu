@@ -64,6 +64,9 @@ enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // ro
 #define WP_DECL(n)
 #define WP_WAIT(acc, stmt) stmt;
 #endif
+#ifndef PROD2
+#define PROD2 1  // 1: without the fused gather, warp 3 issues the B (weight) loads and warp 0 the A loads
+#endif
 #ifndef EPI8
 #define EPI8 0  // 1: 8 epilogue warps on CTA-pair GEMMs (two per TMEM lane quadrant, split columns)
 #endif
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     if (MODE == EPI_PLAIN || MODE == EPI_SWIGLU) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
       // leader: own expect_tx arrive + peer producer's arrive (+ peer's gathered-A forward)
-      mbar_init(&full[s], NCTA + (gather && NCTA == 2 ? 1 : 0));
+      mbar_init(&full[s], (PROD2 && !gather ? 2 : 1) * NCTA + (gather && NCTA == 2 ? 1 : 0));
       mbar_init(&empty[s], 1);
       mbar_init(&afull[s], 64);  // one .noinc cp.async arrival per gather thread
     }
@@ -354,7 +357,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       mbar_init(&sfull[r], 1);
       // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue
       // warps}; fused dispatch adds the 2 gather warps of each CTA and the peer's forwarder
-      mbar_init(&sempty[r], (1 + C::EW) * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0));
+      mbar_init(&sempty[r], (1 + C::EW) * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0) +
+                                (PROD2 && !gather ? NCTA : 0));
     }
     fence_barrier_init();
   }
@@ -373,14 +377,18 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
   const TileRing ring{sfull, sempty, sring};
 
-  if (warp == 0) {
+  if (warp == 0 || (PROD2 && !gather && warp == 3)) {
     // Producer warp, lane 0: arms the stage barrier and loads B (and A unless it is gathered).
+    // PROD2 without the gather: warp 0 loads A (and runs the scheduler), warp 3 loads B.
+    const bool do_a = !gather && (!PROD2 || warp == 0);
+    const bool do_b = !PROD2 || gather || warp == 3;
+    const bool sched_lead = warp == 0;
     if (lane == 0) {
-      const uint32_t tx = (uint32_t)NCTA * ((gather ? 0u : (uint32_t)A_BYTES) + (uint32_t)bn_cta * BK * 2);
+      const uint32_t tx = (uint32_t)NCTA * ((do_a ? (uint32_t)A_BYTES : 0u) + (do_b ? (uint32_t)bn_cta * BK * 2 : 0u));
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
-      WP_DECL(wp_e) WP_DECL(wp_s)
+      WP_DECL(wp_e) WP_DECL(wp_s) WP_DECL(wp_i)
 #if GEMM_WAITPROF
       const long long wp_t0 = clock64();
 #endif
@@ -390,10 +398,12 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       // tile's row indices while they copy the current tile (in the peer CTA a gather warp is
       // then the consumer that arms the ring slot for the st.async; without the gather the peer
       // producer arms it -- a complete_tx that lands before the arm leaves the phase pending).
-      int t_next = leader ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
+      int t_next = (leader && sched_lead) ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
       for (int seq = 0;; ++seq) {
         int t;
-        if (leader) {
+        if (!sched_lead) {
+          WP_WAIT(wp_s, t = sched_consume<NCTA>(ring, seq, leader, false))
+        } else if (leader) {
           t = t_next;
           if (t < total) WP_WAIT(wp_s, t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits))
         } else {
@@ -411,27 +421,33 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         const int brow = nt * p.BN + (int)rank * bn_cta;
         for (int kb = 0; kb < nkb; ++kb) {
           WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
+#if GEMM_WAITPROF
+          const long long wp_c = clock64();
+#endif
           if (NCTA == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], tx);
             else mbar_arrive_cluster_relaxed(&full[stage], 0);
-            if (!gather) {
+            if (do_a) {
               if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+            if (do_b) tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           } else {
             mbar_arrive_expect_tx(&full[stage], tx);
-            if (!gather) {
+            if (do_a) {
               if (p.pol_a == 3) tma_load_2d_nohint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            tma_load_3d(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+            if (do_b) tma_load_3d(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           }
+#if GEMM_WAITPROF
+          wp_i += clock64() - wp_c;
+#endif
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
 #if GEMM_WAITPROF
-      printf("WPP %d %d %lld %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_e, wp_s);
+      printf("WPP %d %d %lld %lld %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_e, wp_s, wp_i);
 #endif
     }
     __syncwarp();
