@@ -25,6 +25,43 @@ __device__ __forceinline__ int sw128(int r, int k) {
   return (r / 8) * 1024 + (r % 8) * 128 + ((((k * 2) / 16) ^ (r % 8)) * 16) + (k * 2) % 16;
 }
 
+// back-to-back issue rate: n MMAs (K = 16 each) into one accumulator, clock64 around issue + commit wait
+__global__ void __cluster_dims__(2, 1, 1) rate(int M, int n, long long* cycles) {
+  __shared__ __align__(1024) uint8_t sa[128 * 128];
+  __shared__ __align__(1024) uint8_t sb[128 * 128];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const uint32_t rank = cluster_ctarank();
+  for (int i = tid; i < 128 * 128; i += blockDim.x) sa[i] = sb[i] = 0;
+  fence_proxy_async_smem();
+  if (tid < 32) tmem_alloc2(&tslot, 512);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_barrier_init();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (rank == 0 && tid == 0) {
+    const uint64_t a0 = desc(smem_u32(sa), 16, 1024, 2), b0 = desc(smem_u32(sb), 16, 1024, 2);
+    const uint32_t id = make_idesc(M, 256, true);
+    const long long c0 = clock64();
+    for (int i = 0; i < n; ++i) mma_bf16_2(tslot, a0 + 2 * (i & 3), b0 + 2 * (i & 3), id, 1u);
+    tc_commit2_mc(&bar, 0x3);
+    mbar_wait(&bar, 0);
+    cycles[blockIdx.x / 2] = clock64() - c0;
+  } else {
+    mbar_wait(&bar, 0);
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (tid < 32) {
+    tc_fence_after();
+    tmem_dealloc2(tslot, 512);
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) probe(int M, float* out) {
   __shared__ __align__(1024) uint8_t sa[128 * 128];
   __shared__ __align__(1024) uint8_t sb[128 * 128];
@@ -111,6 +148,17 @@ int main() {
         }
         printf("\n");
       }
+  }
+  long long* cyc;
+  cudaMalloc(&cyc, 74 * sizeof(long long));
+  static long long hc[74];
+  for (int M : {256, 128, 256, 128}) {
+    rate<<<148, 128>>>(M, 4096, cyc);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, cyc, sizeof(hc), cudaMemcpyDeviceToHost);
+    double avg = 0;
+    for (int i = 0; i < 74; ++i) avg += hc[i] / 74.0;
+    printf("rate M=%d N=256 K=16 cta_group::2, 4096 MMAs on 74 pairs: %.1f cycles per MMA\n", M, avg / 4096);
   }
   return 0;
 }
