@@ -28,6 +28,8 @@ for i, s in enumerate(segs):
             n = len(s[tag])
             tot = sum(r[2] for r in s[tag]) / n
             extra = f" sched {sum(r[4] for r in s[tag]) / n / tot:.3f}" if len(s[tag][0]) > 4 else ""
+            if len(s[tag][0]) > 5:
+                extra += f" issue {sum(r[5] for r in s[tag]) / n / tot:.3f}"
             out.append(f"{name} x{n} empty-wait {sum(r[3] for r in s[tag]) / n / tot:.3f}{extra}")
     if s["WPE"]:
         n = len(s["WPE"])
