@@ -993,12 +993,20 @@ bool launch_dense_gemm_tc(const bf16* A, int64_t M, int K, const bf16* W, int N,
 // ------------------------------------------------------------------ router on tcgen05
 // Logits tile = 128 tokens x E_pad experts (M=128, N=E_pad, K=H, 1-CTA) in TMEM, fp32;
 // the epilogue threads (one per token) do the top-k straight out of TMEM.
+// With E_pad >= 64 the router runs on CTA pairs (M = 256 tokens, each CTA loading half of W_r):
+// W_r is streamed through shared memory once per 256 tokens instead of once per 128, and each
+// CTA's accumulator still holds its 128 tokens x all E logits (the top-k epilogue is unchanged).
 bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E) {
+  static const bool pair_ok = env_int("ASYNCEP_ROUTER_PAIR", 1) != 0;
   rt.E_pad = (E + 15) / 16 * 16;
+  rt.pair = pair_ok && rt.E_pad >= 64 && rt.E_pad % 32 == 0;
   const uint64_t dims[3] = {(uint64_t)H, (uint64_t)E, 1};
   const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)H * 2 * E};
   const uint32_t box[3] = {BK, (uint32_t)rt.E_pad, 1};
+  const uint32_t box2[3] = {BK, (uint32_t)rt.E_pad / 2, 1};
   return encode_tmap(&rt.map_wr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box,
+                     CU_TENSOR_MAP_SWIZZLE_128B) &&
+         encode_tmap(&rt.map_wr2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box2,
                      CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
@@ -1023,6 +1031,13 @@ bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E
   a.norm_topk = norm_topk;
   a.ids = ids;
   a.w = w;
+  if (rt.pair) {
+    const int tiles = (int)((T + 2 * BM - 1) / (2 * BM)), units = num_sms / 2;
+    const int grid = 2 * (tiles < units ? tiles : units);
+    if (k <= 8) launch_mode<EPI_ROUTER, 2>(a, map_x, rt.map_wr2, map_x, grid, s);
+    else launch_mode<EPI_ROUTER16, 2>(a, map_x, rt.map_wr2, map_x, grid, s);
+    return true;
+  }
   const int tiles = (int)((T + BM - 1) / BM);
   if (k <= 8) launch_mode<EPI_ROUTER, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);
   else launch_mode<EPI_ROUTER16, 1>(a, map_x, rt.map_wr, map_x, tiles < num_sms ? tiles : num_sms, s);

@@ -23,8 +23,10 @@ void launch_router_simt(const bf16* x, const bf16* wr, int64_t T, int H, int E, 
 
 // Step (1) on tensor cores: tcgen05 logits tile (128 tokens x E) + top-k epilogue.
 struct RouterTc {
-  CUtensorMap map_wr; // [E, H] bf16 (3-D {H, E, 1}), box {64, E_pad, 1}, SW128 -- per layer
-  int E_pad;          // E rounded up to a multiple of 16 (MMA N)
+  CUtensorMap map_wr;  // [E, H] bf16 (3-D {H, E, 1}), box {64, E_pad, 1}, SW128 -- per layer
+  CUtensorMap map_wr2; // same, box {64, E_pad / 2, 1}: the half each CTA of a pair loads
+  int E_pad;           // E rounded up to a multiple of 16 (MMA N)
+  bool pair;           // E_pad >= 64 (and a multiple of 32): CTA-pair router, 256 tokens per tile
 };
 bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E);
 // x map is built per call (x is the caller's buffer): [T, H] bf16, box {64, 128}
