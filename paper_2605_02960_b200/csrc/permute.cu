@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
                                                                  int32_t* __restrict__ src_tok) {
   __shared__ int32_t warp_tot[SCAN_THREADS / 32];
   __shared__ int32_t tot[kMaxExperts];
+  __shared__ int32_t s_off[kMaxExperts + 1];  // padded row offsets (the last CTA's copy)
   __shared__ bool last;
   const int e = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   int32_t* row = bc + (int64_t)e * nblk;
@@ -78,22 +79,39 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
   __threadfence();
   for (int i = tid; i < E; i += SCAN_THREADS) tot[i] = ((volatile int32_t*)counts)[i];
   __syncthreads();
-  if (tid == 0) {
-    int32_t ts = 0;  // expert row ranges padded to kRowAlign: offsets[e] = kRowAlign * tile_start[e]
-    for (int i = 0; i < E; ++i) {
-      offsets[i] = ts * kRowAlign;
-      tile_start[i] = ts;
-      ts += (tot[i] + kRowAlign - 1) / kRowAlign;
-    }
-    offsets[E] = ts * kRowAlign;
-    tile_start[E] = ts;
-    *done = 0;  // re-arm for the next forward (stream-ordered)
+  // exclusive scan of the padded tile counts over experts (E <= kMaxExperts <= SCAN_THREADS):
+  // offsets[e] = kRowAlign * tile_start[e], expert row ranges padded to kRowAlign
+  static_assert(kMaxExperts <= SCAN_THREADS, "one thread per expert");
+  const int32_t tiles = tid < E ? (tot[tid] + kRowAlign - 1) / kRowAlign : 0;
+  int32_t inc = tiles;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
   }
+  __syncthreads();  // warp_tot is reused
+  if (lane == 31) warp_tot[wid] = inc;
   __syncthreads();
-  // padding rows of every expert gather token 0 (their GEMM rows are never read)
-  for (int i = 0; i < E; ++i) {
-    const int32_t b = offsets[i] + tot[i], end = offsets[i + 1];
-    for (int r = b + tid; r < end; r += SCAN_THREADS) src_tok[r] = 0;
+  int32_t base = 0;
+  for (int w = 0; w < wid; ++w) base += warp_tot[w];
+  const int32_t ts = base + inc - tiles;
+  if (tid < E) {
+    s_off[tid] = ts * kRowAlign;
+    offsets[tid] = ts * kRowAlign;
+    tile_start[tid] = ts;
+  }
+  if (tid == E - 1) {
+    s_off[E] = (ts + tiles) * kRowAlign;
+    offsets[E] = (ts + tiles) * kRowAlign;
+    tile_start[E] = ts + tiles;
+  }
+  if (tid == 0) *done = 0;  // re-arm for the next forward (stream-ordered)
+  __syncthreads();
+  // padding rows of every expert gather token 0 (their GEMM rows are never read): one warp per
+  // expert, offsets from shared memory
+  for (int i = wid; i < E; i += SCAN_THREADS / 32) {
+    const int32_t b = s_off[i] + tot[i], end = s_off[i + 1];
+    for (int r = b + lane; r < end; r += 32) src_tok[r] = 0;
   }
 }
 
@@ -105,34 +123,59 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
                                                            int32_t* __restrict__ dest,
                                                            int32_t* __restrict__ src_tok,
                                                            bf16* __restrict__ xperm) {
-  __shared__ int32_t cnt[kMaxExperts];
+  constexpr int NW = 8;                                        // warps per CTA (blockDim 256)
+  constexpr int MAXR = kPermTokensPerBlock * kMaxTopK / (NW * 32);  // rounds of 32 entries per warp
+  __shared__ int32_t wcnt[NW][kMaxExperts];  // per (warp, expert): entries, then the warp's base row
   __shared__ int32_t dst[kPermTokensPerBlock * kMaxTopK];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t t0 = (int64_t)blockIdx.x * kPermTokensPerBlock;
   const int tn = (int)min((int64_t)kPermTokensPerBlock, T - t0);
   const int n = tn * k;
-  for (int e = threadIdx.x; e < E; e += blockDim.x)
-    cnt[e] = offsets[e] + blk_base[(int64_t)e * nblk + blockIdx.x];  // first row of this chunk in e
+  // the chunk's entries in (t, j) order, split into NW contiguous ranges of whole 32-entry rounds
+  const int per = ((n + NW * 32 - 1) / (NW * 32)) * 32;
+  const int i0 = warp * per;
+  for (int e = threadIdx.x; e < NW * E; e += blockDim.x) wcnt[e / E][e % E] = 0;
   __syncthreads();
-  if (warp == 0) {
-    // entries in (t, j) order, 32 at a time; stable rank inside each expert
-    for (int c = 0; c < n; c += 32) {
-      const int i = c + lane;
-      const bool valid = i < n;
-      const int e = valid ? ids[t0 * k + i] : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, e);
-      const unsigned lt = (1u << lane) - 1u;
-      const int rank = __popc(peers & lt);
-      int d = 0;
-      if (valid) d = cnt[e] + rank;
-      __syncwarp();
-      if (valid && (peers & lt) == 0) cnt[e] += __popc(peers);
-      __syncwarp();
-      if (valid) {
-        dst[i] = d;
-        dest[t0 * k + i] = d;
-        src_tok[d] = (int32_t)(t0 + i / k);
-      }
+  const unsigned lt = (1u << lane) - 1u;
+  int ev[MAXR];
+  // pass 1: this warp's per-expert entry counts
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+    const int i = i0 + 32 * r + lane;
+    const bool valid = 32 * r < per && i < n;
+    ev[r] = valid ? ids[t0 * k + i] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, ev[r]);
+    if (valid && (peers & lt) == 0) wcnt[warp][ev[r]] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per expert: chunk base (offsets + the scan's chunk base), then exclusive prefix over the warps
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int32_t run = offsets[e] + blk_base[(int64_t)e * nblk + blockIdx.x];  // first row of this chunk in e
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      const int32_t c = wcnt[w][e];
+      wcnt[w][e] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // pass 2: stable rank inside each expert = warp base + rank among this warp's earlier entries
+#pragma unroll
+  for (int r = 0; r < MAXR; ++r) {
+    const int i = i0 + 32 * r + lane;
+    const bool valid = 32 * r < per && i < n;
+    const int e = ev[r];
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    int d = 0;
+    if (valid) d = wcnt[warp][e] + __popc(peers & lt);
+    __syncwarp();
+    if (valid && (peers & lt) == 0) wcnt[warp][e] += __popc(peers);
+    __syncwarp();
+    if (valid) {
+      dst[i] = d;
+      dest[t0 * k + i] = d;
+      src_tok[d] = (int32_t)(t0 + i / k);
     }
   }
   if (xperm == nullptr) return;
