@@ -9,6 +9,8 @@
 //             __match_any_sync + popc), then one warp per token copies x_t (16-B vectors)
 //             to its k destination rows of X_perm.
 // Pure integer work + data movement: the result is bit-exact and deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -241,6 +243,39 @@ __global__ void __launch_bounds__(256) perm_quant_kernel(const bf16* __restrict_
   if (lane < k) xscale[d[lane]] = sc;
 }
 
+// Token-major form of perm_quant_kernel for the fused dispatch (x_q row t = token t): the same
+// rule, with no destination list, so a warp needs few registers and 64 warps fit on an SM.
+__global__ void __launch_bounds__(256, 8) quant_tokens_kernel(const bf16* __restrict__ x, int64_t T, int H,
+                                                               uint8_t* __restrict__ xq, float* __restrict__ xscale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+  const int nv = H / 8;
+  float amax = 0.f;
+  for (int v = lane; v < nv; v += 32) {
+    const uint4 u = src[v];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) amax = fmaxf(amax, fmaxf(fabsf(bf16_lo(w[q])), fabsf(bf16_hi(w[q]))));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float inv = amax > 0.f ? 448.0f / amax : 0.f;
+  uint2* dst = reinterpret_cast<uint2*>(xq + t * H);
+  for (int v = lane; v < nv; v += 32) {
+    const uint4 u = src[v];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint2 o;
+    o.x = (uint32_t)e4m3x2(bf16_lo(w[0]) * inv, bf16_hi(w[0]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[1]) * inv, bf16_hi(w[1]) * inv) << 16);
+    o.y = (uint32_t)e4m3x2(bf16_lo(w[2]) * inv, bf16_hi(w[2]) * inv) |
+          ((uint32_t)e4m3x2(bf16_lo(w[3]) * inv, bf16_hi(w[3]) * inv) << 16);
+    dst[v] = o;
+  }
+  if (lane == 0) xscale[t] = amax / 448.0f;
+}
+
 // FP8 intermediate: act (bf16, written by the GEMM1 epilogue together with the row amax of
 // |act| in act_amax, as fp32 bits) -> e4m3 codes + per-row scale, same rule as above.
 __global__ void __launch_bounds__(256) act_quant_kernel(const bf16* __restrict__ act, uint32_t* __restrict__ act_amax,
@@ -273,7 +308,9 @@ __global__ void __launch_bounds__(256) act_quant_kernel(const bf16* __restrict__
 void launch_perm_quant(const bf16* x, const int32_t* dest, int64_t T, int H, int k, uint8_t* xq, float* xscale,
                        cudaStream_t s) {
   if (T <= 0) return;
-  perm_quant_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, dest, T, H, k, xq, xscale);
+  static const bool tok_kernel = getenv("ASYNCEP_QUANT_TOKENS") == nullptr || atoi(getenv("ASYNCEP_QUANT_TOKENS")) != 0;
+  if (!dest && tok_kernel) quant_tokens_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, T, H, xq, xscale);
+  else perm_quant_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, dest, T, H, k, xq, xscale);
 }
 
 void launch_act_quant(const bf16* act, uint32_t* act_amax, const int32_t* offsets, int E, int64_t R, int h,
