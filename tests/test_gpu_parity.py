@@ -262,3 +262,19 @@ def test_qwen3_235b_eight_layer_stack_sampled(fp8):
         rep = check_layer(xl, wr, g, u, d, wl.k, outs[l], orc["ids"], orc["w"], None, tol=6e-2 if fp8 else 2e-2)
         print(l, rep)
         del wr, g, u, d
+
+
+@pytest.mark.parametrize("E,k", [(64, 12), (96, 8), (80, 8)], ids=["pair_router_top12", "pair_router_E96",
+                                                                   "cta_router_E80"])
+def test_router_tile_shapes(E, k):
+    """Router paths: CTA pairs with the 16-wide top-k epilogue (E=64, k=12), pairs with N = 96, and the
+    1-CTA fallback (E_pad = 80 is not a multiple of 32); 700 tokens = 2 full 256-token pair tiles + a
+    ragged one."""
+    wl = Workload(L=1, E=E, k=k, H=512, h=256, seed=13)
+    st = wl.stack(max_tokens=700)
+    x = wl.tokens(700)
+    y, ids, w, counts = run_layer(wl, st, 0, x)
+    wr, g, u, d = wl.host_layer(0)
+    rep = check_layer(f32(x), wr, g, u, d, wl.k, y, ids, w, counts)
+    assert counts.sum() == 700 * k
+    print(rep)
