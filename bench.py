@@ -458,7 +458,9 @@ def main():
                                   (f", shards offloaded to pinned host memory, {args.offload}-deep device window "
                                    "(NEXT-2)" if args.offload else ""),
                    "gather": gather_mode,
-                   "l2": "inputs larger than L2 (38.7 GB weights, 268 MB activations/layer); no flush"},
+                   "l2": (f"inputs larger than L2 ({L * E_ * 3 * H_ * h_ * (1 if args.fp8 else 2) / 1e9:.1f} GB expert "
+                          f"weights + {T * K_ * H_ * 2 / 1e6:.0f} MB Y_perm per layer streamed each step, "
+                          f"{T * H_ * 2 / 1e6:.0f} MB token activations); no flush")},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,
         "mfu": {"vs_spec_dense": mfu_flops / spec, "spec_dense_flops": spec,
