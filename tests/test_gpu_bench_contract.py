@@ -1,0 +1,45 @@
+"""bench.py's JSON line keeps the driver's contract (keys, types, consistency), on a small run."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run_bench(*args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]  # exactly one JSON line
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("fp8", [False, True], ids=["bf16", "fp8"])
+def test_bench_line_contract(fp8):
+    d = run_bench("--layers", "2", "--tokens", "4096", "--steps", "2", "--warmup", "3", "--no-cpu-baseline",
+                  *(["--fp8"] if fp8 else []))
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 2 and d["warmup"] == 3
+    assert d["value"] > 0 and d["higher_is_better"] is True and d["scaling"] == "weak"
+    assert d["dtype"] == ("fp8_e4m3" if fp8 else "bf16") and d["data"] == "synthetic"
+    assert "workload" in d["config"] and d["config"]["tokens_per_gpu"] == 4096
+    # value = tokens of the timed steps / device time
+    assert abs(d["value"] - 4096 * 1e3 / d["ms_per_step"]) / d["value"] < 1e-6
+    rf = d["roofline"]
+    assert rf["bound"] == "tensor" and rf["unit"] == "TFLOP/s" and rf["peak"] > 0
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-9 and 0 < rf["frac"] < 1.5
+    ck = d["clocks"]
+    assert ck["sm_max_mhz"] > 0 and isinstance(ck["reasons"], list)
+    e = d["e2e"]
+    assert e["value"] > 0 and e["unit"] == d["unit"]
+    assert e["h2d_bytes_per_step"] == 4096 * 4096 * 2 and e["d2h_bytes_per_step"] == 4096 * 4096 * 2
+    # our kernels launched inside the timed region: 7 per BF16 layer, 9 per FP8 layer
+    assert d["gpu_launches"] == 2 * 2 * (9 if fp8 else 7)
