@@ -182,8 +182,8 @@ ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void*
 /* The gather's transport primitive, exposed for measurement: a device-to-device (or NVLink
  * peer) copy of `bytes` on `stream` by a copy kernel of small CTAs that co-reside with the
  * persistent GEMM CTAs (the driver's D2D memcpy and NCCL kernels cannot start beside them).
- * ASYNCEP_GATHER_COPY=ce selects cudaMemcpyBatchAsync with the copy-engine hint, =memcpy
- * cudaMemcpyAsync. */
+ * ASYNCEP_GATHER_COPY=memcpy (alias ce) selects one cudaMemcpyAsync per copy instead (copy
+ * engines for peer pointers on another GPU). */
 ASYNCEP_API asyncep_status asyncep_gather_copy(void* dst, const void* src, size_t bytes, void* stream);
 
 /*

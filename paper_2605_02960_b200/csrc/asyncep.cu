@@ -32,15 +32,14 @@ asyncep_status fail(asyncep_status st, const char* fmt, ...) {
 }
 
 // The gather's transport primitive.  Default: aep::launch_gather_copy, a copy kernel whose small
-// CTAs co-reside with the persistent GEMM CTAs (measured: the driver's D2D memcpy -- also with the
-// copy-engine hint -- stalls for the whole duration of a persistent GEMM, profiles/copy_timeline.py).
-// ASYNCEP_GATHER_COPY=ce: cudaMemcpyBatchAsync with cudaMemcpyFlagPreferOverlapWithCompute;
-// =memcpy: cudaMemcpyAsync.
+// CTAs co-reside with the persistent GEMM CTAs (measured: the driver's same-device D2D memcpy
+// stalls for the whole duration of a persistent GEMM, profiles/copy_timeline.py).
+// ASYNCEP_GATHER_COPY=memcpy (alias: ce): one cudaMemcpyAsync per copy -- for IPC-mapped peer
+// pointers on another GPU the driver moves the bytes with the copy engines, no SMs.
 cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0) {
   static const int mode = [] {
     const char* e = getenv("ASYNCEP_GATHER_COPY");
-    if (e && !strcmp(e, "ce")) return 1;
-    if (e && !strcmp(e, "memcpy")) return 2;
+    if (e && (!strcmp(e, "ce") || !strcmp(e, "memcpy"))) return 1;
     return 0;
   }();
   static const int ctas = [] {  // two 128-thread CTAs per SM: both fit beside any GEMM CTA (<= 224
@@ -54,20 +53,7 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
     return cudaGetLastError();
   }
   if (min_ns) aep::launch_spin_ns(min_ns, st);  // other transports: link time, then the copy
-  if (mode == 1) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    void* dsts[1] = {dst};
-    void* srcs[1] = {const_cast<void*>(src)};
-    size_t sizes[1] = {n};
-    size_t idx[1] = {0};
-    size_t fail_idx = 0;
-    if (cudaMemcpyBatchAsync(dsts, srcs, sizes, 1, &attr, idx, 1, &fail_idx, st) == cudaSuccess)
-      return cudaSuccess;
-    cudaGetLastError();  // clear, fall back
-  }
-  return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st);
+  return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st);
 }
 
 #define CUDA_TRY(expr)                                                                              \
