@@ -59,6 +59,8 @@ def _load():
             lib.oracle_e4m3_encode_fast.restype = ctypes.c_uint8
             lib.oracle_e4m3_decode_array.argtypes = [P, I64, P]
             lib.oracle_e4m3_decode_array.restype = None
+            lib.oracle_to_bf16_array.argtypes = [P, I64, P]
+            lib.oracle_to_bf16_array.restype = None
             lib.oracle_eq1_threshold.argtypes = [D, D, D]
             lib.oracle_eq1_threshold.restype = D
             lib.oracle_saturation_T.argtypes = [I32, I32, I32, I32, D, I32, D, D, D, P, P]
@@ -163,6 +165,15 @@ def e4m3_decode(q) -> np.ndarray:
     q = np.ascontiguousarray(q, dtype=np.uint8)
     out = np.empty(q.shape, np.float32)
     _load().oracle_e4m3_decode_array(_ptr(q), q.size, _ptr(out))
+    return out
+
+
+def to_bf16(v) -> np.ndarray:
+    """fp64 values -> fp32 -> bf16 round-to-nearest-even (as float32 arrays): the rounding the
+    act_quant emulation applies to the intermediate (R5)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.empty(v.shape, np.float32)
+    _load().oracle_to_bf16_array(_ptr(v), v.size, _ptr(out))
     return out
 
 

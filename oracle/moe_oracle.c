@@ -391,6 +391,11 @@ static float to_bf16(double v) {
     return f;
 }
 
+/* Exported for the pins (tests/test_oracle_pins.py): to_bf16 over an array. */
+void oracle_to_bf16_array(const double *v, int64_t n, float *out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = to_bf16(v[i]);
+}
+
 /*
  * FP8 activation-quantisation emulation (reading R6, the rule the CUDA path applies):
  *   amax = max_i |v_i| (fp32); inv = 448 / amax (fp32); q_i = RNE_satfinite_e4m3(fp32(v_i * inv));

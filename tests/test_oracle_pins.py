@@ -285,3 +285,87 @@ def test_act_quant_emulation_of_the_input_row():
         np.testing.assert_allclose(r["y"][t], q * float(sc) * r["w"][t].sum(), rtol=1e-14, atol=0)
     # quantisation error is bounded by half an e4m3 ulp (2^-4 relative) of each element
     assert np.all(np.abs(r["y"] - x) <= np.abs(x) * 2.0 ** -4 + 2.0 ** -9 * np.abs(x).max(1, keepdims=True))
+
+
+# ------------------------------------------------------------------ FP8 emulation branch (R5, R6)
+
+def _bf16_nearest(v64: float) -> float:
+    """bf16 RNE of fp32(v) by choosing between the two neighbouring bf16 values (no bit trick):
+    the candidates are fp32(v) truncated to 16 bits and the next bf16 away from zero; the nearer
+    wins, an exact tie goes to the one with an even last mantissa bit."""
+    f = np.float32(v64)
+    if not np.isfinite(f):
+        return float(f)
+    b = np.array([f], np.float32).view(np.uint32)[0]
+    lo_bits = np.uint32(b & np.uint32(0xFFFF0000))
+    hi_bits = np.uint32(lo_bits + np.uint32(0x10000))
+    lo = np.array([lo_bits], np.uint32).view(np.float32)[0]
+    hi = np.array([hi_bits], np.uint32).view(np.float32)[0]
+    dlo = abs(float(f) - float(lo))
+    dhi = abs(float(hi) - float(f)) if np.isfinite(hi) else abs((2.0 ** 128) * math.copysign(1, f) - float(f))
+    if dlo < dhi:
+        return float(lo)
+    if dhi < dlo:
+        return float(hi)
+    return float(lo) if ((int(lo_bits) >> 16) & 1) == 0 else float(hi)
+
+
+def test_to_bf16_rounding_points():
+    """The intermediate's bf16 rounding (R5): RNE at ties, sign of zero, inf/NaN pass through,
+    overflow past the largest bf16 goes to inf; random values against the nearest-neighbour rule."""
+    ulp = 2.0 ** -7
+    cases = {1.0 + ulp / 2: 1.0,                      # tie -> even (mantissa 0)
+             1.0 + 3 * ulp / 2: 1.0 + 2 * ulp,        # tie -> even (up)
+             1.0 + ulp / 2 + 2.0 ** -20: 1.0 + ulp,   # just above the tie -> up
+             -(1.0 + ulp / 2): -1.0, 0.0: 0.0, 2.0 ** -133: 2.0 ** -133}
+    for v, want in cases.items():
+        assert float(oracle.to_bf16([v])[0]) == want, v
+    z = oracle.to_bf16([0.0, -0.0])
+    assert not np.signbit(z[0]) and np.signbit(z[1])
+    sp = oracle.to_bf16([np.inf, -np.inf, np.nan, 3.4e38, -3.4e38])
+    assert sp[0] == np.inf and sp[1] == -np.inf and np.isnan(sp[2])
+    assert sp[3] == np.inf and sp[4] == -np.inf             # 3.4e38 rounds past 0x7F7F -> inf
+    assert float(oracle.to_bf16([3.389e38])[0]) == float(np.array([0x7F7F0000], np.uint32).view(np.float32)[0])
+    rng = np.random.default_rng(5)
+    v = np.concatenate([rng.standard_normal(4000) * 10.0 ** rng.integers(-30, 30, 4000), rng.standard_normal(500)])
+    got = oracle.to_bf16(v)
+    want = np.array([_bf16_nearest(a) for a in v], np.float32)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def _q_row(v32):
+    """R6 per-row e4m3 quantisation with the brute-force nearest-code encoder, numpy fp32."""
+    v32 = np.asarray(v32, np.float32)
+    amax = np.float32(np.abs(v32).max())
+    if amax == 0:
+        return np.zeros(v32.shape)
+    inv = np.float32(448.0) / amax
+    sc = amax / np.float32(448.0)
+    return np.array([oracle.e4m3_decode_one(oracle.e4m3_encode_one(float(np.float32(a * inv)))) for a in v32]) * float(sc)
+
+
+@pytest.mark.parametrize("E,k", [(1, 1), (4, 2)])
+def test_act_quant_full_expert_path(E, k):
+    """act_quant with real experts (the branch identity experts never reach): per token,
+    x -> per-token e4m3, g/u by numpy matmul, silu(g)*u, -> fp32 -> bf16 (nearest-neighbour rule),
+    -> per-row e4m3, W_down, weighted sum with the oracle's routing weights.  E=1, k=1 reduces to
+    one dense FP8-emulated SwiGLU FFN (weight 1)."""
+    T, H, h = 24, 64, 96
+    x, wr, wg, wu, wd = _layer(T=T, H=H, E=E, k=k, h=h, seed=7)
+    r = oracle.moe_layer(x, wr, wg, wu, wd, k, residual=False, act_quant=True)
+    if E == 1:
+        assert np.all(r["w"] == 1.0)
+    for t in range(T):
+        xq = _q_row(x[t])
+        y = np.zeros(H)
+        for j in range(k):
+            e = int(r["ids"][t, j])
+            g = wg[e].astype(np.float64) @ xq
+            u = wu[e].astype(np.float64) @ xq
+            a = g / (1.0 + np.exp(-g)) * u
+            ab = np.array([_bf16_nearest(v) for v in a], np.float32)
+            y += r["w"][t, j] * (wd[e].astype(np.float64) @ _q_row(ab))
+        np.testing.assert_allclose(r["y"][t], y, rtol=1e-12, atol=1e-12 * np.abs(y).max())
+    # the order matters: quantising before the bf16 rounding (or skipping it) gives another answer
+    plain = oracle.moe_layer(x, wr, wg, wu, wd, k, residual=False, act_quant=False)["y"]
+    assert np.abs(plain - r["y"]).max() > 1e-4 * np.abs(plain).max()
