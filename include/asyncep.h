@@ -281,6 +281,19 @@ ASYNCEP_API asyncep_status asyncep_calibrated_T(double gamma, double t_e, double
                                                 double* flops_out);
 
 /*
+ * NEXT-1 profile-run calibration, App. B.4, end to end: from the last
+ * num_layers recorded forwards of `ctx` (one profile pass of the stack at n_ref tokens per GPU,
+ * ASYNCEP_FLAG_STAGE_TIMING), t_c = the wall time of layer 0 (resident: pure compute) and
+ * t_e = the max wall time of the layers >= 1 (each max(compute, transfer)); f_tok = 2HE + 6kHh
+ * (router + experts, per token per layer), C_dummy = f_tok * n_ref, and T by
+ * asyncep_calibrated_T (gamma <= 0: the config's gamma).  Outputs: T in FLOPs and in tokens per
+ * GPU (T / f_tok), t_c and t_e in ms (each nullable).  Synchronises on the recorded events.
+ * Errors: INVALID_ARG (no timing flag, fewer than num_layers forwards recorded, layer 0 absent).
+ */
+ASYNCEP_API asyncep_status asyncep_calibrate_T(asyncep_ctx* ctx, double gamma, int64_t n_ref, double* flops_out,
+                                               double* tokens_out, double* t_c_out, double* t_e_out);
+
+/*
  * ---- NEXT-4: saturation-bounded admission (frontend consumer of T; host only) ----
  * Algorithm 1 (App. A) with the Eq. 2 cost and the load
  * band [T, T + Delta_last].  Functional forms of Eq. 2 (reading R18):
@@ -353,14 +366,15 @@ ASYNCEP_API size_t asyncep_attn_workspace_size(const asyncep_attn_config* cfg);
  *  head, prompt b's keys at columns [vt_cu[b], vt_cu[b] + len_b) (vt_cu [B+1] int32 device,
  *  every vt_cu[b] a multiple of 8 -- the TMA start along the contiguous dimension must be
  *  16-B aligned; columns outside the prompts must hold finite values); ldv % 8 == 0;
- *  o [T, Hq, d] bf16 output.
+ *  o [T, Hq, d] bf16 output;  sched: one int32 of caller-owned device memory for the kernel's
+ *  dynamic work-item scheduler (zeroed by the call on `stream`; concurrent calls need their own).
  * Causal within each prompt.  T == 0 is a no-op.  Errors: INVALID_ARG (d != 128, Hq % Hkv,
  * alignment), CUDA.
  */
 ASYNCEP_API asyncep_status asyncep_attention(const asyncep_attn_config* cfg, const void* q, const void* k,
                                              const void* vt, int64_t ldv, const int32_t* vt_cu,
                                              const int32_t* cu_seqlens, int32_t B, int64_t T, void* o,
-                                             void* stream);
+                                             int32_t* sched, void* stream);
 
 /*
  * One full attention layer (the formulas above), on `stream`.

@@ -92,6 +92,8 @@ def lib() -> ctypes.CDLL:
             "asyncep_kernel_launches": ([P], I64),
             "asyncep_forward_times": ([P, ctypes.POINTER(D), ctypes.POINTER(I32), I32, ctypes.POINTER(I32)], I32),
             "asyncep_calibrated_T": ([D, D, D, D, ctypes.POINTER(D)], I32),
+            "asyncep_calibrate_T": ([P, D, I64, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(D),
+                                     ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
             "asyncep_set_peer_shards": ([P, P], I32),
             "asyncep_gather_copy": ([P, P, SZ, P], I32),
@@ -109,7 +111,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_ep_workspace_size": ([CP, I64], SZ),
             "asyncep_ep_forward": ([P, I32, P, I64, P, P, P, I64], I32),
             "asyncep_attn_workspace_size": ([ctypes.POINTER(AttnConfig)], SZ),
-            "asyncep_attention": ([ctypes.POINTER(AttnConfig), P, P, P, I64, P, P, I32, I64, P, P], I32),
+            "asyncep_attention": ([ctypes.POINTER(AttnConfig), P, P, P, I64, P, P, I32, I64, P, P, P], I32),
             "asyncep_attn_layer": ([ctypes.POINTER(AttnConfig), P, I64, P, I32, P, P, P, P, P, P, P, P, P, SZ, P],
                                    I32),
             "asyncep_destroy": ([P], I32),
@@ -311,6 +313,13 @@ def asyncep_calibrated_T(gamma: float, t_e: float, t_c: float, c_dummy: float) -
     return out.value
 
 
+def asyncep_calibrate_T(ctx: Context, gamma: float, n_ref: int):
+    """NEXT-1 (App. B.4) from the last profile pass: -> dict(T_flops, T_tokens, t_c_ms, t_e_ms)."""
+    out = [ctypes.c_double() for _ in range(4)]
+    _check(lib().asyncep_calibrate_T(ctx.handle, float(gamma), int(n_ref), *[ctypes.byref(o) for o in out]))
+    return dict(zip(("T_flops", "T_tokens", "t_c_ms", "t_e_ms"), (o.value for o in out)))
+
+
 def asyncep_reset_stage_times(ctx: Context) -> None:
     _check(lib().asyncep_reset_stage_times(ctx.handle))
 
@@ -344,12 +353,14 @@ def asyncep_attn_workspace_size(cfg: AttnConfig) -> int:
     return n
 
 
-def asyncep_attention(cfg: AttnConfig, q, k, vt, ldv: int, vt_cu, cu_seqlens, o, stream=None) -> None:
+def asyncep_attention(cfg: AttnConfig, q, k, vt, ldv: int, vt_cu, cu_seqlens, o, stream=None, sched=None) -> None:
     """Causal GQA attention core: q [T,Hq,d], k [T,Hkv,d], vt [Hkv,d,ldv] with prompt b at columns
-    vt_cu[b] (multiples of 8), cu_seqlens int32 [B+1]."""
+    vt_cu[b] (multiples of 8), cu_seqlens int32 [B+1]; sched: int32 device counter (one per call)."""
     T = q.shape[0]
+    if sched is None:
+        sched = torch.empty(1, dtype=torch.int32, device=q.device)
     _check(lib().asyncep_attention(ctypes.byref(cfg), _p(q), _p(k), _p(vt), ldv, _p(vt_cu), _p(cu_seqlens),
-                                   cu_seqlens.shape[0] - 1, T, _p(o),
+                                   cu_seqlens.shape[0] - 1, T, _p(o), _p(sched),
                                    _stream(stream or torch.cuda.current_stream())))
 
 

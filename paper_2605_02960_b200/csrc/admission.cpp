@@ -25,7 +25,12 @@ struct asyncep_router {
   std::vector<std::unordered_set<uint64_t>> committed, pending;
 };
 
+namespace aep {
+asyncep_status set_error(asyncep_status st, const char* msg);  // asyncep.cu: asyncep_last_error()
+}
+
 namespace {
+asyncep_status bad(const char* msg) { return aep::set_error(ASYNCEP_ERR_INVALID_ARG, msg); }
 double c_pfx(const asyncep_router_config& c, double n) { return n * c.f_tok + 2.0 * n * n * c.attn_hl; }
 double c_sfx(const asyncep_router_config& c, double S, double P) {
   return S * c.f_tok + 2.0 * S * S * c.attn_hl + 4.0 * S * P * c.attn_hl;
@@ -45,7 +50,7 @@ double asyncep_cost_delta(const asyncep_router_config* c, int64_t P, int64_t M, 
 asyncep_status asyncep_router_create(const asyncep_router_config* cfg, asyncep_router** out) {
   if (!cfg || !out || cfg->num_gpus <= 0 || cfg->block_size <= 0 || !(cfg->f_tok > 0) || cfg->attn_hl < 0 ||
       !(cfg->T_flops > 0))
-    return ASYNCEP_ERR_INVALID_ARG;
+    return bad("asyncep_router_create: need num_gpus > 0, block_size > 0, f_tok > 0, attn_hl >= 0, T_flops > 0");
   asyncep_router* r = new asyncep_router();
   r->cfg = *cfg;
   r->load.assign(cfg->num_gpus, 0.0);
@@ -61,13 +66,13 @@ asyncep_status asyncep_router_destroy(asyncep_router* r) {
 }
 
 asyncep_status asyncep_router_set_T(asyncep_router* r, double T_flops) {
-  if (!r || !(T_flops > 0)) return ASYNCEP_ERR_INVALID_ARG;
+  if (!r || !(T_flops > 0)) return bad("asyncep_router_set_T: null router or T_flops <= 0");
   r->cfg.T_flops = T_flops;
   return ASYNCEP_OK;
 }
 
 asyncep_status asyncep_router_loads(const asyncep_router* r, double* loads_out) {
-  if (!r || !loads_out) return ASYNCEP_ERR_INVALID_ARG;
+  if (!r || !loads_out) return bad("asyncep_router_loads: null argument");
   for (size_t i = 0; i < r->load.size(); ++i) loads_out[i] = r->load[i];
   return ASYNCEP_OK;
 }
@@ -77,7 +82,14 @@ asyncep_status asyncep_router_schedule_round(asyncep_router* r, int32_t reset_lo
                                              const int64_t* prefix_len, const int64_t* suffix_len, int32_t* gpu_out,
                                              double* delta_out, int64_t* admitted_out) {
   if (!r || n_req < 0 || (n_req > 0 && (!chain_off || !prefix_len || !suffix_len || !gpu_out)))
-    return ASYNCEP_ERR_INVALID_ARG;
+    return bad("asyncep_router_schedule_round: null argument or n_req < 0");
+  // validate every request before any state changes, so a malformed round changes nothing
+  for (int64_t q = 0; q < n_req; ++q) {
+    if (chain_off[q + 1] < chain_off[q] || chain_off[q] < 0 || prefix_len[q] < 0 || suffix_len[q] < 0)
+      return bad("asyncep_router_schedule_round: request with chain_off[q+1] < chain_off[q] or negative length");
+  }
+  if (n_req > 0 && chain_off[n_req] > chain_off[0] && !hashes)
+    return bad("asyncep_router_schedule_round: hashes is NULL with a non-empty block chain");
   const int N = r->cfg.num_gpus;
   const double T = r->cfg.T_flops;
   if (reset_loads)
@@ -91,7 +103,6 @@ asyncep_status asyncep_router_schedule_round(asyncep_router* r, int32_t reset_lo
     if (delta_out) delta_out[q] = 0.0;
     if (n_active == 0) continue;  // requests stay queued for the next round
     const int64_t b0 = chain_off[q], b1 = chain_off[q + 1];
-    if (b1 < b0 || prefix_len[q] < 0 || suffix_len[q] < 0) return ASYNCEP_ERR_INVALID_ARG;
     int best = -1;
     int64_t best_m = -1;
     for (int i = 0; i < N; ++i) {
@@ -122,7 +133,8 @@ asyncep_status asyncep_router_schedule_round(asyncep_router* r, int32_t reset_lo
 }
 
 asyncep_status asyncep_router_blocks_stored(asyncep_router* r, int32_t gpu, const uint64_t* hashes, int64_t n) {
-  if (!r || gpu < 0 || gpu >= r->cfg.num_gpus || n < 0 || (n > 0 && !hashes)) return ASYNCEP_ERR_INVALID_ARG;
+  if (!r || gpu < 0 || gpu >= r->cfg.num_gpus || n < 0 || (n > 0 && !hashes))
+    return bad("asyncep_router_blocks_stored: bad router / gpu / hashes");
   for (int64_t i = 0; i < n; ++i) {  // pending -> committed (App. B.2 promotion)
     r->pending[gpu].erase(hashes[i]);
     r->committed[gpu].insert(hashes[i]);
@@ -131,7 +143,8 @@ asyncep_status asyncep_router_blocks_stored(asyncep_router* r, int32_t gpu, cons
 }
 
 asyncep_status asyncep_router_progress(asyncep_router* r, int32_t gpu, int64_t tokens) {
-  if (!r || gpu < 0 || gpu >= r->cfg.num_gpus || tokens < 0) return ASYNCEP_ERR_INVALID_ARG;
+  if (!r || gpu < 0 || gpu >= r->cfg.num_gpus || tokens < 0)
+    return bad("asyncep_router_progress: bad router / gpu / tokens");
   // App. B.3: L_i <- max(0, L_i - tokens * f_tok)
   r->load[gpu] = std::max(0.0, r->load[gpu] - (double)tokens * r->cfg.f_tok);
   return ASYNCEP_OK;

@@ -56,6 +56,18 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
   return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st);
 }
 
+}  // namespace
+
+namespace aep {
+// error reporting for the other translation units of the library (admission.cpp)
+asyncep_status set_error(asyncep_status st, const char* msg) {
+  g_last_error = msg;
+  return st;
+}
+}  // namespace aep
+
+namespace {
+
 #define CUDA_TRY(expr)                                                                              \
   do {                                                                                              \
     cudaError_t _e = (expr);                                                                        \
@@ -205,11 +217,12 @@ struct asyncep_ctx {
   aep::GemmMaps slot_maps[2];
   std::vector<aep::RouterTc> router_maps;  // per layer
   // stage timing
-  std::vector<cudaEvent_t> ev_pool;
-  int ev_used = 0;  // forwards recorded since the last flush
+  std::vector<cudaEvent_t> ev_pool;  // ring of kMaxPendingFwd forwards x kEventsPerFwd events
+  int ev_head = 0;  // ring slot of the oldest pending (recorded, not yet read) forward
+  int ev_used = 0;  // pending forwards
   double stage_ms[kStages] = {0};
   int64_t fwd_count = 0;
-  std::vector<int32_t> ev_layer;                 // layer of each pending recorded forward
+  std::vector<int32_t> ev_layer;                 // layer of the forward in each ring slot
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   int64_t launches = 0;
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
@@ -234,11 +247,22 @@ bool layer_resident(const asyncep_ctx* c, int l) {
   return c->cfg.world_size == 1 || (l == 0 && c->cfg.replicate_layer0);
 }
 
-asyncep_status flush_timing(asyncep_ctx* c) {
-  if (c->ev_used == 0) return ASYNCEP_OK;
-  CUDA_TRY(cudaEventSynchronize(c->ev_pool[(size_t)c->ev_used * kEventsPerFwd - 1]));
-  for (int f = 0; f < c->ev_used; ++f) {
-    cudaEvent_t* e = &c->ev_pool[(size_t)f * kEventsPerFwd];
+// Reads the pending forwards' events oldest first.  blocking = false (the forward path when the
+// ring is full): wait only for the OLDEST forward to finish, then read every forward that has
+// already completed -- the host never drains the GPU queue, it just stays <= kMaxPendingFwd
+// forwards ahead.  blocking = true (the query calls): wait for all of them.
+asyncep_status flush_timing(asyncep_ctx* c, bool blocking = true) {
+  bool first = true;
+  while (c->ev_used > 0) {
+    cudaEvent_t* e = &c->ev_pool[(size_t)c->ev_head * kEventsPerFwd];
+    if (blocking || first) {
+      CUDA_TRY(cudaEventSynchronize(e[kStages]));
+    } else {
+      const cudaError_t q = cudaEventQuery(e[kStages]);
+      if (q == cudaErrorNotReady) break;
+      CUDA_TRY(q);
+    }
+    first = false;
     for (int s = 0; s < kStages; ++s) {
       float ms = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&ms, e[s], e[s + 1]));
@@ -246,12 +270,12 @@ asyncep_status flush_timing(asyncep_ctx* c) {
     }
     float tot = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&tot, e[0], e[kStages]));
-    c->recent.emplace_back(c->ev_layer[f], (double)tot);
+    c->recent.emplace_back(c->ev_layer[(size_t)c->ev_head], (double)tot);
     if (c->recent.size() > 4096) c->recent.erase(c->recent.begin(), c->recent.begin() + 2048);
+    c->ev_head = (c->ev_head + 1) % kMaxPendingFwd;
+    --c->ev_used;
+    ++c->fwd_count;
   }
-  c->ev_layer.clear();
-  c->fwd_count += c->ev_used;
-  c->ev_used = 0;
   return ASYNCEP_OK;
 }
 
@@ -595,16 +619,18 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   CUDA_TRY(cudaMemsetAsync(sched, 0, 16, st));
   if (timing) {
     if (c->ev_used == kMaxPendingFwd) {
-      asyncep_status fs = flush_timing(c);
+      asyncep_status fs = flush_timing(c, /*blocking=*/false);
       if (fs) return fs;
     }
     if (c->ev_pool.empty()) {
       c->ev_pool.resize((size_t)kMaxPendingFwd * kEventsPerFwd);
       for (auto& e : c->ev_pool) CUDA_TRY(cudaEventCreate(&e));
+      c->ev_layer.assign(kMaxPendingFwd, -1);
     }
-    ev = &c->ev_pool[(size_t)c->ev_used * kEventsPerFwd];
+    const int slot = (c->ev_head + c->ev_used) % kMaxPendingFwd;
+    ev = &c->ev_pool[(size_t)slot * kEventsPerFwd];
     ++c->ev_used;
-    c->ev_layer.push_back(layer);
+    c->ev_layer[(size_t)slot] = layer;
     CUDA_TRY(cudaEventRecord(ev[0], st));
   }
   // (1) router GEMM + softmax + top-k
@@ -954,6 +980,40 @@ asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double
   return ASYNCEP_OK;
 }
 
+asyncep_status asyncep_calibrate_T(asyncep_ctx* c, double gamma, int64_t n_ref, double* flops_out,
+                                   double* tokens_out, double* t_c_out, double* t_e_out) {
+  if (!c || n_ref <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "calibrate_T: null ctx or n_ref <= 0");
+  if (!(c->cfg.flags & ASYNCEP_FLAG_STAGE_TIMING))
+    return fail(ASYNCEP_ERR_INVALID_ARG, "calibrate_T: the context was created without ASYNCEP_FLAG_STAGE_TIMING");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  const int L = c->cfg.num_layers;
+  if ((int)c->recent.size() < L)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "calibrate_T: %d forwards recorded, the profile pass needs %d",
+                (int)c->recent.size(), L);
+  // the profile pass = the last L forwards: t_c = the resident layer 0 (pure compute),
+  // t_e = max over the gathered layers >= 1 (each the envelope max(compute, transfer))
+  double t_c = -1.0, t_e = -1.0;
+  for (size_t i = c->recent.size() - (size_t)L; i < c->recent.size(); ++i) {
+    if (c->recent[i].first == 0) t_c = c->recent[i].second;
+    else t_e = std::max(t_e, c->recent[i].second);
+  }
+  if (t_c <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "calibrate_T: layer 0 is not among the last %d forwards", L);
+  if (t_e < 0) t_e = t_c;  // a one-layer stack: nothing gathered
+  // C_dummy = f_tok * n_ref, f_tok = per-token FLOPs of one MoE layer (router 2HE + experts 6kHh)
+  const double H = c->cfg.hidden, E = c->cfg.num_experts, k = c->cfg.top_k, h = c->cfg.ffn;
+  const double f_tok = 2.0 * H * E + 6.0 * k * H * h;
+  const double g = gamma > 0 ? gamma : (double)c->cfg.gamma;
+  double T = 0.0;
+  st = asyncep_calibrated_T(g, t_e, t_c, f_tok * (double)n_ref, &T);
+  if (st) return st;
+  if (flops_out) *flops_out = T;
+  if (tokens_out) *tokens_out = T / f_tok;
+  if (t_c_out) *t_c_out = t_c;
+  if (t_e_out) *t_e_out = t_e;
+  return ASYNCEP_OK;
+}
+
 // ------------------------------------------------------------------ NEXT-3 attention layer
 namespace {
 struct AttnWs {
@@ -1013,16 +1073,16 @@ size_t asyncep_attn_workspace_size(const asyncep_attn_config* c) {
 
 asyncep_status asyncep_attention(const asyncep_attn_config* c, const void* q, const void* k, const void* vt,
                                  int64_t ldv, const int32_t* vt_cu, const int32_t* cu, int32_t B, int64_t T, void* o,
-                                 void* stream) {
+                                 int32_t* sched, void* stream) {
   if (asyncep_status st = attn_check(c)) return st;
   if (T == 0) return ASYNCEP_OK;
-  if (!q || !k || !vt || !vt_cu || !cu || !o || B <= 0 || T < 0 || ldv < T || ldv % 8)
+  if (!q || !k || !vt || !vt_cu || !cu || !o || !sched || B <= 0 || T < 0 || ldv < T || ldv % 8)
     return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attention: bad pointers / B / T / ldv");
   if (((uintptr_t)q | (uintptr_t)k | (uintptr_t)vt | (uintptr_t)o) % 16)
     return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_attention: tensors must be 16-B aligned");
   if (!aep::launch_flash_attn((const bf16*)q, (const bf16*)k, (const bf16*)vt, ldv, cu, vt_cu, B, T, c->q_heads,
-                              c->kv_heads, (bf16*)o, (cudaStream_t)stream))
-    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (attention maps)");
+                              c->kv_heads, (bf16*)o, sched, (cudaStream_t)stream))
+    return fail(ASYNCEP_ERR_CUDA, "attention launch failed (tensor maps or scheduler counter)");
   CUDA_TRY(cudaGetLastError());
   return ASYNCEP_OK;
 }
@@ -1064,8 +1124,8 @@ asyncep_status asyncep_attn_layer(const asyncep_attn_config* c, const void* x, i
   int32_t* vcu = (int32_t*)(ws + L.vcu);
   const int64_t ldv = (T + 7 * (int64_t)B + 7) / 8 * 8;
   aep::launch_v_transpose(qkv, T, Hq, Hkv, cu, B, vcu, ldv, vt, st);
-  if (!aep::launch_flash_attn(qb, kb, vt, ldv, cu, vcu, B, T, Hq, Hkv, ob, st))
-    return fail(ASYNCEP_ERR_CUDA, "attention: tensor map encoding failed");
+  if (!aep::launch_flash_attn(qb, kb, vt, ldv, cu, vcu, B, T, Hq, Hkv, ob, cnt + 2, st))
+    return fail(ASYNCEP_ERR_CUDA, "attention: launch failed (tensor maps or scheduler counter)");
   if (!aep::launch_dense_gemm_tc(ob, T, Hq * d, (const bf16*)w_o, H, ao, cnt + 1, device_sms(), st))
     return fail(ASYNCEP_ERR_CUDA, "O projection: tensor map encoding failed");
   aep::launch_residual_rmsnorm((const bf16*)x, ao, (const bf16*)w_ln2, T, H, eps, (bf16*)x_out, (bf16*)xn2_out, st);

@@ -10,9 +10,10 @@
 // residual_rmsnorm (x + attn -> x', RMSNorm(x')).  The two projections run on the tcgen05
 // GEMM (gemm_tc.cu, dense mode).
 //
-// flash_attn2 (default) and flash_attn3 (64-key variant) are described above each kernel.
-// (A first single-tile version -- P through smem, row sums from a ones block appended to V^T --
-// reached 620-850 TFLOP/s and was replaced by the two-tile kernel.)
+// flash_attn4 (the kernel below) is a persistent CTA per SM holding two 128-query tiles of one
+// (prompt, head) item, P kept in TMEM.  Earlier generations -- a single-tile kernel (P through
+// smem), the non-persistent two-tile kernel ("v2") and a 64-key variant ("v3") -- were measured
+// slower and removed (S6, profiles/r01/ab_attn_*.log).
 // The rows of a tile past the end of its prompt are computed but never stored.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -103,238 +104,6 @@ __device__ bool fa2_pair(const int32_t* cu, int B, int u, int& b, int& pair, int
     acc += np;
   }
   return false;
-}
-
-__global__ void __launch_bounds__(FA2_NTHREADS, 1)
-    flash_attn2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Fa2Smem::BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;    // [2]
-  uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* v_full = bars + 5;    // [2]
-  uint64_t* v_empty = bars + 7;   // [2]
-  uint64_t* s_full = bars + 9;    // [tile]
-  uint64_t* p_full = bars + 11;   // [tile]
-  uint64_t* pv_done = bars + 13;  // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
-  __shared__ int s_job[4];
-
-  const int warp = warp_id(), lane = lane_id();
-  const int head = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int b = 0, pair = 0, start = 0, len = 0;
-    const bool ok = fa2_pair(p.cu, p.B, blockIdx.y, b, pair, start, len);
-    s_job[0] = ok ? pair : -1;
-    s_job[1] = start;
-    s_job[2] = len;
-    s_job[3] = ok ? p.vcu[b] : 0;
-  }
-  __syncthreads();
-  const int pair = s_job[0];
-  if (pair < 0) return;
-  const int start = s_job[1], len = s_job[2], vstart = s_job[3];
-  const int q0 = pair * 2 * FA_BM;           // first query position of tile A
-  const int nA = 2 * pair + 1, nB = 2 * pair + 2;  // causal key blocks of tiles A and B
-  const int kvh = head / (p.Hq / p.Hkv);
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
-      mbar_init(&pv_done[i], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch_desc(&map_q);
-      tma_prefetch_desc(&map_k);
-      tma_prefetch_desc(&map_vt);
-      mbar_arrive_expect_tx(q_full, 2 * FA_TILE);
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d_nohint(smem + Fa2Smem::QA + c * FA_KB, &map_q, q_full, c * 64, head, start + q0);
-        tma_load_3d_nohint(smem + Fa2Smem::QB + c * FA_KB, &map_q, q_full, c * 64, head, start + q0 + FA_BM);
-      }
-      for (int j = 0; j < nB; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = ((j >> 1) & 1) ^ 1;
-        mbar_wait(&k_empty[st], ph);
-        mbar_arrive_expect_tx(&k_full[st], FA_TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + Fa2Smem::K0 + st * FA_TILE + c * FA_KB, &map_k, &k_full[st], c * 64, kvh,
-                             start + j * FA_BN);
-        mbar_wait(&v_empty[st], ph);
-        mbar_arrive_expect_tx(&v_full[st], FA_TILE);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + Fa2Smem::V0 + st * FA_TILE + c * FA_KB, &map_vt, &v_full[st],
-                             vstart + j * FA_BN + c * 64, 0, kvh);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 9) {
-    constexpr uint32_t idesc = make_idesc(FA_BM, FA_BN, true);  // M = 128, N = 128 (keys or d)
-    const uint64_t dq[2] = {make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QA)),
-                            make_smem_desc_sw128(smem_u32(smem + Fa2Smem::QB))};
-    const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::K0));
-    const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + Fa2Smem::V0));
-    constexpr uint64_t kKb = FA_KB >> 4, kTile = FA_TILE >> 4;
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int t, int j, bool release_k) {  // S_t(j) = Q_t K_j^T
-      const int st = j & 1;
-      if (t == 0 || j >= nA) mbar_wait(&k_full[st], (j >> 1) & 1);  // first user of K_j waits for it
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
-          mma_bf16(tmem + 256 * t, dq[t] + off, dk + st * kTile + off, idesc, k > 0 ? 1u : 0u);
-        }
-        tc_commit(&s_full[t]);
-        if (release_k) tc_commit(&k_empty[st]);
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j, bool release_v) {  // O_t += P_t(j) V_j
-      const int st = j & 1;
-      mbar_wait(&p_full[t], j & 1);
-      if (t == 0 || j >= nA) mbar_wait(&v_full[st], (j >> 1) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 128 keys = 8 x 16: P columns advance by 8 (2 bf16 each)
-          const uint64_t off = (uint64_t)(k >> 2) * kKb + (uint64_t)(k & 3) * 2;
-          mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 8 * k, dv + st * kTile + off, idesc,
-                      (j > 0 || k > 0) ? 1u : 0u);
-        }
-        tc_commit(&pv_done[t]);
-        if (release_v) tc_commit(&v_empty[st]);
-      }
-      __syncwarp();
-    };
-    issue_s(0, 0, false);
-    issue_s(1, 0, true);
-    for (int j = 0; j < nB; ++j) {
-      if (j < nA) {
-        issue_pv(0, j, false);
-        if (j + 1 < nA) issue_s(0, j + 1, false);
-      }
-      issue_pv(1, j, true);
-      if (j + 1 < nB) issue_s(1, j + 1, true);
-    }
-  } else {
-    // softmax: warps 0-3 tile A, 4-7 tile B; thread = query row (TMEM lane)
-    const int t = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const int qpos = q0 + t * FA_BM + r;
-    const int nblk = t == 0 ? nA : nB;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t t_s = tmem + 256 * t + lane_off, t_o = t_s + 128;
-    const float scl = p.scale_log2;
-    float m_used = -1e30f, l0 = 0.f, l1 = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      uint32_t s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32 * c));
-      tmem_ld_wait();
-      if (j == nblk - 1 || (t == 1 && j == nblk - 2)) {  // blocks that can hold masked keys
-        const int lim = min(qpos, len - 1) - j * FA_BN;
-#pragma unroll
-        for (int c = 0; c < 128; ++c)
-          if (c > lim) s[c] = __float_as_uint(-INFINITY);
-      }
-      float mx = -1e30f;
-#pragma unroll
-      for (int c = 0; c < 128; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
-      mx *= scl;
-      float alpha = 1.f;
-      const bool resc = mx > m_used + kRescaleThresh;
-      if (resc) {
-        alpha = fast_exp2(m_used - mx);
-        m_used = mx;
-        l0 *= alpha;
-        l1 *= alpha;
-      }
-      const float nm = -m_used;
-      // p = exp2(s * scale - m) -> bf16 pairs into the first 64 columns of S_t (P_t)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float xa = fmaf(__uint_as_float(s[64 * c + 2 * i]), scl, nm);
-          const float xb = fmaf(__uint_as_float(s[64 * c + 2 * i + 1]), scl, nm);
-          const bool poly = FA_POLY_EVERY > 0 && (i % (FA_POLY_EVERY > 0 ? FA_POLY_EVERY : 1)) == 0;
-          const float a = poly ? poly_exp2(xa) : fast_exp2(xa);
-          const float b = poly ? poly_exp2(xb) : fast_exp2(xb);
-          add2(l0, l1, l0, l1, a, b);
-          pk[i] = pack_bf16x2(a, b);
-        }
-        tmem_st32(t_s + 32 * c, pk);
-      }
-      // O_t is final for blocks < j once PV_t(j-1) is done; rescale it (rare) before PV_t(j)
-      if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
-      tc_fence_after();
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + c * 32, o);
-        }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    mbar_wait(&pv_done[t], (nblk - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / (l0 + l1);
-    const bool valid = qpos < len;
-    __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + c * 32, o);
-      tmem_ld_wait();
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
 }
 
 // ------------------------------------------------------------------ flash attention v4 (persistent v2)
@@ -624,260 +393,6 @@ __global__ void __launch_bounds__(FA2_NTHREADS, 1)
   }
 }
 
-// ------------------------------------------------------------------ flash attention v3
-// v3 = v2 (two query tiles, P in TMEM, two softmax warpgroups) with 64-key blocks, which frees
-// TMEM for a double-buffered S per tile: [S0 | S1 | O] = 64 + 64 + 128 columns per tile.  The
-// MMA runs S_t(j+2) right after PV_t(j) (it reuses the buffer PV_t(j) just read), so a softmax
-// group starts block j+1 as soon as it finishes block j -- it no longer waits for its own PV
-// and the next S.  K and V^T move in a 4-stage ring of 64-key blocks (32 KB per stage).
-constexpr int FA3_BN = 64;
-constexpr int FA3_STAGES = 4;
-constexpr int FA3_KT = FA3_BN * 128 * 2;  // K block: [64 keys x 128 d] = 2 k-blocks of [64 x 128 B]
-constexpr int FA3_VT = FA_D * 128;        // V^T block: [128 d x 64 keys] = 1 k-block of [128 x 128 B]
-struct Fa3Smem {
-  static constexpr int QA = 0;
-  static constexpr int QB = QA + FA_TILE;
-  static constexpr int K0 = QB + FA_TILE;
-  static constexpr int V0 = K0 + FA3_STAGES * FA3_KT;
-  static constexpr int BAR = V0 + FA3_STAGES * FA3_VT;
-  static constexpr int BYTES = BAR + 256;
-  static constexpr int ALLOC = BYTES + 1024;
-};
-
-__global__ void __launch_bounds__(FA2_NTHREADS, 1)
-    flash_attn3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                       const __grid_constant__ CUtensorMap map_vt, const FaArgs p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Fa3Smem::BAR);
-  uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;     // [4]
-  uint64_t* k_empty = bars + 5;    // [4]
-  uint64_t* v_full = bars + 9;     // [4]
-  uint64_t* v_empty = bars + 13;   // [4]
-  uint64_t* s_full = bars + 17;    // [tile][2]
-  uint64_t* p_full = bars + 21;    // [tile]
-  uint64_t* pv_done = bars + 23;   // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 26);
-  __shared__ int s_job[4];
-
-  const int warp = warp_id(), lane = lane_id();
-  const int head = blockIdx.x;
-  if (threadIdx.x == 0) {
-    int b = 0, pair = 0, start = 0, len = 0;
-    const bool ok = fa2_pair(p.cu, p.B, blockIdx.y, b, pair, start, len);
-    s_job[0] = ok ? pair : -1;
-    s_job[1] = start;
-    s_job[2] = len;
-    s_job[3] = ok ? p.vcu[b] : 0;
-  }
-  __syncthreads();
-  const int pair = s_job[0];
-  if (pair < 0) return;
-  const int start = s_job[1], len = s_job[2], vstart = s_job[3];
-  const int q0 = pair * 2 * FA_BM;
-  const int nA = 4 * pair + 2, nB = 4 * pair + 4;  // causal 64-key blocks of tiles A and B
-  const int kvh = head / (p.Hq / p.Hkv);
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int i = 0; i < FA3_STAGES; ++i) {
-      mbar_init(&k_full[i], 1);
-      mbar_init(&k_empty[i], 1);
-      mbar_init(&v_full[i], 1);
-      mbar_init(&v_empty[i], 1);
-    }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
-    for (int t = 0; t < 2; ++t) {
-      mbar_init(&p_full[t], 4);
-      mbar_init(&pv_done[t], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 8) {
-    if (lane == 0) {
-      tma_prefetch_desc(&map_q);
-      tma_prefetch_desc(&map_k);
-      tma_prefetch_desc(&map_vt);
-      mbar_arrive_expect_tx(q_full, 2 * FA_TILE);
-      for (int c = 0; c < 2; ++c) {
-        tma_load_3d_nohint(smem + Fa3Smem::QA + c * FA_KB, &map_q, q_full, c * 64, head, start + q0);
-        tma_load_3d_nohint(smem + Fa3Smem::QB + c * FA_KB, &map_q, q_full, c * 64, head, start + q0 + FA_BM);
-      }
-      for (int j = 0; j < nB; ++j) {
-        const int st = j % FA3_STAGES;
-        const uint32_t ph = ((j / FA3_STAGES) & 1) ^ 1;
-        mbar_wait(&k_empty[st], ph);
-        mbar_arrive_expect_tx(&k_full[st], FA3_KT);
-        for (int c = 0; c < 2; ++c)
-          tma_load_3d_nohint(smem + Fa3Smem::K0 + st * FA3_KT + c * (FA3_KT / 2), &map_k, &k_full[st], c * 64, kvh,
-                             start + j * FA3_BN);
-        mbar_wait(&v_empty[st], ph);
-        mbar_arrive_expect_tx(&v_full[st], FA3_VT);
-        tma_load_3d_nohint(smem + Fa3Smem::V0 + st * FA3_VT, &map_vt, &v_full[st], vstart + j * FA3_BN, 0, kvh);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 9) {
-    constexpr uint32_t idesc_s = make_idesc(FA_BM, FA3_BN, true);   // M = 128, N = 64 keys
-    constexpr uint32_t idesc_pv = make_idesc(FA_BM, FA_D, true);    // M = 128, N = 128 d
-    const uint64_t dq[2] = {make_smem_desc_sw128(smem_u32(smem + Fa3Smem::QA)),
-                            make_smem_desc_sw128(smem_u32(smem + Fa3Smem::QB))};
-    const uint64_t dk = make_smem_desc_sw128(smem_u32(smem + Fa3Smem::K0));
-    const uint64_t dv = make_smem_desc_sw128(smem_u32(smem + Fa3Smem::V0));
-    constexpr uint64_t kQkb = FA_KB >> 4, kKkb = (FA3_KT / 2) >> 4, kKst = FA3_KT >> 4, kVst = FA3_VT >> 4;
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T into S buffer j & 1 of tile t
-      const int st = j % FA3_STAGES;
-      const bool first = (t == 0 && j < nA) || (t == 1 && j >= nA);  // the first user of K_j waits for it
-      if (first) mbar_wait(&k_full[st], (j / FA3_STAGES) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // d = 128: 2 k-blocks x 4 steps of 16
-          const uint64_t qo = (uint64_t)(k >> 2) * kQkb + (uint64_t)(k & 3) * 2;
-          const uint64_t ko = (uint64_t)(k >> 2) * kKkb + (uint64_t)(k & 3) * 2;
-          mma_bf16(tmem + 256 * t + 64 * (j & 1), dq[t] + qo, dk + st * kKst + ko, idesc_s, k > 0 ? 1u : 0u);
-        }
-        tc_commit(&s_full[2 * t + (j & 1)]);
-        if (t == 1) tc_commit(&k_empty[st]);  // tile B is the last user of every K block
-      }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j
-      const int st = j % FA3_STAGES;
-      mbar_wait(&p_full[t], j & 1);
-      const bool first = (t == 0 && j < nA) || (t == 1 && j >= nA);
-      if (first) mbar_wait(&v_full[st], (j / FA3_STAGES) & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)  // 64 keys = 4 x 16: P columns + 8, V^T k-block + 32 B
-          mma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 64 * (j & 1) + 8 * k, dv + st * kVst + 2 * k, idesc_pv,
-                      (j > 0 || k > 0) ? 1u : 0u);
-        tc_commit(&pv_done[t]);
-        if (t == 1) tc_commit(&v_empty[st]);
-      }
-      __syncwarp();
-    };
-    issue_s(0, 0);
-    issue_s(1, 0);
-    if (nA > 1) issue_s(0, 1);
-    issue_s(1, 1);
-    for (int j = 0; j < nB; ++j) {
-      if (j < nA) {
-        issue_pv(0, j);
-        if (j + 2 < nA) issue_s(0, j + 2);
-      }
-      issue_pv(1, j);
-      if (j + 2 < nB) issue_s(1, j + 2);
-    }
-  } else {
-    const int t = warp >> 2;
-    const int r = (warp & 3) * 32 + lane;
-    const int qfirst = q0 + t * FA_BM;
-    const int qpos = qfirst + r;
-    const int nblk = t == 0 ? nA : nB;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t t_base = tmem + 256 * t + lane_off, t_o = t_base + 128;
-    const float scl = p.scale_log2;
-    const int lim0 = min(qpos, len - 1), mlim = min(qfirst, len - 1);
-    float m_used = -1e30f, l0 = 0.f, l1 = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      const uint32_t t_s = t_base + 64 * (j & 1);
-      mbar_wait(&s_full[2 * t + (j & 1)], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t s[64];
-      tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(s));
-      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(s + 32));
-      tmem_ld_wait();
-      if ((j + 1) * FA3_BN - 1 > mlim) {  // a block that can hold masked keys for this tile
-        const int lim = lim0 - j * FA3_BN;
-#pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if (c > lim) s[c] = __float_as_uint(-INFINITY);
-      }
-      float mx = -1e30f;
-#pragma unroll
-      for (int c = 0; c < 64; c += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(s[c]), __uint_as_float(s[c + 1])));
-      mx *= scl;
-      float alpha = 1.f;
-      const bool resc = mx > m_used + kRescaleThresh;
-      if (resc) {
-        alpha = fast_exp2(m_used - mx);
-        m_used = mx;
-        l0 *= alpha;
-        l1 *= alpha;
-      }
-      const float nm = -m_used;
-      uint32_t pk[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float xa = fmaf(__uint_as_float(s[2 * i]), scl, nm);
-        const float xb = fmaf(__uint_as_float(s[2 * i + 1]), scl, nm);
-        const bool poly = FA_POLY_EVERY > 0 && (i % (FA_POLY_EVERY > 0 ? FA_POLY_EVERY : 1)) == 0;
-        const float a = poly ? poly_exp2(xa) : fast_exp2(xa);
-        const float b = poly ? poly_exp2(xb) : fast_exp2(xb);
-        add2(l0, l1, l0, l1, a, b);
-        pk[i] = pack_bf16x2(a, b);
-      }
-      tmem_st32(t_s, pk);  // P_t(j) over the first 32 columns of its S buffer
-      // PV_t(j-1) done: O final for blocks < j (rescale it, rarely, before PV_t(j) accumulates)
-      if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1);
-      tc_fence_after();
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld32(t_o + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(t_o + c * 32, o);
-        }
-      }
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
-    }
-    mbar_wait(&pv_done[t], (nblk - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / (l0 + l1);
-    const bool valid = qpos < len;
-    __nv_bfloat16* dst = p.o + ((int64_t)(start + qpos) * p.Hq + head) * FA_D;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + c * 32, o);
-      tmem_ld_wait();
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint4 v;
-          v.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
-          v.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
-          v.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
-          v.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
-          *reinterpret_cast<uint4*>(dst + c * 32 + i) = v;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 9) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
 // ------------------------------------------------------------------ elementwise kernels
 // RMSNorm of rows of n (multiple of 8) bf16 values: warp per row, fp32 math.
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
@@ -1097,9 +612,10 @@ void launch_v_transpose(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32
 }
 
 bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv, const int32_t* cu,
-                       const int32_t* vcu, int B, int64_t T, int Hq, int Hkv, bf16* o, cudaStream_t s) {
+                       const int32_t* vcu, int B, int64_t T, int Hq, int Hkv, bf16* o, int* sched,
+                       cudaStream_t s) {
   if (T <= 0 || B <= 0) return true;
-  CUtensorMap mq, mk, mv, mk64;
+  CUtensorMap mq, mk, mv;
   {
     const uint64_t dims[3] = {(uint64_t)FA_D, (uint64_t)Hq, (uint64_t)T};
     const uint64_t strides[2] = {(uint64_t)FA_D * 2, (uint64_t)Hq * FA_D * 2};
@@ -1115,13 +631,6 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
       return false;
   }
   {
-    const uint64_t dims[3] = {(uint64_t)FA_D, (uint64_t)Hkv, (uint64_t)T};
-    const uint64_t strides[2] = {(uint64_t)FA_D * 2, (uint64_t)Hkv * FA_D * 2};
-    const uint32_t box[3] = {64, 1, FA3_BN};
-    if (!encode_tmap(&mk64, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, k, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
-      return false;
-  }
-  {
     const uint64_t dims[3] = {(uint64_t)ldv, (uint64_t)FA_D, (uint64_t)Hkv};
     const uint64_t strides[2] = {(uint64_t)ldv * 2, (uint64_t)FA_D * ldv * 2};
     const uint32_t box[3] = {64, FA_D, 1};
@@ -1130,13 +639,8 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   }
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(flash_attn2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
-    cudaFuncSetAttribute(flash_attn3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa3Smem::ALLOC);
     cudaFuncSetAttribute(flash_attn4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Fa2Smem::ALLOC);
   });
-  // Default: the persistent, dynamically scheduled v4 (same-box A/B, profiles/r01/ab_attn_v2_v4*.log:
-  // +4 % on 4K prompts, +10 % on 1K, equal on 32K against v2); v2 / v3 on request.
-  static const int ver = getenv("ASYNCEP_FA_VER") ? atoi(getenv("ASYNCEP_FA_VER")) : 4;
   FaArgs a{};
   a.cu = cu;
   a.vcu = vcu;
@@ -1145,26 +649,16 @@ bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv
   a.Hkv = Hkv;
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)FA_D));
   a.o = o;
-  if (ver == 4) {
-    // exact item count needs the prompt lengths on the host; the upper bound is enough: items past
-    // the end map to no pair (fa2_pair fails) -- guarded by counting the real pairs on the device
-    const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int* sched = nullptr;  // the dynamic scheduler's counter (one per process / device)
-    if (!sched && cudaMalloc(&sched, sizeof(int)) != cudaSuccess) return false;
-    cudaMemsetAsync(sched, 0, sizeof(int), s);
-    flash_attn4_kernel<<<sms, FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv, a, (int)(pairs_upper * Hq), sched);
-  } else if (ver != 3) {
-    const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
-    flash_attn2_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv,
-                                                                                                      a);
-  } else {
-    const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
-    flash_attn3_kernel<<<dim3((unsigned)Hq, (unsigned)pairs_upper), FA2_NTHREADS, Fa3Smem::ALLOC, s>>>(mq, mk64, mv,
-                                                                                                      a);
-  }
+  // exact item count needs the prompt lengths on the host; the upper bound is enough: items past
+  // the end map to no pair (fa2_pair fails) -- guarded by counting the real pairs on the device
+  const int64_t pairs_upper = (T + 2 * FA_BM - 1) / (2 * FA_BM) + B;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // the dynamic scheduler's counter lives in caller-owned memory (one per call, zeroed on the
+  // launching stream), so concurrent calls on different streams / devices never share it
+  if (cudaMemsetAsync(sched, 0, sizeof(int), s) != cudaSuccess) return false;
+  flash_attn4_kernel<<<sms, FA2_NTHREADS, Fa2Smem::ALLOC, s>>>(mq, mk, mv, a, (int)(pairs_upper * Hq), sched);
   return true;
 }
 

@@ -147,8 +147,10 @@ void launch_qk_rope(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32_t* 
 // vcu [B+1] (output): per-prompt V^T column offsets, each prompt padded to 8 columns
 void launch_v_transpose(const bf16* qkv, int64_t T, int Hq, int Hkv, const int32_t* cu, int B, int32_t* vcu,
                         int64_t ldv, bf16* vt, cudaStream_t s);
+// sched: one int of caller-owned device memory (zeroed here, on s) for the dynamic item scheduler
 bool launch_flash_attn(const bf16* q, const bf16* k, const bf16* vt, int64_t ldv, const int32_t* cu,
-                       const int32_t* vcu, int B, int64_t T, int Hq, int Hkv, bf16* o, cudaStream_t s);
+                       const int32_t* vcu, int B, int64_t T, int Hq, int Hkv, bf16* o, int* sched,
+                       cudaStream_t s);
 // dense out[M, N] = A[M, K] . W[N, K]^T on the tcgen05 GEMM (CTA pairs, N % 256 == 0,
 // K % 64 == 0); sched: a zeroed int for the dynamic tile scheduler (nullable)
 bool launch_dense_gemm_tc(const bf16* A, int64_t M, int K, const bf16* W, int N, bf16* out, int* sched, int num_sms,

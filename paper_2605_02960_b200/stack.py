@@ -173,12 +173,16 @@ class MoEStack:
         """One pass of the whole stack: x_{l+1} = x_l + MoE_l(x_l) (reading R9), or with
         attention enabled the decoder layer x' = x + Attn_l(x), x_{l+1} = x' + MoE_l(RMSNorm(x'))
         over the packed prompts cu_seqlens (int32 device [B+1]).
-        Returns the final activations (a ping-pong buffer unless ``out`` is given).
+        Returns the final activations (a ping-pong buffer unless ``out`` is given; it may be
+        passed back in as ``x``, but the next call reuses it).
         ``record(l, x_l)`` (optional) sees each layer's input before it runs."""
         T = x.shape[0]
         if self._bufs is None or self._bufs[0].shape[0] < T:
             self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
                           for _ in range(2)]
+        # ping-pong parity chosen so that no layer's destination is its own input, even when x is
+        # a buffer this stack returned earlier
+        par = 1 if self._bufs[0].data_ptr() == x.data_ptr() else 0
         cur = x
         for op, l, _slot in stack_schedule(self.L, self.N, bool(self.cfg.replicate_layer0), self.offload_w):
             if op == "stage":
@@ -189,7 +193,7 @@ class MoEStack:
                 continue
             if record is not None:
                 record(l, cur)
-            dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
+            dst = out if (out is not None and l == self.L - 1) else self._bufs[(l + par) % 2][:T]
             if self.attn_w is not None:
                 xa, xn = self.attention(l, cur, cu_seqlens)
                 self.forward(l, xn, residual=xa, y=dst)
@@ -212,9 +216,10 @@ class MoEStack:
         if self._bufs is None or self._bufs[0].shape[0] < T:
             self._bufs = [torch.empty((self.cfg.max_tokens, self.H), dtype=torch.bfloat16, device=self.device)
                           for _ in range(2)]
+        par = 1 if self._bufs[0].data_ptr() == x.data_ptr() else 0
         cur = x
         for l in range(self.L):
-            dst = out if (out is not None and l == self.L - 1) else self._bufs[l % 2][:T]
+            dst = out if (out is not None and l == self.L - 1) else self._bufs[(l + par) % 2][:T]
             A.asyncep_ep_forward(self.ctx, l, cur, self._ep_ws, self._ep_cap, residual=cur if residual else None,
                                  y=dst)
             cur = dst
@@ -227,17 +232,9 @@ class MoEStack:
         envelope max(compute, transfer)); C_dummy = f_tok * n_ref with f_tok the per-token
         FLOPs of one MoE layer (2HE + 6kHh); returns T = gamma * (t_e/t_c) * C_dummy in FLOPs
         and in tokens per GPU (T / f_tok), plus the measured (t_c, t_e)."""
-        if not (self.cfg.flags & A.FLAG_STAGE_TIMING):
-            raise ValueError("calibrate_T needs a context created with FLAG_STAGE_TIMING")
         gamma = float(self.cfg.gamma) if gamma is None else gamma
         A.asyncep_reset_stage_times(self.ctx)
         self.run(x, local_shards=local_shards)
-        times = A.asyncep_forward_times(self.ctx, self.L)
-        t_c = next(ms for l, ms in times if l == 0)
-        rest = [ms for l, ms in times if l >= 1]
-        t_e = max(rest) if rest else t_c
-        f_tok = 2.0 * self.H * self.E + 6.0 * self.k * self.H * self.h
-        c_dummy = f_tok * x.shape[0]
-        T = A.asyncep_calibrated_T(gamma, t_e, t_c, c_dummy)
-        return {"T_flops": T, "T_tokens": T / f_tok, "t_c_ms": t_c, "t_e_ms": t_e, "n_ref": x.shape[0],
-                "f_tok": f_tok}
+        r = A.asyncep_calibrate_T(self.ctx, gamma, x.shape[0])
+        r["n_ref"] = x.shape[0]
+        return r

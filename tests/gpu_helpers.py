@@ -15,20 +15,32 @@ def f32(t) -> np.ndarray:
 class Workload:
     """Natural-layout weights of an L-layer stack, generated on demand on any device."""
 
-    def __init__(self, L, E, k, H, h, seed=0, zipf_s=0.0, fp8=False):
+    def __init__(self, L, E, k, H, h, seed=0, zipf_s=0.0, fp8=False, draw=None):
         self.L, self.E, self.k, self.H, self.h, self.seed, self.zipf_s = L, E, k, H, h, seed, zipf_s
         self.fp8 = fp8
+        # draw="cpu": generate on the host and copy (synth is bit-identical on both), so a tiny
+        # run launches no torch kernels besides copies (smoke(): the driver's launch capture)
+        self.draw = draw
+
+    def _on(self, device, fn):
+        if self.draw is None:
+            return fn(device)
+        out = fn(self.draw)
+        return tuple(t.to(device) for t in out) if isinstance(out, tuple) else out.to(device)
 
     def router(self, l, device="cuda"):
-        return synth.router_weight(self.E, self.H, self.seed, l, device=device, zipf_s=self.zipf_s)
+        return self._on(device, lambda d: synth.router_weight(self.E, self.H, self.seed, l, device=d,
+                                                              zipf_s=self.zipf_s))
 
     def experts(self, l, experts=None, device="cuda"):
         if self.fp8:
-            return synth.expert_weights_fp8(self.E, self.H, self.h, self.seed, l, device=device, experts=experts)
-        return synth.expert_weights(self.E, self.H, self.h, self.seed, l, device=device, experts=experts)
+            return self._on(device, lambda d: synth.expert_weights_fp8(self.E, self.H, self.h, self.seed, l,
+                                                                       device=d, experts=experts))
+        return self._on(device, lambda d: synth.expert_weights(self.E, self.H, self.h, self.seed, l, device=d,
+                                                               experts=experts))
 
     def tokens(self, T, device="cuda"):
-        return synth.tokens(T, self.H, self.seed, device=device, zipf_s=self.zipf_s)
+        return self._on(device, lambda d: synth.tokens(T, self.H, self.seed, device=d, zipf_s=self.zipf_s))
 
     def host_layer(self, l):
         """fp32 numpy copies for the oracle (drawn on the GPU: synth is bit-identical).

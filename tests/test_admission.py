@@ -96,3 +96,19 @@ def test_native_router_events(A):
     cfg = A.RouterConfig(2, B, F_TOK, HL, 1.0)
     assert A.asyncep_cost_delta(cfg, 64, 16, 10) == pytest.approx(O.cost_delta(64, 16, 10, F_TOK, HL), rel=1e-15)
     assert np.isnan(A.asyncep_cost_delta(cfg, 10, 11, 0))
+
+
+def test_malformed_round_changes_nothing_and_reports(A):
+    """A round with a bad request after good ones is rejected before any state changes, and
+    asyncep_last_error names the call (half-applied rounds, stale messages)."""
+    r = A.Router(2, B, F_TOK, HL, 1e18)
+    r.schedule_round([[1, 2], [3]], [2 * B, B], [10, 10], reset_loads=False)
+    before = r.loads().copy()
+    with pytest.raises(A.AsyncEPError, match="schedule_round"):
+        r.schedule_round([[5, 6], [7]], [2 * B, -1], [10, 10], reset_loads=False)
+    assert np.array_equal(r.loads(), before)
+    # the good prefix [5, 6] was not made pending either: a later request sharing it sees no match
+    g, d = r.schedule_round([[5, 6]], [2 * B], [10], reset_loads=False)
+    assert d[0] == pytest.approx(O.cost_delta(2 * B, 0, 10, F_TOK, HL), rel=1e-12)
+    with pytest.raises(A.AsyncEPError, match="router_progress"):
+        r.progress(5, 10)

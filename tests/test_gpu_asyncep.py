@@ -154,6 +154,7 @@ def test_peer_shards_and_calibrated_T():
     f_tok = 2 * 256 * 16 + 6 * 4 * 256 * 256
     ratio = max(1.0, cal["t_e_ms"] / cal["t_c_ms"])
     assert cal["T_flops"] == pytest.approx(1.2 * ratio * f_tok * T, rel=1e-6)
+    assert cal["T_tokens"] == pytest.approx(1.2 * ratio * T, rel=1e-6)
     times = A.asyncep_forward_times(st.ctx)
     assert [l for l, _ in times][-4:] == [0, 1, 2, 3]
 
@@ -277,3 +278,18 @@ def test_attention_abi_errors():
     A.asyncep_attention(cfg, q, k, vt, 64, cu, cu, o)  # all-zero inputs: uniform attention over v = 0
     torch.cuda.synchronize()
     assert int(torch.count_nonzero(o)) == 0
+
+
+@pytest.mark.parametrize("L", [2, 3])
+def test_stack_output_fed_back_as_input(L):
+    """MoEStack.run's returned ping-pong buffer may be passed back in as x: the
+    second pass equals running the stack on a private copy, for odd and even L."""
+    wl = Workload(L=L, E=16, k=4, H=256, h=256, seed=21)
+    T = 700
+    st = wl.stack(max_tokens=T)
+    y1 = st.run(wl.tokens(T))
+    y1_copy = y1.clone()
+    y2 = st.run(y1).clone()
+    ref = wl.stack(max_tokens=T).run(y1_copy).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(y2), _bits(ref))

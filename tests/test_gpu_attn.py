@@ -138,3 +138,39 @@ def test_attn_layer_deterministic_and_empty():
         big = synth.tokens(1001, H, 3, device="cuda")
         A.asyncep_attn_layer(cfg, big, torch.tensor([0, 1001], dtype=torch.int32, device="cuda"), w,
                              torch.empty_like(big), torch.empty_like(big), ws)
+
+
+def test_attention_concurrent_streams_bitwise():
+    """Two attention calls in flight at once on two streams (each with its own scheduler
+    counter) give bitwise the outputs of serial calls (a shared global counter let
+    one launch take the other's work items)."""
+    lengths = [3000, 1100, 700]
+    cu = _cu(lengths)
+    T, d, Hq, Hkv = int(cu[-1]), 128, 16, 4
+    vcu = np.concatenate([[0], np.cumsum([(n + 7) // 8 * 8 for n in lengths])]).astype(np.int32)
+    ldv = int(vcu[-1]) + 8
+    cfg = A.make_attn_config(256, Hq, Hkv, d, max_tokens=T)
+    cu_d, vcu_d = torch.from_numpy(cu).cuda(), torch.from_numpy(vcu).cuda()
+    ins = []
+    for seed in (11, 12):
+        q = synth.normal((T, Hq, d), seed, 0xA1, 1.0, "cuda")
+        k = synth.normal((T, Hkv, d), seed, 0xA2, 1.0, "cuda")
+        vt = synth.normal((Hkv, d, ldv), seed, 0xA3, 1.0, "cuda")
+        ins.append((q, k, vt))
+    serial = []
+    for q, k, vt in ins:
+        o = torch.empty((T, Hq, d), dtype=torch.bfloat16, device="cuda")
+        A.asyncep_attention(cfg, q, k, vt, ldv, vcu_d, cu_d, o)
+        serial.append(o)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty((T, Hq, d), dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    for rep in range(3):
+        for (q, k, vt), o, s in zip(ins, outs, streams):
+            o.fill_(float("nan"))
+        torch.cuda.synchronize()
+        for (q, k, vt), o, s in zip(ins, outs, streams):
+            A.asyncep_attention(cfg, q, k, vt, ldv, vcu_d, cu_d, o, stream=s)
+        torch.cuda.synchronize()
+        for o, ref in zip(outs, serial):
+            assert torch.equal(o.view(torch.int16), ref.view(torch.int16))
