@@ -8,13 +8,22 @@ One "step" = one pass of the whole hot path (router -> permute -> grouped GEMM w
 SwiGLU -> combine) through all 8 layers over one batch of synthetic tokens.
 
   N = 1  : all layers resident (world_size 1, no gather).
-  N > 1  : one process per GPU (torchrun), experts of layers >= 1 sharded 1/N by expert
-           index, layer 0 replicated, NCCL AllGather of layer l+1 on a side stream while
-           layer l computes.  No data-path collective.
+  N > 1  : one process per GPU.  `python bench.py --gpus N` launches the N ranks itself
+           (torch.distributed.run on 127.0.0.1) when WORLD_SIZE is unset; under torchrun it
+           is one rank.  Experts of layers >= 1 are sharded 1/N by expert index, layer 0 is
+           replicated, and layer l+1 is gathered into a double-buffered slot on a side stream
+           while layer l computes.  No data-path collective.  Every
+           available gather transport (NCCL AllGather, copy engines over CUDA-IPC peer
+           shards, the co-resident copy kernel) is probed and measured; the fastest carries
+           the headline (or the one --gather names).
 
 Timing: W warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
 events on the compute stream, max over ranks.  Inputs are larger than L2 (38.7 GB of
 weights, 268 MB of activations per layer), so no explicit L2 flush.
+
+Exposed AllGather: exposed_AG = wall(gathered stack) - wall(resident
+stack), the same kernels and tokens with every layer resident, timed step by step
+interleaved in the same process after the timed region -- wait plus interference.
 
 --impl reference: the CPU oracle (oracle/, plain fp64 C) on the host cores, on a bounded
 sample of the same workload (see cpu_baseline.sample in the JSON line).
@@ -23,8 +32,9 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -43,6 +53,8 @@ COMBINE_BYTES_TOK = K_ * H_ * 2 + 2 * H_ * 2               # read k rows + resid
 GEMM1_FLOPS_TOK = 4 * K_ * H_ * h_                        # gate/up: 2 * k * H * 2h
 GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
 SPEC_BF16 = 2.25e15
+ORACLE_SAMPLE_TOKENS = 2048  # per oracle sample, the same in cpu_baseline and --impl reference
+NVLINK_ASSUMED_GBS = 770.0   # B200_PROFILING.md measured NVLink-5 peer copy (only when no probe ran)
 
 
 def set_shape(name: str) -> None:
@@ -66,10 +78,30 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def tensor_peak(peaks: dict, src: str, run_mhz, fp8: bool):
+    """Clock-aware tensor peak for the dominant kernel: MEASURED_PEAKS' sustained cuBLAS bf16 rate
+    was taken at clocks_under_load.sm_mhz_median; the tensor pipe's rate is linear in the SM clock,
+    so the peak at this run's median clock is sustained x run_mhz / that clock, capped at the burst
+    figure (the most the part reached at all).  FP8: x 2 (nominal fp8:bf16 dense ratio)."""
+    burst = peaks.get("bf16_tflops", 1590.0)
+    sus = peaks.get("bf16_tflops_sustained", burst)
+    sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+    mult = 2.0 if fp8 else 1.0
+    if run_mhz and sus_mhz:
+        peak = min(burst, sus * run_mhz / sus_mhz)
+        note = (f"{src} bf16_tflops_sustained {sus} at {sus_mhz} MHz scaled to this run's median {run_mhz} MHz, "
+                f"capped at the burst {burst}")
+    else:
+        peak, note = sus, f"{src} bf16_tflops_sustained (no clock record)"
+    if fp8:
+        note += " x 2 (nominal fp8:bf16 dense ratio)"
+    return peak * mult, note, {"burst": burst * mult, "sustained": sus * mult}
+
+
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
 
-    def __init__(self, dev_index: int, period=0.1):
+    def __init__(self, dev_index: int, period=0.02):
         self.dev_index, self.period = dev_index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -170,7 +202,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    n_tok = int(os.environ.get("ASYNCEP_REF_TOKENS", "256"))
+    n_tok = int(os.environ.get("ASYNCEP_REF_TOKENS", str(ORACLE_SAMPLE_TOKENS)))
     orc = OracleSample()
     vals = []
     desc = ""
@@ -195,6 +227,29 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------------------ launcher
+def self_launch(argv, n: int) -> int:
+    """`bench.py --gpus N` without a torchrun environment: start the N ranks here (one process
+    per GPU, rendezvous on 127.0.0.1) and pass rank 0's JSON line through."""
+    import torch
+    if "ASYNCEP_BENCH_DEVICE" not in os.environ and torch.cuda.device_count() < n:
+        print(f"bench.py: --gpus {n} but only {torch.cuda.device_count()} visible GPU(s)", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")           # communicator init (transport, NVLS, channels) to stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "8")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+    r = subprocess.run(cmd, env=env, stdout=subprocess.PIPE, text=True)
+    sys.stdout.write(r.stdout)
+    sys.stdout.flush()
+    return r.returncode
+
+
 # ------------------------------------------------------------------------------ GPU arm
 def main():
     pre = argparse.ArgumentParser(add_help=False)
@@ -208,20 +263,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=T_LOC, help="tokens per GPU")
-    ap.add_argument("--replicate-layer0", type=int, default=1)
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
     ap.add_argument("--xperm", action="store_true", help="materialise X_perm (unfused dispatch, FLAG_XPERM)")
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
-                    help="1-GPU emulation of the N-rank AsyncEP gather (D2D copies of all N shards into "
-                         "the slot on the comm stream); measures exposed wait + HBM interference")
+                    help="1-GPU emulation of the N-rank AsyncEP gather (copies of the N-1 peer shards into "
+                         "the slot on the comm stream); measures exposed wait + interference")
     ap.add_argument("--link-gbs", type=float, default=0.0,
                     help="with --emulate-gather: pace the peer-shard copies at this GB/s (NVLink receive "
                          "bandwidth; B200_PROFILING.md measured peer copy: 770)")
-    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
-                    help="N>1: the weight gather over NVLink copy engines on CUDA-IPC-mapped peer shards "
-                         "(default; leaves every SM to the persistent GEMMs) or ncclAllGather")
+    ap.add_argument("--gather", choices=["auto", "kernel", "ce", "nccl"], default="auto",
+                    help="N>1 gather transport: auto = measure every available one and keep the fastest; "
+                         "kernel = co-resident copy kernel over CUDA-IPC peer shards; ce = copy engines over the "
+                         "same peer shards; nccl = ncclAllGather (GEMMs leave ASYNCEP_RESERVE_SMS, default 16, "
+                         "SMs to NCCL's kernels)")
+    ap.add_argument("--no-ab", action="store_true",
+                    help="skip the resident-vs-gathered interleaved measurement of exposed AllGather")
+    ap.add_argument("--ab-steps", type=int, default=0, help="interleaved A/B pairs (default: max(steps, 6))")
     ap.add_argument("--ep", action="store_true",
                     help="contrast baseline: the same stack as synchronous DP x EP (two on-path AllToAlls "
                          "per layer, PAPER.md:196-199) instead of AsyncEP")
@@ -239,6 +298,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(sys.argv[1:], args.gpus)
 
     import torch
     import torch.distributed as dist
@@ -254,7 +315,7 @@ def main():
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     # Test hooks for running N ranks on ONE GPU (NCCL refuses that): ASYNCEP_BENCH_DEVICE pins every
     # rank to one device, ASYNCEP_BENCH_BACKEND=gloo runs the control plane (barrier, max-over-ranks)
-    # on gloo; the gather then must be the peer-copy transport (CUDA IPC works within one GPU).
+    # on gloo; the gather then must be a peer-copy transport (CUDA IPC works within one GPU).
     backend = os.environ.get("ASYNCEP_BENCH_BACKEND", "nccl")
     dev_idx = int(os.environ.get("ASYNCEP_BENCH_DEVICE", local))
     torch.cuda.set_device(dev_idx)
@@ -273,22 +334,24 @@ def main():
     seed = 0
     flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0) | (A.FLAG_XPERM if args.xperm else 0)
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
-    if world > 1 and args.gather == "nccl":  # NCCL's SM-based AllGather needs SMs the GEMMs leave free
-        os.environ.setdefault("ASYNCEP_RESERVE_SMS", "16")
     emu = args.emulate_gather if world == 1 else 0
-    stack = MoEStack(L, E_, K_, H_, h_, T,
-                     lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf),
-                     lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex),
+    router_fn = lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf)
+    expert_fn = lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex)
+    stack = MoEStack(L, E_, K_, H_, h_, T, router_fn, expert_fn,
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
                      nccl_comm=comm, fp8=args.fp8, offload_window=args.offload)
     local_shards = stack.peer_shards() if emu > 1 else None
-    gather_mode = "emulated" if emu > 1 else ("none" if world == 1 else args.gather)
-    if world > 1 and args.gather == "p2p" and not args.ep:
+    gathered = (world > 1 or emu > 1) and not args.ep
+    reserve_nccl = int(os.environ.get("ASYNCEP_RESERVE_SMS", "16"))
+    p2p_error = None
+    if world > 1 and not args.ep and args.gather != "nccl":
         try:
             stack.enable_p2p_gather()
-        except Exception as e:  # fall back to NCCL (recorded in the JSON line)
-            gather_mode = f"nccl (p2p setup failed: {type(e).__name__}: {str(e)[:120]})"
+        except Exception as e:  # recorded in the JSON line; NCCL remains
+            p2p_error = f"{type(e).__name__}: {str(e)[:160]}"
             A.asyncep_set_peer_shards(stack.ctx, None)
+    if emu > 1 and args.link_gbs > 0:
+        A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
     cu = None
     attn_flops_layer = 0.0
     if args.attn:
@@ -302,8 +365,6 @@ def main():
         _run = lambda xin, out: stack.run_ep(xin, out=out)
     else:
         _run = lambda xin, out: stack.run(xin, out=out, local_shards=local_shards, cu_seqlens=cu)
-    if emu > 1 and args.link_gbs > 0:
-        A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
     # tokens: DP -- every rank its own batch
     x = synth.tokens(T, H_, seed + 17 + rank, device=dev, zipf_s=args.zipf)
     out = torch.empty_like(x)
@@ -325,6 +386,58 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    def timed_steps(n, run=_run, xin=x, o=out):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(cs)
+        for _ in range(n):
+            torch.cuda.nvtx.range_push("step")
+            run(xin, o)
+            torch.cuda.nvtx.range_pop()
+        e1.record(cs)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1)) / n
+
+    # ---------------- gather transports (N > 1): startup probe of each, then a short timed run of
+    # each; the fastest carries the headline unless --gather names one.
+    transports = {}
+    chosen = None
+    if gathered:
+        cands = []
+        if emu > 1:
+            cands = [{"kernel": A.GATHER_COPY_KERNEL, "ce": A.GATHER_COPY_ENGINE}.get(args.gather, A.GATHER_COPY_KERNEL)]
+        else:
+            have_p2p = p2p_error is None and args.gather != "nccl"
+            if args.gather in ("auto", "kernel") and have_p2p:
+                cands.append(A.GATHER_COPY_KERNEL)
+            if args.gather in ("auto", "ce") and have_p2p:
+                cands.append(A.GATHER_COPY_ENGINE)
+            if args.gather in ("auto", "nccl") and comm is not None:
+                cands.append(A.GATHER_NCCL)
+        if not cands:
+            raise SystemExit(f"no gather transport available (p2p: {p2p_error}, nccl comm: {comm is not None})")
+        probe_layer = 1 if L > 1 else 0
+        for tr in cands:
+            A.asyncep_set_gather_transport(stack.ctx, tr, reserve_nccl if tr == A.GATHER_NCCL else 0)
+            barrier()
+            probe = None
+            if probe_layer >= 1:
+                ms_p, nbytes = A.asyncep_probe_gather(stack.ctx, probe_layer,
+                                                      local_shards(probe_layer) if local_shards else None)
+                ms_p = max_over_ranks(ms_p)
+                probe = {"ms": ms_p, "bytes_per_rank": nbytes, "gbs": nbytes / (ms_p / 1e3) / 1e9}
+            for _ in range(2):
+                _run(x, out)
+            ms_tr = timed_steps(2) if len(cands) > 1 else None
+            transports[A.GATHER_NAMES[tr]] = {"probe": probe, "ms_per_step": ms_tr,
+                                              "reserve_sms": reserve_nccl if tr == A.GATHER_NCCL else 0}
+        if len(cands) > 1:
+            chosen = min(cands, key=lambda t: transports[A.GATHER_NAMES[t]]["ms_per_step"])
+        else:
+            chosen = cands[0]
+        A.asyncep_set_gather_transport(stack.ctx, chosen, reserve_nccl if chosen == A.GATHER_NCCL else 0)
+
     for _ in range(args.warmup):
         _run(x, out)
     barrier()
@@ -336,7 +449,9 @@ def main():
     barrier()
     e0.record(cs)
     for _ in range(args.steps):
+        torch.cuda.nvtx.range_push("step")
         _run(x, out)
+        torch.cuda.nvtx.range_pop()
     e1.record(cs)
     barrier()
     clk = clocks.stop()
@@ -419,26 +534,77 @@ def main():
     g1_ms = stages["gemm1_gateup_swiglu"] / max(nfwd, 1)
     g1_flops = GEMM1_FLOPS_TOK * T
     g1_tflops = g1_flops / (g1_ms / 1e3) / 1e12 if g1_ms > 0 else 0.0  # 0: no stage events (--ep)
-    peak_tf = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    peak_note = f"{peak_src} bf16_tflops_sustained (kernel timed inside a long step)"
-    spec = SPEC_BF16
-    if args.fp8:  # FP8 contraction: the bf16 measured peak x the nominal fp8/bf16 ratio (2x)
-        peak_tf *= 2.0
-        spec *= 2.0
-        peak_note = f"{peak_src} bf16_tflops_sustained x 2 (nominal fp8:bf16 dense ratio)"
+    peak_tf, peak_note, peak_ref = tensor_peak(peaks, peak_src, clk.get("sm_mhz"), args.fp8)
+    spec = SPEC_BF16 * (2.0 if args.fp8 else 1.0)
     traffic = ncu_traffic(args.fp8)
     per_layer_ms = {k: v / max(nfwd, 1) for k, v in stages.items()}
-    # Eq. 1 (R11/R12): T in tokens/GPU with F = this run's grouped-GEMM
-    # rate and the gather bandwidth of NVLink 5 (measured peer copy 770 GB/s, B200_PROFILING.md)
     gemm_ms = per_layer_ms["gemm1_gateup_swiglu"] + per_layer_ms["gemm2_down"]
     f_gemm = (GEMM1_FLOPS_TOK + GEMM2_FLOPS_TOK) * T / (gemm_ms / 1e3) if gemm_ms > 0 else 0.0
+    step_layer_ms = ms_step / L
+
+    # ---------------- exposed AllGather: wall(gathered) - wall(resident), same kernels
+    # and tokens, every layer resident in the second stack; step by step, interleaved.
+    exposed = {"ms_per_layer": 0.0, "frac_of_layer": 0.0, "wait_ms_per_layer": per_layer_ms["gather_wait"],
+               "note": "N=1: every layer resident, nothing gathered"}
+    if gathered and not args.no_ab and L > 1:
+        res = MoEStack(L, E_, K_, H_, h_, T, router_fn, expert_fn, world_size=1, rank=0, replicate_layer0=True,
+                       flags=flags & ~A.FLAG_STAGE_TIMING, device=dev, fp8=args.fp8,
+                       compute_stream=cs)
+        if args.attn:
+            res.enable_attention(lambda l: synth.attn_weights(H_, ATT_HQ, ATT_HKV, 128, seed, l, device=dev),
+                                 ATT_HQ, ATT_HKV, max_prompts=int(cu.numel() - 1))
+        run_res = lambda xin, o: res.run(xin, out=o, cu_seqlens=cu)
+        out_r = torch.empty_like(x)
+        for _ in range(2):
+            run_res(x, out_r)
+            _run(x, out)
+        n_ab = args.ab_steps or max(args.steps, 6)
+        clocks_ab = ClockSampler(dev_idx).start()
+        t_res, t_gat = [], []
+        for _ in range(n_ab):
+            t_res.append(timed_steps(1, run_res, x, out_r))
+            t_gat.append(timed_steps(1))
+        clk_ab = clocks_ab.stop()
+        med_r, med_g = float(np.median(t_res)), float(np.median(t_gat))
+        bitwise = bool(torch.equal(out.view(torch.int16), out_r.view(torch.int16)))
+        exp_layer = (med_g - med_r) / (L - 1)
+        exposed = {
+            "ms_per_layer": exp_layer, "frac_of_layer": exp_layer / (med_r / L),
+            "wait_ms_per_layer": per_layer_ms["gather_wait"],
+            "step_ms_gathered": med_g, "step_ms_resident": med_r, "pairs": n_ab, "clocks": clk_ab,
+            "output_bitwise_equal_resident": bitwise,
+            "note": ("SURVEY S8(d): (median gathered step - median resident step) / (L-1 gathered layers), "
+                     "steps interleaved one by one in this process (max over ranks); frac = that / resident "
+                     "layer time.  wait_ms_per_layer = the compute stream's wait for the slot before GEMM1 "
+                     "(inside the timed region) -- the part of the exposure that is not interference")}
+        del res
+        torch.cuda.empty_cache()
+
+    # Eq. 1 (R11/R12): T in tokens/GPU with F = this run's grouped-GEMM rate and the
+    # gather bandwidth probed at startup with the chosen transport (else assumed NVLink 5 peer copy).
     n_for_T = world if world > 1 else (emu if emu > 1 else 8)
-    bw = (args.link_gbs or 770.0) * 1e9
+    probe = transports.get(A.GATHER_NAMES.get(chosen, ""), {}).get("probe") if chosen is not None else None
+    if probe:
+        bw, bw_src = probe["gbs"] * 1e9, f"probed at startup ({A.GATHER_NAMES[chosen]}, one layer's gather)"
+    else:
+        bw, bw_src = (args.link_gbs or NVLINK_ASSUMED_GBS) * 1e9, "assumed (no gather at this N)"
     tcfg = A.make_config(L, E_, K_, H_, h_, expert_dtype=A.FP8_E4M3 if args.fp8 else A.BF16,
                          world_size=n_for_T, max_tokens=T, gamma=1.2)
     t_tok, t_flops = A.asyncep_saturation_T(tcfg, f_gemm, bw) if f_gemm > 0 else (None, None)
-    step_layer_ms = ms_step / L
     model = "qwen3-30b-a3b (config 2)" if args.shape == "30b" else "qwen3-235b-a22b"
+    if world > 1:
+        par = f"dp{world}+asyncep{world}"
+    elif emu > 1:
+        par = (f"dp1, asyncep{emu} gather emulated on 1 GPU (copies of the {emu - 1} peer shards into the slot on "
+               "the comm stream" + (f", paced at {args.link_gbs} GB/s" if args.link_gbs else "") + ")")
+    else:
+        par = "dp1 (all experts resident)"
+    if args.ep:
+        par = f"dp{world}xep{world} contrast (2 on-path AllToAlls/layer)"
+    if args.offload:
+        par += f", shards offloaded to pinned host memory, {args.offload}-deep device window (NEXT-2)"
+    gather_desc = "none" if not gathered else A.GATHER_NAMES[chosen] + (
+        " (emulated peers)" if emu > 1 else "") + (f"; p2p setup failed: {p2p_error}" if p2p_error else "")
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
@@ -449,22 +615,14 @@ def main():
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
-                   "parallelism": (f"dp{world}xep{world} contrast (2 on-path AllToAlls/layer)" if args.ep else
-                                   f"dp{world}+asyncep{world}" if world > 1 else
-                                   f"dp1, asyncep{emu} gather emulated on 1 GPU (D2D copies of the {emu} shards "
-                                   "into the slot on the comm stream" +
-                                   (f", peer shards paced at {args.link_gbs} GB/s" if args.link_gbs else "") + ")"
-                                   if emu > 1 else "dp1 (all experts resident)") +
-                                  (f", shards offloaded to pinned host memory, {args.offload}-deep device window "
-                                   "(NEXT-2)" if args.offload else ""),
-                   "gather": gather_mode,
+                   "parallelism": par, "gather": gather_desc,
                    "l2": (f"inputs larger than L2 ({L * E_ * 3 * H_ * h_ * (1 if args.fp8 else 2) / 1e9:.1f} GB expert "
                           f"weights + {T * K_ * H_ * 2 / 1e6:.0f} MB Y_perm per layer streamed each step, "
                           f"{T * H_ * 2 / 1e6:.0f} MB token activations); no flush")},
         "tokens_per_s_per_gpu": per_gpu,
         "layer_tokens_per_s_per_gpu": per_gpu * L,
         "mfu": {"vs_spec_dense": mfu_flops / spec, "spec_dense_flops": spec,
-                "vs_measured_sustained": mfu_flops / (peak_tf * 1e12),
+                "vs_measured_peak_at_run_clock": mfu_flops / (peak_tf * 1e12),
                 "flops_per_token_layer": FLOPS_TOK_LAYER},
         "stage_ms_per_layer": per_layer_ms,
         "hbm": {  # achieved HBM bandwidth of the memory-bound steps (algorithmic bytes / stage time)
@@ -476,17 +634,17 @@ def main():
                     "writes only the row maps (the row copy is fused into GEMM1's A load)"},
         "attention": attn_info,
         "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
-                         "flops_per_s": f_gemm, "ag_bytes_per_s": bw,
+                         "flops_per_s": f_gemm, "ag_bytes_per_s": bw, "ag_bandwidth_source": bw_src,
                          "note": "Eq. 1 per layer, F = measured grouped-GEMM rate of this run"},
         "layer_ms": step_layer_ms,
-        "exposed_ag": {"ms_per_layer": per_layer_ms["gather_wait"],
-                       "frac_of_layer": per_layer_ms["gather_wait"] / step_layer_ms if step_layer_ms and nfwd else None,
-                       "note": ("stream wait before GEMM1 on gathered layers (0 when N=1)" if not emu else
-                                f"emulated {emu}-rank gather (local D2D, no NVLink): exposed wait")},
+        "exposed_ag": exposed,
+        "gather_transports": transports or None,
         "roofline": {"kernel": "grouped GEMM1 gate/up + SwiGLU (tcgen05)", "bound": "tensor",
                      "achieved": g1_tflops, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": g1_tflops / peak_tf if g1_tflops else None,
                      "peak_source": peak_note,
+                     "frac_of_burst": g1_tflops / peak_ref["burst"] if g1_tflops else None,
+                     "frac_of_sustained": g1_tflops / peak_ref["sustained"] if g1_tflops else None,
                      "algorithmic_flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "traffic": traffic},
         "clocks": clk,
@@ -498,13 +656,16 @@ def main():
                         "steps' compute (double-buffered); all copies inside the timed region"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_tok = int(os.environ.get("ASYNCEP_CPU_TOKENS", "4096"))
+        n_tok = int(os.environ.get("ASYNCEP_CPU_TOKENS", str(ORACLE_SAMPLE_TOKENS)))
+        n_samp = 3
         del stack
         torch.cuda.empty_cache()
         orc = OracleSample()
-        v, dt, desc = orc.run(n_tok)
+        runs = [orc.run(n_tok, sample=i) for i in range(n_samp)]
+        dt = sum(r[1] for r in runs)
+        v = n_tok * n_samp / dt / L_
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": orc.threads, "kind": "oracle",
-                                "sample": desc + f"; {dt:.1f} s of CPU work"}
+                                "sample": f"{n_samp} x " + runs[0][2] + f"; {dt:.1f} s of CPU work"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

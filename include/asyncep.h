@@ -179,6 +179,34 @@ ASYNCEP_API asyncep_status asyncep_stage_layer(asyncep_ctx* ctx, int32_t layer);
  */
 ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void* const* shards);
 
+/*
+ * Gather transport of asyncep_prefetch_layer (and the copy mode of asyncep_prefetch_layer_local):
+ *  ASYNCEP_GATHER_COPY_KERNEL  copy kernel over the IPC-mapped peer shards, small CTAs that
+ *                              co-reside with the persistent GEMMs (needs asyncep_set_peer_shards);
+ *  ASYNCEP_GATHER_COPY_ENGINE  one cudaMemcpyAsync per 64 MiB chunk over the peer shards (the
+ *                              copy engines for peers on other GPUs; no SMs);
+ *  ASYNCEP_GATHER_NCCL         ncclAllGather on the borrowed communicator (north_star's path);
+ *  -1                          default: copy (ASYNCEP_GATHER_COPY env: kernel, or ce / memcpy) when
+ *                              peer shards are set, else NCCL.
+ * reserve_sms: SMs the persistent grouped GEMMs leave free (for NCCL's SM-based kernels, which do
+ * not fit beside a GEMM CTA); 0 = all SMs.  Errors: INVALID_ARG, NCCL (no communicator).
+ */
+#define ASYNCEP_GATHER_COPY_KERNEL 0
+#define ASYNCEP_GATHER_COPY_ENGINE 1
+#define ASYNCEP_GATHER_NCCL 2
+ASYNCEP_API asyncep_status asyncep_set_gather_transport(asyncep_ctx* ctx, int32_t transport, int32_t reserve_sms);
+
+/*
+ * Startup gather-bandwidth probe for Eq. 1's t_EP (T "computed once at startup
+ * from hardware and model configuration"; reading R12): one full gather of `layer` (a gathered
+ * layer whose slot is free) with the current transport on the comm stream, nothing else
+ * running; returns its time (ms) and the bytes each rank received ((N-1) x shard bytes).  The
+ * slot is handed back unconsumed.  With NCCL it is collective: every rank must call it.
+ * shards: NULL (peer shards / NCCL) or, in the one-GPU emulation, the N local shards of `layer`.
+ */
+ASYNCEP_API asyncep_status asyncep_probe_gather(asyncep_ctx* ctx, int32_t layer, const void* const* shards,
+                                                double* ms_out, double* bytes_out);
+
 /* The gather's transport primitive, exposed for measurement: a device-to-device (or NVLink
  * peer) copy of `bytes` on `stream` by a copy kernel of small CTAs that co-reside with the
  * persistent GEMM CTAs (the driver's D2D memcpy and NCCL kernels cannot start beside them).

@@ -85,6 +85,8 @@ def lib() -> ctypes.CDLL:
             "asyncep_init": ([CP, P, P, P, P, P, P, P, P, ctypes.POINTER(P)], I32),
             "asyncep_prefetch_layer": ([P, I32], I32),
             "asyncep_prefetch_layer_local": ([P, I32, P], I32),
+            "asyncep_set_gather_transport": ([P, I32, I32], I32),
+            "asyncep_probe_gather": ([P, I32, P, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
             "asyncep_moe_forward": ([P, I32, P, I64, P, P, P, P, P], I32),
             "asyncep_saturation_T": ([CP, D, D, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
             "asyncep_stage_times": ([P, ctypes.POINTER(D), I32, ctypes.POINTER(I64)], I32),
@@ -262,6 +264,24 @@ def asyncep_set_peer_shards(ctx: Context, shards) -> None:
     arr = (ctypes.c_void_p * (L * N))(*flat)
     _check(lib().asyncep_set_peer_shards(ctx.handle, arr))
     ctx.keep.append(shards)
+
+
+GATHER_COPY_KERNEL, GATHER_COPY_ENGINE, GATHER_NCCL = 0, 1, 2
+GATHER_NAMES = {GATHER_COPY_KERNEL: "copy_kernel", GATHER_COPY_ENGINE: "copy_engine", GATHER_NCCL: "nccl"}
+
+
+def asyncep_set_gather_transport(ctx: Context, transport: int, reserve_sms: int = 0) -> None:
+    _check(lib().asyncep_set_gather_transport(ctx.handle, int(transport), int(reserve_sms)))
+
+
+def asyncep_probe_gather(ctx: Context, layer: int, shards=None):
+    """One timed gather of `layer` (startup probe, R12) -> (ms, bytes received per rank)."""
+    arr = None
+    if shards is not None:
+        arr = (ctypes.c_void_p * len(shards))(*[_p(t) for t in shards])
+    ms, nb = ctypes.c_double(), ctypes.c_double()
+    _check(lib().asyncep_probe_gather(ctx.handle, int(layer), arr, ctypes.byref(ms), ctypes.byref(nb)))
+    return ms.value, nb.value
 
 
 def asyncep_gather_copy(dst, src, nbytes: int, stream=None) -> None:

@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "asyncep.h"
 #include "common.cuh"
 #include "kernels.cuh"
@@ -31,30 +33,43 @@ asyncep_status fail(asyncep_status st, const char* fmt, ...) {
   return st;
 }
 
-// The gather's transport primitive.  Default: aep::launch_gather_copy, a copy kernel whose small
-// CTAs co-reside with the persistent GEMM CTAs (measured: the driver's same-device D2D memcpy
-// stalls for the whole duration of a persistent GEMM, profiles/copy_timeline.py).
-// ASYNCEP_GATHER_COPY=memcpy (alias: ce): one cudaMemcpyAsync per copy -- for IPC-mapped peer
-// pointers on another GPU the driver moves the bytes with the copy engines, no SMs.
-cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0) {
-  static const int mode = [] {
-    const char* e = getenv("ASYNCEP_GATHER_COPY");
-    if (e && (!strcmp(e, "ce") || !strcmp(e, "memcpy"))) return 1;
-    return 0;
-  }();
+// The gather's transport primitives (asyncep_set_gather_transport):
+//  ASYNCEP_GATHER_COPY_KERNEL: aep::launch_gather_copy, a copy kernel whose small CTAs co-reside
+//    with the persistent GEMM CTAs (measured: the driver's same-device D2D memcpy stalls for the
+//    whole duration of a persistent GEMM, profiles/copy_timeline.py);
+//  ASYNCEP_GATHER_COPY_ENGINE: one cudaMemcpyAsync per chunk -- for IPC-mapped peer pointers on
+//    another GPU the driver moves the bytes with the copy engines, no SMs.
+// The default copy mode comes from ASYNCEP_GATHER_COPY (memcpy / ce: copy engine).
+int default_copy_mode() {
+  const char* e = getenv("ASYNCEP_GATHER_COPY");
+  return (e && (!strcmp(e, "ce") || !strcmp(e, "memcpy"))) ? ASYNCEP_GATHER_COPY_ENGINE : ASYNCEP_GATHER_COPY_KERNEL;
+}
+cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0,
+                        int mode = ASYNCEP_GATHER_COPY_KERNEL) {
   static const int ctas = [] {  // two 128-thread CTAs per SM: both fit beside any GEMM CTA (<= 224
     int dev = 0, n = 148;         // registers/thread) and keep more NVLink reads in flight
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return 2 * n;
   }();
-  if (mode == 0 && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
+  if (mode == ASYNCEP_GATHER_COPY_KERNEL && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
     aep::launch_gather_copy(dst, src, n, ctas, st, min_ns);
     return cudaGetLastError();
   }
-  if (min_ns) aep::launch_spin_ns(min_ns, st);  // other transports: link time, then the copy
+  if (min_ns) aep::launch_spin_ns(min_ns, st);  // copy engine: link time, then the copy
   return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st);
 }
+
+// NVTX ranges around the host-side enqueue of each call (the paper's gated per-layer hooks,
+// PAPER.md:650-655); free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* fmt, int layer) {
+    char b[64];
+    snprintf(b, sizeof(b), fmt, layer);
+    nvtxRangePushA(b);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 }  // namespace
 
@@ -205,6 +220,9 @@ struct asyncep_ctx {
   WsLayout L;
   size_t expert_bytes = 0, slot_bytes = 0, shard_bytes = 0;
   int num_sms = 148;
+  int dev_sms = 148;
+  int transport = -1;  // ASYNCEP_GATHER_*; -1: copy (default mode) when peer shards are set, else NCCL
+  int copy_mode = ASYNCEP_GATHER_COPY_KERNEL;
   // slot bookkeeping (host side): layer held / being gathered, and whether its forward ran
   int slot_layer[2] = {-1, -1};
   bool slot_consumed[2] = {true, true};
@@ -245,6 +263,24 @@ namespace {
 
 bool layer_resident(const asyncep_ctx* c, int l) {
   return c->cfg.world_size == 1 || (l == 0 && c->cfg.replicate_layer0);
+}
+
+// An asynchronous NCCL fault (a peer died, a network error) surfaces at the next call instead of
+// as a hang (ncclCommGetAsyncError; ncclInProgress = 7 is not an error).
+asyncep_status check_nccl_async(asyncep_ctx* c) {
+  if (!c->comm || !c->nccl.async_err) return ASYNCEP_OK;
+  int e = 0;
+  const int r = c->nccl.async_err(c->comm, &e);
+  if (r == 0 && (e == 0 || e == 7)) return ASYNCEP_OK;
+  const int code = r ? r : e;
+  return fail(ASYNCEP_ERR_NCCL, "NCCL asynchronous error on the borrowed communicator: %s (%d)",
+              c->nccl.errstr ? c->nccl.errstr(code) : "?", code);
+}
+
+// the gather transport a prefetch uses
+int gather_transport(const asyncep_ctx* c) {
+  if (c->transport >= 0) return c->transport;
+  return c->peer.empty() ? ASYNCEP_GATHER_NCCL : c->copy_mode;
 }
 
 // Reads the pending forwards' events oldest first.  blocking = false (the forward path when the
@@ -355,6 +391,8 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   c->cs = (cudaStream_t)compute_stream;
   c->ms = (cudaStream_t)comm_stream;
   c->num_sms = prop.multiProcessorCount;
+  c->dev_sms = prop.multiProcessorCount;
+  c->copy_mode = default_copy_mode();
   if (cfg->world_size > 1) {  // leave SMs to NCCL's AllGather kernels (persistent GEMMs fill every SM)
     const char* rs = getenv("ASYNCEP_RESERVE_SMS");
     const int reserve = rs && *rs ? atoi(rs) : 0;
@@ -432,6 +470,9 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
   if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
   if (layer < 0 || layer >= c->cfg.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
   if (layer_resident(c, layer)) return ASYNCEP_OK;
+  NvtxRange nv("asyncep_gather L%d", layer);
+  if (asyncep_status e = check_nccl_async(c)) return e;
+  const int tr = gather_transport(c);
   const int s = layer % 2;
   if (!c->slot_consumed[s] && c->slot_layer[s] != layer)
     return fail(ASYNCEP_ERR_INVALID_ARG,
@@ -448,8 +489,12 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     CUDA_TRY(cudaStreamWaitEvent(c->ms, c->h2d_done[wi], 0));
     own = c->window[wi];
   }
-  if (!shards && !c->peer.empty()) shards = c->peer.data() + (size_t)layer * c->cfg.world_size;  // P2P gather
+  if (!shards && tr != ASYNCEP_GATHER_NCCL) {  // P2P gather over the IPC-mapped peer shards
+    if (c->peer.empty()) return fail(ASYNCEP_ERR_INVALID_ARG, "copy transport without peer shards (asyncep_set_peer_shards)");
+    shards = c->peer.data() + (size_t)layer * c->cfg.world_size;
+  }
   if (shards) {
+    const int mode = tr == ASYNCEP_GATHER_NCCL ? c->copy_mode : tr;  // local shards (emulation): a copy
     // copy-engine gather: the N - 1 peer shards (then the own one), each rank starting at its
     // right-hand neighbour so that the N readers of a shard are spread over time
     constexpr size_t kChunk = (size_t)64 << 20;
@@ -464,7 +509,8 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       const bool paced = c->link_bps > 0 && r != c->cfg.rank;  // own shard is a local copy
       for (size_t o = 0; o < c->shard_bytes; o += kChunk) {
         const size_t n = std::min(kChunk, c->shard_bytes - o);
-        CUDA_TRY(gather_copy(dst + o, src + o, n, c->ms, paced ? (uint64_t)((double)n / c->link_bps * 1e9) : 0));
+        CUDA_TRY(gather_copy(dst + o, src + o, n, c->ms, paced ? (uint64_t)((double)n / c->link_bps * 1e9) : 0,
+                             mode));
         c->launches += 1;
       }
     }
@@ -563,6 +609,51 @@ asyncep_status asyncep_set_peer_shards(asyncep_ctx* c, const void* const* shards
   return ASYNCEP_OK;
 }
 
+asyncep_status asyncep_set_gather_transport(asyncep_ctx* c, int32_t transport, int32_t reserve_sms) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (transport < -1 || transport > ASYNCEP_GATHER_NCCL)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "unknown gather transport %d", transport);
+  if (transport == ASYNCEP_GATHER_NCCL && !c->comm)
+    return fail(ASYNCEP_ERR_NCCL, "NCCL transport without a communicator");
+  if (reserve_sms < 0 || reserve_sms >= c->dev_sms - 2)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "reserve_sms %d out of range", reserve_sms);
+  c->transport = transport;
+  if (transport == ASYNCEP_GATHER_COPY_KERNEL || transport == ASYNCEP_GATHER_COPY_ENGINE) c->copy_mode = transport;
+  c->num_sms = c->dev_sms - (reserve_sms & ~1);  // the grouped GEMMs' persistent grid (CTA pairs)
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_probe_gather(asyncep_ctx* c, int32_t layer, const void* const* shards, double* ms_out,
+                                    double* bytes_out) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (c->cfg.world_size < 2) return fail(ASYNCEP_ERR_INVALID_ARG, "probe_gather needs world_size > 1");
+  if (layer < 0 || layer >= c->cfg.num_layers || layer_resident(c, layer))
+    return fail(ASYNCEP_ERR_INVALID_ARG, "probe_gather: layer %d is not a gathered layer", layer);
+  const int s = layer % 2;
+  if (!c->slot_consumed[s]) return fail(ASYNCEP_ERR_INVALID_ARG, "probe_gather: slot %d is in use", s);
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
+  CUDA_TRY(cudaEventRecord(e0, c->ms));
+  asyncep_status st = prefetch_common(c, layer, shards);
+  if (st == ASYNCEP_OK) {
+    CUDA_TRY(cudaEventRecord(e1, c->ms));
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+    // the slot held the layer but no forward read it: hand it back (same stream orders the next fill)
+    c->slot_consumed[s] = true;
+    CUDA_TRY(cudaEventRecord(c->slot_free[s], c->ms));
+    if (ms_out) *ms_out = ms;
+    // bytes each rank receives: the N - 1 peer shards
+    if (bytes_out) *bytes_out = (double)(c->cfg.world_size - 1) * (double)c->shard_bytes;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return st;
+}
+
 asyncep_status asyncep_gather_copy(void* dst, const void* src, size_t bytes, void* stream) {
   if ((!dst || !src) && bytes) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
   if (!bytes) return ASYNCEP_OK;
@@ -586,6 +677,8 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
                                      (long long)cf.max_tokens);
   if (T == 0) return ASYNCEP_OK;
   if (!x || !y) return fail(ASYNCEP_ERR_INVALID_ARG, "x / y is NULL");
+  NvtxRange nv("asyncep_moe_forward L%d", layer);
+  if (asyncep_status e = check_nccl_async(c)) return e;
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "x / y / residual must be 16-B aligned");
   if (x == y) return fail(ASYNCEP_ERR_INVALID_ARG, "y must not alias x");
@@ -807,6 +900,8 @@ asyncep_status asyncep_ep_forward(asyncep_ctx* c, int32_t layer, const void* x, 
   if (!x || !y || !ep_ws || max_recv_rows <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "null argument");
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual | (uintptr_t)ep_ws) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "pointers must be 16-B aligned");
+  NvtxRange nv("asyncep_ep_forward L%d", layer);
+  if (asyncep_status e = check_nccl_async(c)) return e;
   const int N = cf.world_size, E = cf.num_experts, per = E / N, k = cf.top_k, H = cf.hidden, h = cf.ffn;
   if (N > 1 && (!c->comm || !c->nccl.send || !c->nccl.recv))
     return fail(ASYNCEP_ERR_NCCL, "EP contrast with world_size > 1 needs an NCCL communicator");

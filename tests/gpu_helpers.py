@@ -58,3 +58,27 @@ class Workload:
         from paper_2605_02960_b200.stack import MoEStack
         return MoEStack(self.L, self.E, self.k, self.H, self.h, max_tokens,
                         lambda l: self.router(l), lambda l, ex: self.experts(l, ex), fp8=self.fp8, **kw)
+
+    def host_layer_subset(self, l, experts):
+        """Like host_layer, but only the listed experts' weights are filled (the others stay zero
+        pages of np.zeros, never touched by an oracle call whose routing avoids them).  FP8 codes are
+        decoded on the device through the oracle's own 256-entry decode table (oracle.e4m3_decode of
+        every byte), then scaled by the row scale -- the same values host_layer produces."""
+        E, H, h = self.E, self.H, self.h
+        wr = f32(self.router(l))
+        g = np.zeros((E, h, H), np.float32)
+        u = np.zeros((E, h, H), np.float32)
+        d = np.zeros((E, H, h), np.float32)
+        table = None
+        if self.fp8:
+            import oracle
+            table = torch.from_numpy(oracle.e4m3_decode(np.arange(256, dtype=np.uint8))).cuda()
+        for e in sorted(set(int(v) for v in experts)):
+            if self.fp8:
+                gc, uc, dc, gs, us, ds = self.experts(l, range(e, e + 1))
+                deq = lambda c, sc: (table[c.long()] * sc[..., None]).cpu().numpy()[0]
+                g[e], u[e], d[e] = deq(gc, gs), deq(uc, us), deq(dc, ds)
+            else:
+                ge, ue, de = self.experts(l, range(e, e + 1))
+                g[e], u[e], d[e] = f32(ge)[0], f32(ue)[0], f32(de)[0]
+        return wr, g, u, d

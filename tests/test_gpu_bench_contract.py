@@ -43,3 +43,28 @@ def test_bench_line_contract(fp8):
     assert e["h2d_bytes_per_step"] == 4096 * 4096 * 2 and e["d2h_bytes_per_step"] == 4096 * 4096 * 2
     # our kernels launched inside the timed region: 7 per BF16 layer, 9 per FP8 layer
     assert d["gpu_launches"] == 2 * 2 * (9 if fp8 else 7)
+
+
+def test_bench_self_launches_two_ranks_on_one_gpu():
+    """`bench.py --gpus 2` without torchrun launches the two ranks itself (here both on GPU 0 with a
+    gloo control plane, ASYNCEP_BENCH_DEVICE / _BACKEND): one JSON line from rank 0, both peer-copy
+    transports probed and timed, exposed AllGather = gathered - resident wall with the gathered
+    output bitwise equal to the resident stack's."""
+    env = dict(os.environ, ASYNCEP_BENCH_DEVICE="0", ASYNCEP_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--layers", "3",
+                        "--tokens", "4096", "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch_tokens"] == 8192
+    tr = d["gather_transports"]
+    assert set(tr) == {"copy_kernel", "copy_engine"}
+    for v in tr.values():
+        assert v["probe"]["gbs"] > 0 and v["ms_per_step"] > 0
+    assert d["config"]["gather"].split(" ")[0] in tr
+    ex = d["exposed_ag"]
+    assert ex["output_bitwise_equal_resident"] is True
+    assert ex["step_ms_gathered"] > 0 and ex["step_ms_resident"] > 0
+    assert d["saturation_T"]["ag_bandwidth_source"].startswith("probed")

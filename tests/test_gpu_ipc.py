@@ -16,23 +16,43 @@ pytestmark = pytest.mark.gpu
 L, E, K, H, h, T = 4, 16, 4, 256, 256, 900
 
 
-def _rank(rank, world, port, q):
+def _rank(rank, world, port, q, transport="kernel"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nccl = transport == "nccl"
+    dev = rank if nccl else 0
+    torch.cuda.set_device(dev)
+    if nccl:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import sys
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
         from gpu_helpers import Workload
+        from paper_2605_02960_b200 import asyncep as A
         wl = Workload(L=L, E=E, k=K, H=H, h=h, seed=41)
         x = wl.tokens(T)
-        st = wl.stack(max_tokens=T, world_size=world, rank=rank)
-        st.enable_p2p_gather()
+        comm = None
+        if nccl:
+            dist.all_reduce(torch.ones(1, device="cuda"))
+            comm = A.nccl_comm_ptr()
+        st = wl.stack(max_tokens=T, world_size=world, rank=rank, nccl_comm=comm)
+        if nccl:
+            A.asyncep_set_gather_transport(st.ctx, A.GATHER_NCCL, 16)
+        else:
+            st.enable_p2p_gather()
+            A.asyncep_set_gather_transport(st.ctx, A.GATHER_COPY_ENGINE if transport == "ce" else
+                                           A.GATHER_COPY_KERNEL, 0)
+        ms, nbytes = A.asyncep_probe_gather(st.ctx, 1)  # startup bandwidth probe (collective)
+        assert ms > 0 and nbytes == (world - 1) * st.shards[1].numel()
         outs = []
         for _ in range(2):  # the second pass reuses both slots
             outs.append(st.run(x).clone())
         torch.cuda.synchronize()
+        if nccl:  # the gathered slot holds the unsharded layer, byte for byte
+            full = wl.stack(max_tokens=T).shards[L - 1]
+            assert torch.equal(st.slots[(L - 1) % 2], full)
         ref = wl.stack(max_tokens=T).run(x).clone()
         torch.cuda.synchronize()
         ok = all(torch.equal(o.view(torch.int16), ref.view(torch.int16)) for o in outs)
@@ -50,14 +70,27 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_two_process_ipc_gather_bitwise_equals_resident():
+@pytest.mark.parametrize("transport", ["kernel", "ce"])
+def test_two_process_ipc_gather_bitwise_equals_resident(transport):
+    """Both peer-copy transports: the co-resident copy kernel and the copy-engine memcpy."""
+    _spawn(2, transport)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs 2 GPUs (NCCL refuses two ranks on one GPU)")
+def test_two_gpu_nccl_allgather_bitwise_equals_resident():
+    """The north_star path across two real GPUs: ncclAllGather of layer l+1 on the side stream
+    (GEMMs leave 16 SMs), slot = the unsharded layer bytes, output = the resident stack."""
+    _spawn(2, "nccl")
+
+
+def _spawn(world, transport):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(2)]
+    res = [q.get(timeout=600) for _ in range(world)]
     for p in procs:
         p.join(timeout=120)
     for rank, ok, err in sorted(res):
