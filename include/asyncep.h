@@ -196,6 +196,10 @@ ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void*
 #define ASYNCEP_GATHER_NCCL 2
 ASYNCEP_API asyncep_status asyncep_set_gather_transport(asyncep_ctx* ctx, int32_t transport, int32_t reserve_sms);
 
+/* Measurement knob: CTAs of the co-resident copy kernel (0 = default: ASYNCEP_GATHER_CTAS, else
+ * 2 per SM).  Fewer CTAs keep fewer warps beside the GEMMs; NVLink latency needs ~1 MB in flight. */
+ASYNCEP_API asyncep_status asyncep_set_gather_copy_ctas(asyncep_ctx* ctx, int32_t ctas);
+
 /*
  * Startup gather-bandwidth probe for Eq. 1's t_EP (T "computed once at startup
  * from hardware and model configuration"; reading R12): one full gather of `layer` (a gathered

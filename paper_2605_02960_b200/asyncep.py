@@ -86,6 +86,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_prefetch_layer": ([P, I32], I32),
             "asyncep_prefetch_layer_local": ([P, I32, P], I32),
             "asyncep_set_gather_transport": ([P, I32, I32], I32),
+            "asyncep_set_gather_copy_ctas": ([P, I32], I32),
             "asyncep_probe_gather": ([P, I32, P, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
             "asyncep_moe_forward": ([P, I32, P, I64, P, P, P, P, P], I32),
             "asyncep_saturation_T": ([CP, D, D, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
@@ -274,6 +275,10 @@ def asyncep_set_gather_transport(ctx: Context, transport: int, reserve_sms: int 
     _check(lib().asyncep_set_gather_transport(ctx.handle, int(transport), int(reserve_sms)))
 
 
+def asyncep_set_gather_copy_ctas(ctx: Context, ctas: int) -> None:
+    _check(lib().asyncep_set_gather_copy_ctas(ctx.handle, int(ctas)))
+
+
 def asyncep_probe_gather(ctx: Context, layer: int, shards=None):
     """One timed gather of `layer` (startup probe, R12) -> (ms, bytes received per rank)."""
     arr = None
@@ -377,11 +382,12 @@ def asyncep_attention(cfg: AttnConfig, q, k, vt, ldv: int, vt_cu, cu_seqlens, o,
     """Causal GQA attention core: q [T,Hq,d], k [T,Hkv,d], vt [Hkv,d,ldv] with prompt b at columns
     vt_cu[b] (multiples of 8), cu_seqlens int32 [B+1]; sched: int32 device counter (one per call)."""
     T = q.shape[0]
-    if sched is None:
-        sched = torch.empty(1, dtype=torch.int32, device=q.device)
+    st = stream or torch.cuda.current_stream()
+    if sched is None:  # allocated in the launching stream's pool: a concurrent call never gets the same int
+        with torch.cuda.stream(st):
+            sched = torch.empty(1, dtype=torch.int32, device=q.device)
     _check(lib().asyncep_attention(ctypes.byref(cfg), _p(q), _p(k), _p(vt), ldv, _p(vt_cu), _p(cu_seqlens),
-                                   cu_seqlens.shape[0] - 1, T, _p(o), _p(sched),
-                                   _stream(stream or torch.cuda.current_stream())))
+                                   cu_seqlens.shape[0] - 1, T, _p(o), _p(sched), _stream(st)))
 
 
 def asyncep_attn_layer(cfg: AttnConfig, x, cu_seqlens, weights, x_out, xn2_out, workspace, stream=None) -> None:

@@ -44,16 +44,19 @@ int default_copy_mode() {
   const char* e = getenv("ASYNCEP_GATHER_COPY");
   return (e && (!strcmp(e, "ce") || !strcmp(e, "memcpy"))) ? ASYNCEP_GATHER_COPY_ENGINE : ASYNCEP_GATHER_COPY_KERNEL;
 }
+// copy-kernel CTAs: ASYNCEP_GATHER_CTAS, else per_sm x SMs (asyncep_set_gather_copy_ctas at run time)
+int default_copy_ctas() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  const char* e = getenv("ASYNCEP_GATHER_CTAS");
+  return (e && *e && atoi(e) > 0) ? atoi(e) : 2 * n;
+}
 cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0,
-                        int mode = ASYNCEP_GATHER_COPY_KERNEL) {
-  static const int ctas = [] {  // two 128-thread CTAs per SM: both fit beside any GEMM CTA (<= 224
-    int dev = 0, n = 148;         // registers/thread) and keep more NVLink reads in flight
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return 2 * n;
-  }();
+                        int mode = ASYNCEP_GATHER_COPY_KERNEL, int ctas = 0) {
   if (mode == ASYNCEP_GATHER_COPY_KERNEL && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
-    aep::launch_gather_copy(dst, src, n, ctas, st, min_ns);
+    static const int dflt = default_copy_ctas();
+    aep::launch_gather_copy(dst, src, n, ctas > 0 ? ctas : dflt, st, min_ns);
     return cudaGetLastError();
   }
   if (min_ns) aep::launch_spin_ns(min_ns, st);  // copy engine: link time, then the copy
@@ -223,6 +226,7 @@ struct asyncep_ctx {
   int dev_sms = 148;
   int transport = -1;  // ASYNCEP_GATHER_*; -1: copy (default mode) when peer shards are set, else NCCL
   int copy_mode = ASYNCEP_GATHER_COPY_KERNEL;
+  int copy_ctas = 0;  // 0: default_copy_ctas()
   // slot bookkeeping (host side): layer held / being gathered, and whether its forward ran
   int slot_layer[2] = {-1, -1};
   bool slot_consumed[2] = {true, true};
@@ -510,7 +514,7 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       for (size_t o = 0; o < c->shard_bytes; o += kChunk) {
         const size_t n = std::min(kChunk, c->shard_bytes - o);
         CUDA_TRY(gather_copy(dst + o, src + o, n, c->ms, paced ? (uint64_t)((double)n / c->link_bps * 1e9) : 0,
-                             mode));
+                             mode, c->copy_ctas));
         c->launches += 1;
       }
     }
@@ -620,6 +624,12 @@ asyncep_status asyncep_set_gather_transport(asyncep_ctx* c, int32_t transport, i
   c->transport = transport;
   if (transport == ASYNCEP_GATHER_COPY_KERNEL || transport == ASYNCEP_GATHER_COPY_ENGINE) c->copy_mode = transport;
   c->num_sms = c->dev_sms - (reserve_sms & ~1);  // the grouped GEMMs' persistent grid (CTA pairs)
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_set_gather_copy_ctas(asyncep_ctx* c, int32_t ctas) {
+  if (!c || ctas < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "bad arguments");
+  c->copy_ctas = ctas;
   return ASYNCEP_OK;
 }
 

@@ -77,24 +77,38 @@ __global__ void spin_ns_kernel(uint64_t ns) {
 // progresses DURING the GEMMs instead of waiting for SMs to drain (the driver's D2D memcpy and
 // NCCL's kernels do not fit beside a ~220 KB-smem GEMM CTA).  Streaming 16-B loads / stores
 // (evict-first: the slot is read once, by the next layer); works on NVLink peer pointers too.
+// Each thread keeps 8 x 16 B in flight per round (the NVLink read latency needs ~1 MB in flight
+// per GPU for the link rate, so few CTAs suffice).
 // min_ns > 0 (1-GPU link emulation): block 0 holds the kernel open until min_ns after it started,
-// so a chunk takes max(copy time, link time) -- the copy overlaps the emulated link time.
+// so a chunk takes max(copy, link) time, and ns_per_round > 0: every CTA paces itself -- round r of its strided share
+// may start only ns_per_round * r after the kernel started -- so the copy streams smoothly at the
+// emulated link rate over the whole chunk, like a remote read, instead of bursting at HBM speed.
+constexpr int kCopyUnroll = 8;
 __global__ void __launch_bounds__(128) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                                          size_t n16, uint64_t min_ns) {
+                                                          size_t n16, uint64_t ns_per_round, uint64_t min_ns) {
   uint64_t t0 = 0;
-  if (min_ns && blockIdx.x == 0 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (ns_per_round || min_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   const size_t stride = (size_t)gridDim.x * 128;
   size_t i = (size_t)blockIdx.x * 128 + threadIdx.x;
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    const uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride), c = __ldcs(src + i + 2 * stride),
-                d = __ldcs(src + i + 3 * stride);
-    __stcs(dst + i, a);
-    __stcs(dst + i + stride, b);
-    __stcs(dst + i + 2 * stride, c);
-    __stcs(dst + i + 3 * stride, d);
+  uint64_t round = 0;
+  for (; i + (kCopyUnroll - 1) * stride < n16; i += kCopyUnroll * stride) {
+    if (ns_per_round) {
+      for (;;) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 >= ns_per_round * round) break;
+        __nanosleep(256);
+      }
+      ++round;
+    }
+    uint4 v[kCopyUnroll];
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) __stcs(dst + i + u * stride, v[u]);
   }
   for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
-  if (min_ns && blockIdx.x == 0 && threadIdx.x == 0)
+  if (min_ns && blockIdx.x == 0 && threadIdx.x == 0)  // the chunk takes max(copy, link) time
     for (;;) {
       uint64_t t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -108,8 +122,13 @@ void launch_spin_ns(uint64_t ns, cudaStream_t s) { spin_ns_kernel<<<1, 1, 0, s>>
 
 void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns) {
   if (!bytes) return;
-  gather_copy_kernel<<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), bytes / 16,
-                                         min_ns);
+  const size_t n16 = bytes / 16;
+  // pacing: the chunk must take min_ns; a CTA's share is split into rounds of 128 x kCopyUnroll x 16 B
+  const size_t per_round = (size_t)ctas * 128 * kCopyUnroll;
+  const uint64_t rounds = (n16 + per_round - 1) / per_round;
+  const uint64_t ns_per_round = (min_ns && rounds) ? min_ns / rounds : 0;
+  gather_copy_kernel<<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+                                         ns_per_round, min_ns);
 }
 
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
