@@ -580,6 +580,25 @@ def main():
         del res
         torch.cuda.empty_cache()
 
+    # ---------------- contrast (Table 1 DP x EP): the same stack as
+    # synchronous expert parallelism -- each rank keeps its E/N experts and the permuted token rows
+    # travel to them and back with two on-path AllToAlls per layer -- timed on the same box (N > 1).
+    ep_contrast = None
+    if world > 1 and comm is not None and not args.ep and not args.fp8 and not args.attn and not args.no_ab:
+        o_ep = torch.empty_like(x)
+        stack.run_ep(x, out=o_ep)
+        n_ep = max(2, min(args.steps, 5))
+        ms_ep = timed_steps(n_ep, lambda xin, o: stack.run_ep(xin, out=o), x, o_ep)
+        ep_contrast = {
+            "ms_per_step": ms_ep, "value": world * T / (ms_ep / 1e3), "unit": "tokens/s",
+            "asyncep_speedup": ms_ep / ms_step, "steps": n_ep,
+            "alltoall_bytes_per_layer_per_rank": 4 * K_ * (world - 1) / world * T * H_ * 2,
+            "note": "asyncep_ep_forward per layer: router + permute, per-expert count exchange + host sync, "
+                    "row AllToAll to the expert owners (ncclSend/Recv, on the compute stream), grouped GEMM, "
+                    "reverse AllToAll, combine; same tokens, weights and kernels as the headline"}
+        del o_ep
+        torch.cuda.empty_cache()
+
     # Eq. 1 (R11/R12): T in tokens/GPU with F = this run's grouped-GEMM rate and the
     # gather bandwidth probed at startup with the chosen transport (else assumed NVLink 5 peer copy).
     n_for_T = world if world > 1 else (emu if emu > 1 else 8)
@@ -639,6 +658,7 @@ def main():
         "layer_ms": step_layer_ms,
         "exposed_ag": exposed,
         "gather_transports": transports or None,
+        "ep_contrast": ep_contrast,
         "roofline": {"kernel": "grouped GEMM1 gate/up + SwiGLU (tcgen05)", "bound": "tensor",
                      "achieved": g1_tflops, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": g1_tflops / peak_tf if g1_tflops else None,

@@ -51,9 +51,6 @@ constexpr int RING = 8;
 
 enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // router: top-k <= 8 / <= 16
 
-#ifndef PLAIN_NSTG
-#define PLAIN_NSTG 1
-#endif
 #ifndef GEMM_WAITPROF
 #define GEMM_WAITPROF 0  // 1: the MMA / gather / producer threads printf their barrier-wait cycles (A/B only)
 #endif
@@ -64,23 +61,20 @@ enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // ro
 #define WP_DECL(n)
 #define WP_WAIT(acc, stmt) stmt;
 #endif
-#ifndef PROD2
-#define PROD2 1  // 1: without the fused gather, warp 3 issues the B (weight) loads and warp 0 the A loads
-#endif
-#ifndef EPI8
-#define EPI8 0  // 1: 8 epilogue warps on CTA-pair GEMMs (two per TMEM lane quadrant, split columns)
-#endif
-// Shared memory plan per (CTA group, epilogue mode).  With PLAIN_NSTG = 2 the plain epilogue
-// (GEMM2: four 64-column stores per tile) double-buffers its staging; its FP8 scales are then
-// read as warp-broadcast vector loads instead of an smem copy (the space goes to staging).
+// Without the fused gather, warp 3 issues the B (weight) loads and warp 0 the A loads (and runs the
+// scheduler): GEMM2's single producer spent ~40 % of its time issuing TMA loads.
+#define PROD2 1
+// Shared memory plan per (CTA group, epilogue mode): S-stage operand ring, one 32-row staging
+// buffer and one 256-scale buffer per epilogue warp, barriers, the tile_start prefix.
+// (Measured and dropped, S6: double-buffered staging, 8 epilogue warps.)
 template <int NCTA, int MODE>
 struct Cfg {
   static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
   static constexpr int STAGES = NCTA == 2 ? 6 : 4;
-  static constexpr int EW = (EPI8 && NCTA == 2 && (MODE == EPI_PLAIN || MODE == EPI_SWIGLU)) ? 8 : 4;
+  static constexpr int EW = 4;                // epilogue warps (one per TMEM lane quadrant)
   static constexpr int NTHR = 128 + 32 * EW;  // warps 0-3 roles, then EW epilogue warps
-  static constexpr int NSTG = (MODE == EPI_PLAIN && NCTA == 2 && EW == 4) ? PLAIN_NSTG : 1;
-  static constexpr int NSCL = ((MODE == EPI_PLAIN && NSTG == 2) || EW == 8) ? 0 : SCL_BYTES;
+  static constexpr int NSTG = 1;
+  static constexpr int NSCL = SCL_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + EW * NSTG * STG_BYTES +
                                  EW * NSCL + 512 + (kMaxExperts + 1) * sizeof(int32_t);
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -586,7 +580,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   } else if (warp >= 4) {
     const int ew = warp - 4;           // epilogue warp index (staging / scale buffers)
     const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad+32): this warp's rows
-    const int ch = ew >> 2;            // EW == 8: column half of the tile this warp stores
     uint8_t* stg = sStg + ew * C::NSTG * STG_BYTES;
     uint32_t chunk = 0;  // stores issued by this warp (staging buffer parity)
     int acc = 0;
@@ -634,10 +627,10 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
                    (ge >= p.own_lo && ge < p.own_hi ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
                                                     : p.b_scale_base + (size_t)ge * p.expert_bytes)) +
                nt * 256;
-          if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, 256, lane);
+          sb = stage_scales(sScl + ew * 256, sb, 256, lane);
         }
 #pragma unroll 1
-        for (int c0 = C::EW == 8 ? 64 * ch : 0; c0 < (C::EW == 8 ? 64 * ch + 64 : 128); c0 += 64) {
+        for (int c0 = 0; c0 < 128; c0 += 64) {
           uint32_t o[32];
           uint32_t amax2 = 0;  // |bf16| bit patterns of both halves: unsigned order = magnitude order
           uint32_t gg[2][32], uu[2][32];  // the chunk's 64 gate + 64 up columns, one wait
@@ -647,7 +640,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
             tmem_ld32(tb + 128 + c0 + 32 * half, uu[half]);
           }
           tmem_ld_wait();
-          if (c0 + 64 >= (C::EW == 8 ? 64 * ch + 64 : 128)) release();  // last TMEM read of the tile
+          if (c0 + 64 >= 128) release();  // last TMEM read of the tile
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             const uint32_t(&g)[32] = gg[half];
@@ -662,14 +655,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               }
               if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
                 const int cc = c0 + 32 * half + 4 * q;
-                float4 sg, su;
-                if (C::NSCL > 0) {
-                  sg = ld_shared_f4(smem_u32(sb) + 4 * cc);
-                  su = ld_shared_f4(smem_u32(sb) + 4 * cc + 512);
-                } else {
-                  sg = __ldg(reinterpret_cast<const float4*>(sb + cc));
-                  su = __ldg(reinterpret_cast<const float4*>(sb + 128 + cc));
-                }
+                const float4 sg = ld_shared_f4(smem_u32(sb) + 4 * cc);
+                const float4 su = ld_shared_f4(smem_u32(sb) + 4 * cc + 512);
                 float s0, s1, s2, s3, t0, t1, t2, t3;
                 mul2(s0, s1, sa, sa, sg.x, sg.y);
                 mul2(s2, s3, sa, sa, sg.z, sg.w);
@@ -709,10 +696,10 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
                    (ge >= p.own_lo && ge < p.own_hi ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
                                                     : p.b_scale_base + (size_t)ge * p.expert_bytes)) +
                nt * p.BN;
-          if (C::NSCL > 0) sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
+          sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
         }
-        const int cbeg = C::EW == 8 ? 128 * ch : 0;
-        const int cend = min(C::EW == 8 ? min(128 * ch + 128, p.BN) : p.BN, max(p.n_out - nt * p.BN, 0));
+        const int cbeg = 0;
+        const int cend = min(p.BN, max(p.n_out - nt * p.BN, 0));
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cend; c0 += 64) {
           uint32_t o[32];
@@ -731,8 +718,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               for (int j = 0; j < 4; ++j) v[j] = __uint_as_float(r[4 * q + j]);
               if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
                 const int cc = c0 + 32 * half + 4 * q;
-                const float4 sv = C::NSCL > 0 ? ld_shared_f4(smem_u32(sb) + 4 * cc)
-                                              : __ldg(reinterpret_cast<const float4*>(sb + cc));
+                const float4 sv = ld_shared_f4(smem_u32(sb) + 4 * cc);
                 float s0, s1, s2, s3;
                 mul2(s0, s1, sa, sa, sv.x, sv.y);
                 mul2(s2, s3, sa, sa, sv.z, sv.w);
