@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--ctas", default="296,148,74")
     ap.add_argument("--link-gbs", type=float, default=770.0)
     ap.add_argument("--pairs", type=int, default=8)
+    ap.add_argument("--prio", type=int, default=0, help="compute-stream priority (0 = default, -1/-2 higher)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     T = args.tokens
@@ -44,16 +45,18 @@ def main():
     rf = lambda l: synth.router_weight(E, H, 0, l, device=dev)
     ef = lambda l, ex: gen(E, H, h, 0, l, device=dev, experts=ex)
     flags = A.FLAG_STAGE_TIMING
-    res = MoEStack(L, E, K, H, h, T, rf, ef, world_size=1, flags=flags, device=dev, fp8=args.fp8)
+    cs = torch.cuda.Stream(dev, priority=args.prio) if args.prio else torch.cuda.current_stream(dev)
+    torch.cuda.set_stream(cs)
+    res = MoEStack(L, E, K, H, h, T, rf, ef, world_size=1, flags=flags, device=dev, fp8=args.fp8, compute_stream=cs)
     gat = MoEStack(L, E, K, H, h, T, rf, ef, world_size=args.N, rank=0, flags=flags, device=dev, fp8=args.fp8,
-                   compute_stream=res.compute_stream)
+                   compute_stream=cs)
     shards = gat.peer_shards()
     A.asyncep_set_link_emulation(gat.ctx, args.link_gbs * 1e9)
     x = synth.tokens(T, H, 17, device=dev)
     o_r, o_g = torch.empty_like(x), torch.empty_like(x)
-    cs = res.compute_stream
 
     def step_ms(fn):
+        cs = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(cs)
@@ -86,13 +89,13 @@ def main():
         exp_layer = (mg - mr) / (L - 1)
         print(json.dumps({
             "fp8": args.fp8, "tokens": T, "N": args.N, "link_gbs": args.link_gbs, "copy_ctas": ctas,
+            "compute_priority": args.prio,
             "step_ms_resident": mr, "step_ms_gathered": mg, "exposed_ms_per_layer": exp_layer,
             "exposed_frac_of_layer": exp_layer / (mr / L),
             "bitwise_equal": bool(torch.equal(o_r.view(torch.int16), o_g.view(torch.int16))),
             "stage_ms_resident": {k: v / max(nr, 1) for k, v in sr.items()},
             "stage_ms_gathered": {k: v / max(ng, 1) for k, v in sg.items()},
             "all_resident": tr, "all_gathered": tg, "clocks": clk}), flush=True)
-
 
 if __name__ == "__main__":
     main()
