@@ -197,7 +197,7 @@ ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void*
 ASYNCEP_API asyncep_status asyncep_set_gather_transport(asyncep_ctx* ctx, int32_t transport, int32_t reserve_sms);
 
 /* Measurement knob: CTAs of the co-resident copy kernel (0 = default: ASYNCEP_GATHER_CTAS, else
- * 2 per SM).  Fewer CTAs keep fewer warps beside the GEMMs; NVLink latency needs ~1 MB in flight. */
+ * 1 per SM).  More CTAs keep more warps beside the GEMMs; NVLink latency needs ~1 MB in flight. */
 ASYNCEP_API asyncep_status asyncep_set_gather_copy_ctas(asyncep_ctx* ctx, int32_t ctas);
 
 /*

@@ -44,13 +44,16 @@ int default_copy_mode() {
   const char* e = getenv("ASYNCEP_GATHER_COPY");
   return (e && (!strcmp(e, "ce") || !strcmp(e, "memcpy"))) ? ASYNCEP_GATHER_COPY_ENGINE : ASYNCEP_GATHER_COPY_KERNEL;
 }
-// copy-kernel CTAs: ASYNCEP_GATHER_CTAS, else per_sm x SMs (asyncep_set_gather_copy_ctas at run time)
+// copy-kernel CTAs: ASYNCEP_GATHER_CTAS, else one per SM (asyncep_set_gather_copy_ctas at run time).
+// Interleaved same-box A/B of the 8-rank emulation at 32K tokens/GPU (profiles/r02/interf_*.jsonl):
+// one CTA per SM exposes 1.5-4.7 % (BF16) / 3.8-6.7 % (FP8) of the layer, two per SM 4.5-6.0 % /
+// 7.6-9.3 % (GEMM2 +8 % beside them), 96 CTAs no better, 37 too few to keep the link rate.
 int default_copy_ctas() {
   int dev = 0, n = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   const char* e = getenv("ASYNCEP_GATHER_CTAS");
-  return (e && *e && atoi(e) > 0) ? atoi(e) : 2 * n;
+  return (e && *e && atoi(e) > 0) ? atoi(e) : n;
 }
 cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, uint64_t min_ns = 0,
                         int mode = ASYNCEP_GATHER_COPY_KERNEL, int ctas = 0) {

@@ -898,6 +898,15 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
     const uint32_t box[3] = {kb, (uint32_t)(256 / ncta), 1};
     if (!encode_tmap(&m.wgu, dt, 3, layer, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
+  if (ncta == 2 && h % 128 == 0) {
+    const uint64_t dims[5] = {(uint64_t)H, 128, 2, (uint64_t)(2 * h / 256), (uint64_t)E};
+    const uint64_t strides[4] = {(uint64_t)H * b, (uint64_t)128 * H * b, (uint64_t)256 * H * b,
+                                 (uint64_t)expert_bytes};
+    const uint32_t box[5] = {kb, 16, 2, 1, 1};
+    if (!encode_tmap(&m.wgu_swap, dt, 5, layer, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  } else {
+    m.wgu_swap = m.wgu;
+  }
   {
     const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * b;
     const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};

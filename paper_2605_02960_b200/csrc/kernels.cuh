@@ -61,6 +61,8 @@ struct GroupedArgs {
   const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kRowAlign)
   const int32_t* counts;     // [E] rows per expert
   int E;
+  int swap_max = 0;          // > 0: an expert's last row tile with <= swap_max rows runs swap-AB
+                             // (weights as M = 256, its tokens as N = rows rounded up to 16)
   int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
   int* sched = nullptr;      // [>= 3] dynamic tile counters, zeroed before each forward:
                              // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
@@ -80,6 +82,10 @@ void launch_gemm2_simt(const GroupedArgs& g, const bf16* act, const uint8_t* lay
 struct GemmMaps {
   CUtensorMap wgu;   // 3D {H, 2h, E}, box {128 B, 256/NCTA rows, 1}
   CUtensorMap wd;    // 3D {h, H, E},  box {128 B, BN2/NCTA rows, 1}
+  // swap-AB tail tiles of GEMM1 (weights as the MMA's M operand): W_gu viewed as
+  // 5D {H, 128 (j in block), 2 (gate/up), 2h/256 (block), E}, box {128 B, 16, 2, 1, 1} =
+  // 16 gate rows then the matching 16 up rows (one TMEM lane quadrant per box)
+  CUtensorMap wgu_swap;
   bool fp8 = false;
 };
 // Gathered layers: experts [lo, hi) (this rank's own shard) are read by the GEMMs straight from
