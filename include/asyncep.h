@@ -64,6 +64,8 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
 #define ASYNCEP_FLAG_XPERM           0x10 /* materialise X_perm and TMA-load it (default: GEMM1 gathers
                                                the token rows itself through src_tok, cp.async)     */
 #define ASYNCEP_FLAG_OFFLOAD         0x20 /* NEXT-2: expert_shard[l] may be NULL for offloaded layers  */
+#define ASYNCEP_FLAG_NO_SWAP_TAILS   0x40 /* compute every expert's last row tile as a padded 256-row
+                                               tile (default: swap-AB tail tiles, S6)      */
 
 typedef struct {
   int32_t num_layers;      /* L                                                         */

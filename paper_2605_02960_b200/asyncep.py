@@ -27,6 +27,7 @@ FLAG_STAGE_TIMING = 0x4
 FLAG_SIMT_ROUTER = 0x8
 FLAG_XPERM = 0x10
 FLAG_OFFLOAD = 0x20
+FLAG_NO_SWAP_TAILS = 0x40
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 
 

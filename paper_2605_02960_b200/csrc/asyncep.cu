@@ -66,6 +66,16 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
   return cudaMemcpyAsync(dst, src, n, cudaMemcpyDefault, st);
 }
 
+// Swap-AB tail tiles of the grouped GEMMs (gemm_tc.cu): an expert's last 256-row tile holding at
+// most this many rows runs with the weights as M and its tokens as N.  ASYNCEP_SWAP_MAX: 0 = off.
+int swap_max_rows() {
+  static const int v = [] {
+    const char* e = getenv("ASYNCEP_SWAP_MAX");
+    return (e && *e) ? atoi(e) : 240;
+  }();
+  return v;
+}
+
 // NVTX ranges around the host-side enqueue of each call (the paper's gated per-layer hooks,
 // PAPER.md:650-655); free when no tool is attached.
 struct NvtxRange {
@@ -791,6 +801,7 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   }
   const aep::OwnShard* own = use_own ? &own_sh : nullptr;
   aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
+  g.swap_max = (cf.flags & ASYNCEP_FLAG_NO_SWAP_TAILS) ? 0 : swap_max_rows();
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

@@ -76,7 +76,7 @@ struct Cfg {
   static constexpr int NSTG = 1;
   static constexpr int NSCL = SCL_BYTES;
   static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + EW * NSTG * STG_BYTES +
-                                 EW * NSCL + 512 + (kMaxExperts + 1) * sizeof(int32_t);
+                                 EW * NSCL + 512 + (2 * kMaxExperts + 1) * sizeof(int32_t);
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
@@ -112,6 +112,13 @@ struct TcArgs {
   int top_k, norm_topk;
   int32_t* ids;
   float* w;
+  // swap-AB tail tiles (grouped CTA-pair GEMMs): an expert's last row tile holding r <= swap_max
+  // rows runs with the weights as the M = 256 operand and its r tokens (rounded up to 16) as N, so
+  // the MMA does r/256 of a full tile's work instead of computing padding rows.  The epilogue
+  // writes out_ptr (row stride n_out) directly, transposing through the staging buffer.
+  const int32_t* counts;
+  int swap_max;
+  bf16* out_ptr;
 };
 
 // linear tile index -> (row tile, n tile)
@@ -135,6 +142,16 @@ __device__ __forceinline__ int find_expert(const int32_t* ts, int E, int mt) {
     if (ts[mid] <= mt) lo = mid; else hi = mid - 1;
   }
   return lo;
+}
+
+// Swap-AB classification of row tile mt of expert e (s_ts: row-tile prefix, s_cnt: rows per
+// expert, TM rows per tile): the expert's last tile with r <= swap_max rows -> ntok = r rounded up
+// to 16 (the MMA's N), else 0 (a normal tile).
+__device__ __forceinline__ int swap_ntok(const int32_t* s_ts, const int32_t* s_cnt, int e, int mt, int TM,
+                                         int swap_max) {
+  if (swap_max <= 0 || mt != s_ts[e + 1] - 1) return 0;
+  const int r = s_cnt[e] - (mt - s_ts[e]) * TM;
+  return (r > 0 && r <= swap_max) ? (r + 15) & ~15 : 0;
 }
 
 // Router epilogue, one thread = one token row of the logits tile (E <= 256 fp32 columns
@@ -296,6 +313,7 @@ template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCTA, MODE>::NTHR == 256 ? 224 : 168))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_b2,
+                   const __grid_constant__ CUtensorMap map_bs, const __grid_constant__ CUtensorMap map_bs2,
                    const TcArgs p) {
   using C = Cfg<NCTA, MODE>;
   constexpr int STAGES = C::STAGES;
@@ -315,6 +333,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   int32_t* sring = reinterpret_cast<int32_t*>(afull + STAGES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sring + RING);
   int32_t* s_ts = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(full) + 512);
+  int32_t* s_cnt = s_ts + kMaxExperts + 1;
 
   const int warp = warp_id(), lane = lane_id();
   const uint32_t rank = NCTA == 2 ? cluster_ctarank() : 0;
@@ -330,7 +349,12 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     }
   } else {
     for (int i = threadIdx.x; i <= p.E; i += C::NTHR) s_ts[i] = p.tile_start[i] * p.ts_scale;
+    if (p.swap_max > 0)
+      for (int i = threadIdx.x; i < p.E; i += C::NTHR) s_cnt[i] = p.counts[i];
   }
+  // swap-AB tail tiles: CTA-pair grouped GEMMs with full 256-row weight tiles only
+  const int swap_max = (NCTA == 2 && (MODE == EPI_SWIGLU || MODE == EPI_PLAIN) && p.dense_rows <= 0 &&
+                        p.BN == 256 && p.group_mod == 0) ? p.swap_max : 0;
   const bool gather = p.gather_rows != nullptr;
   if (warp == 0 && lane == 0) {
     if (!gather) tma_prefetch_desc(&map_a);
@@ -407,12 +431,17 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         int mt, nt;
         decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
         int e = find_expert(s_ts, G, mt);
+        const int ntok = swap_ntok(s_ts, s_cnt, e, mt, TM, swap_max);
         if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
         const bool own_e = e >= p.own_lo && e < p.own_hi;
         const CUtensorMap* mb = own_e ? &map_b2 : &map_b;
+        const CUtensorMap* mbs = own_e ? &map_bs2 : &map_bs;
         if (own_e) e -= p.own_lo;
-        const int row0 = mt * TM + (int)rank * BM;
+        // swap: this CTA's ntok/2 token rows go to the B stage, its 128 weight rows to the A stage
+        const int row0 = ntok ? mt * TM + (int)rank * (ntok >> 1) : mt * TM + (int)rank * BM;
         const int brow = nt * p.BN + (int)rank * bn_cta;
+        uint8_t* const dA = ntok ? sB : sA;  // token operand
+        uint8_t* const dB = ntok ? sA : sB;  // weight operand
         for (int kb = 0; kb < nkb; ++kb) {
           WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
 #if GEMM_WAITPROF
@@ -421,11 +450,21 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           if (NCTA == 2) {
             if (leader) mbar_arrive_expect_tx(&full[stage], tx);
             else mbar_arrive_cluster_relaxed(&full[stage], 0);
+            static_assert(A_BYTES == C::B_BYTES_MAX || NCTA == 1, "swap-AB exchanges the A and B stages");
             if (do_a) {
-              if (p.pol_a == 3) tma_load_2d_pair(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
-              else tma_load_2d_pair_hint(sA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
+              if (p.pol_a == 3) tma_load_2d_pair(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
+              else tma_load_2d_pair_hint(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            if (do_b) tma_load_3d_pair(sB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+            if (do_b) {
+              if (ntok && MODE == EPI_SWIGLU) {  // 4 boxes of [16 gate | 16 up] rows: j = rank*64 + 16i + [0,16)
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  tma_load_5d_pair(dB + stage * A_BYTES + i * 4096, mbs, &full[stage], kb * KB_ELEMS,
+                                   (int)rank * 64 + 16 * i, 0, nt, e, pol_b);
+              } else {
+                tma_load_3d_pair(dB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
+              }
+            }
           } else {
             mbar_arrive_expect_tx(&full[stage], tx);
             if (do_a) {
@@ -452,7 +491,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     // the chunk lands at its 128-B-swizzle position j ^ (row & 7) (row & 7 is fixed per thread).
     const int gt = (int)threadIdx.x - 64;
     const int rr = gt >> 3, ch = gt & 7;
-    const uint32_t dst0 = smem_u32(sA) + (uint32_t)(rr * 128 + ((ch ^ (rr & 7)) << 4));
+    const uint32_t off0 = (uint32_t)(rr * 128 + ((ch ^ (rr & 7)) << 4));
+    // swap-AB tail tiles: this CTA's ntok/2 token rows go to the B stage (the MMA's N operand)
     int stage = 0;
     uint32_t phase = 0;
     const bool arm = NCTA == 2 && !leader && warp == 2;  // peer: this warp arms the ring slots
@@ -461,13 +501,17 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, arm);
       return __shfl_sync(0xffffffffu, t, 0);
     };
-    auto load_rows = [&](int t, int32_t (&tok)[16]) {  // the tile's 16 row indices of this thread
+    // the tile's row indices of this thread (16, or ntok/16 for a swap tile) and its stage base
+    auto load_rows = [&](int t, int32_t (&tok)[16], int& nrow, uint32_t& base) {
       if (t >= total) return;
       int mt, nt;
       decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
-      const int row0 = mt * TM + (int)rank * BM;
+      const int ntok = swap_ntok(s_ts, s_cnt, find_expert(s_ts, G, mt), mt, TM, swap_max);
+      const int row0 = ntok ? mt * TM + (int)rank * (ntok >> 1) : mt * TM + (int)rank * BM;
+      nrow = ntok ? ntok >> 4 : 16;
+      base = smem_u32(ntok ? sB : sA) + off0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) tok[i] = __ldg(p.gather_rows + row0 + rr + 8 * i);
+      for (int i = 0; i < 16; ++i) tok[i] = i < nrow ? __ldg(p.gather_rows + row0 + rr + 8 * i) : 0;
     };
     WP_DECL(wp_e)
 #if GEMM_WAITPROF
@@ -475,24 +519,36 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #endif
     int t = next_tile(0);
     int32_t tok[16];
-    load_rows(t, tok);
+    int nrow = 16;
+    uint32_t base = smem_u32(sA) + off0;
+    load_rows(t, tok, nrow, base);
     for (int seq = 0;; ++seq) {
       if (t >= total) break;
       const int tn = next_tile(seq + 1);  // published one tile ahead: prefetch its row indices
       int32_t tok_n[16];
-      load_rows(tn, tok_n);
+      int nrow_n = 16;
+      uint32_t base_n = base;
+      load_rows(tn, tok_n, nrow_n, base_n);
       const uint8_t* src[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) src[i] = p.gather_src + (int64_t)tok[i] * p.gather_ld + ch * 16;
       for (int kb = 0; kb < nkb; ++kb) {
         WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
-        const uint32_t dst = dst0 + (uint32_t)(stage * A_BYTES);
+        const uint32_t dst = base + (uint32_t)(stage * A_BYTES);
+        if (nrow == 16) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+          for (int i = 0; i < 16; ++i) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (i < nrow) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+        }
         cp_async_mbar_arrive_noinc(&afull[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
       t = tn;
+      nrow = nrow_n;
+      base = base_n;
 #pragma unroll
       for (int i = 0; i < 16; ++i) tok[i] = tok_n[i];
     }
@@ -535,7 +591,15 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       for (int seq = 0;; ++seq) {
         int t = 0;
         WP_WAIT(wp_s, if (lane == 0) t = sched_consume<NCTA>(ring, seq, true, false))
-        if (__shfl_sync(0xffffffffu, t, 0) >= total) break;
+        t = __shfl_sync(0xffffffffu, t, 0);
+        if (t >= total) break;
+        uint32_t id = idesc;
+        if (swap_max > 0) {  // swap-AB tail: M = 256 weight rows, N = the tile's tokens
+          int mt, nt;
+          decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+          const int ntok = swap_ntok(s_ts, s_cnt, find_expert(s_ts, G, mt), mt, TM, swap_max);
+          if (ntok) id = make_idesc(TM, ntok, !F8);
+        }
         WP_WAIT(wp_t, mbar_wait(&tempty[acc], acc_phase ^ 1))
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -551,11 +615,11 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
             for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 B of K (16 bf16 / 32 e4m3) per 128-B k-block
               const uint32_t acc_on = (kb | k) != 0 ? 1u : 0u;
               if (F8) {
-                if (NCTA == 2) mma_f8_2(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
-                else mma_f8(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+                if (NCTA == 2) mma_f8_2(d, ad + 2 * k, bd + 2 * k, id, acc_on);
+                else mma_f8(d, ad + 2 * k, bd + 2 * k, id, acc_on);
               } else {
-                if (NCTA == 2) mma_bf16_2(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
-                else mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, acc_on);
+                if (NCTA == 2) mma_bf16_2(d, ad + 2 * k, bd + 2 * k, id, acc_on);
+                else mma_bf16(d, ad + 2 * k, bd + 2 * k, id, acc_on);
               }
             }
             if (NCTA == 2) tc_commit2_mc(&empty[stage], 0x3);
@@ -611,7 +675,113 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         }
         released = true;
       };
-      if (MODE == EPI_ROUTER || MODE == EPI_ROUTER16) {
+      const int ntok = swap_max > 0 ? swap_ntok(s_ts, s_cnt, find_expert(s_ts, G, mt), mt, TM, swap_max) : 0;
+      if ((MODE == EPI_SWIGLU || MODE == EPI_PLAIN) && ntok) {
+        // Swap-AB tail tile: TMEM lane = weight row of this CTA, column c = token row mt*TM + c.
+        // GEMM1: lanes [0,16) of the quadrant hold gate rows j = jq, lanes [16,32) the up rows of
+        // the same j (the [16 gate | 16 up] TMA boxes); GEMM2: lane = output column.  The values are
+        // transposed through the warp's staging buffer and written to out_ptr row by row.
+        const int trow0 = mt * TM;  // the tile's first (token) row
+        const bool upper = lane >= 16;
+        int ge = find_expert(s_ts, G, mt);
+        const bool own_g = ge >= p.own_lo && ge < p.own_hi;
+        float* tsc = sScl + ew * 256;  // FP8: the tile's token (row) scales
+        const float* wsc = nullptr;    // FP8: this expert's weight scales of the N tile
+        if (F8) {
+          wsc = reinterpret_cast<const float*>(own_g ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
+                                                     : p.b_scale_base + (size_t)ge * p.expert_bytes) + nt * 256;
+          __syncwarp();
+          for (int i = lane; i < ntok; i += 32)
+            tsc[i] = p.a_scale[(MODE == EPI_SWIGLU && gather) ? __ldg(p.gather_rows + trow0 + i) : trow0 + i];
+          __syncwarp();
+        }
+        if (lane == 0) bulk_wait_read0();  // earlier TMA stores have finished reading the staging buffer
+        __syncwarp();
+        if (MODE == EPI_SWIGLU) {
+          const int jq = (int)rank * 64 + quad * 16 + (lane & 15);  // act column within the N tile
+          float sg = 1.f, su = 1.f;
+          if (F8) {
+            sg = __ldg(wsc + jq);
+            su = __ldg(wsc + 128 + jq);
+          }
+          bf16* outc = p.out_ptr + nt * 128 + (int)rank * 64 + quad * 16;
+#pragma unroll 1
+          for (int c0 = 0; c0 < ntok; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tb + c0, v);
+            tmem_ld_wait();
+            if (c0 + 32 >= ntok) release();
+            const int cb = upper ? 16 : 0;  // this lane's 16 token columns of the chunk
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              float g[2], u[2];
+#pragma unroll
+              for (int q2 = 0; q2 < 2; ++q2) {
+                const uint32_t send = upper ? v[i + q2] : v[16 + i + q2];
+                const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                g[q2] = __uint_as_float(upper ? recv : v[i + q2]);
+                u[q2] = __uint_as_float(upper ? v[16 + i + q2] : recv);
+                if (F8) {
+                  const float ts = tsc[c0 + cb + i + q2];
+                  g[q2] *= sg * ts;
+                  u[q2] *= su * ts;
+                }
+              }
+              float a0, a1;
+              mul2(a0, a1, silu_f(g[0]), silu_f(g[1]), u[0], u[1]);
+              const uint32_t pk = pack_bf16x2(a0, a1);
+              // staging [32 tokens][16 act columns] bf16
+              *reinterpret_cast<uint16_t*>(stg + (cb + i) * 32 + (lane & 15) * 2) = (uint16_t)(pk & 0xffffu);
+              *reinterpret_cast<uint16_t*>(stg + (cb + i + 1) * 32 + (lane & 15) * 2) = (uint16_t)(pk >> 16);
+            }
+            __syncwarp();
+            {  // lane = token row c0 + lane: 16 act columns = 32 B
+              const uint4* src = reinterpret_cast<const uint4*>(stg + lane * 32);
+              uint4* dst = reinterpret_cast<uint4*>(outc + (int64_t)(trow0 + c0 + lane) * p.n_out);
+              dst[0] = src[0];
+              dst[1] = src[1];
+              if (F8) {  // per-token max |act| of this warp's 16 columns (bf16 magnitudes)
+                const uint16_t* r16 = reinterpret_cast<const uint16_t*>(stg + lane * 32);
+                uint32_t m = 0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) m = max(m, (uint32_t)(r16[j] & 0x7fffu));
+                if (c0 + lane < ntok) atomicMax(p.amax_out + trow0 + c0 + lane, m << 16);
+              }
+            }
+            __syncwarp();
+          }
+        } else {
+          const int ncol = (int)rank * 128 + quad * 32 + lane;  // output column within the N tile
+          const float sw = F8 ? __ldg(wsc + ncol) : 1.f;
+          bf16* outc = p.out_ptr + nt * p.BN + (int)rank * 128 + quad * 32;
+#pragma unroll 1
+          for (int c0 = 0; c0 < ntok; c0 += 32) {
+            uint32_t v[32];
+            tmem_ld32(tb + c0, v);
+            tmem_ld_wait();
+            if (c0 + 32 >= ntok) release();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float x0 = __uint_as_float(v[i]), x1 = __uint_as_float(v[i + 1]);
+              if (F8) {
+                x0 *= sw * tsc[c0 + i];
+                x1 *= sw * tsc[c0 + i + 1];
+              }
+              const uint32_t pk = pack_bf16x2(x0, x1);
+              // staging [32 tokens][32 output columns] bf16
+              *reinterpret_cast<uint16_t*>(stg + i * 64 + lane * 2) = (uint16_t)(pk & 0xffffu);
+              *reinterpret_cast<uint16_t*>(stg + (i + 1) * 64 + lane * 2) = (uint16_t)(pk >> 16);
+            }
+            __syncwarp();
+            const uint4* src = reinterpret_cast<const uint4*>(stg + lane * 64);
+            uint4* dst = reinterpret_cast<uint4*>(outc + (int64_t)(trow0 + c0 + lane) * p.n_out);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = src[j];
+            __syncwarp();
+          }
+        }
+        (void)ge;
+      } else if (MODE == EPI_ROUTER || MODE == EPI_ROUTER16) {
         const int row = wrow0 + lane;
         router_epilogue<MODE == EPI_ROUTER ? 8 : 16>(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows,
                                                      p.ids + (int64_t)row * p.top_k, p.w + (int64_t)row * p.top_k);
@@ -757,7 +927,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 
 template <int MODE, int NCTA, bool F8 = false>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
-                 cudaStream_t s, const CUtensorMap* mb2 = nullptr) {
+                 cudaStream_t s, const CUtensorMap* mb2 = nullptr, const CUtensorMap* mbs = nullptr,
+                 const CUtensorMap* mbs2 = nullptr) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -775,7 +946,8 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, mb2 ? *mb2 : mb, a);
+  const CUtensorMap& b2 = mb2 ? *mb2 : mb;
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, b2, mbs ? *mbs : mb, mbs2 ? *mbs2 : b2, a);
 }
 
 // Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
@@ -792,7 +964,8 @@ int grouped_raster() {
 void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo,
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
                     const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false,
-                    const void* gather_src = nullptr, int64_t gather_ld = 0, const OwnShard* own = nullptr) {
+                    const void* gather_src = nullptr, int64_t gather_ld = 0, const OwnShard* own = nullptr,
+                    const CUtensorMap* mbs = nullptr, bf16* out = nullptr) {
   static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
@@ -810,10 +983,15 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.gather_src = static_cast<const uint8_t*>(gather_src);
   a.gather_ld = gather_ld;
   const CUtensorMap* mb2 = nullptr;
+  const CUtensorMap* mbs2 = nullptr;
+  a.counts = g.counts;
+  a.swap_max = (ncta == 2 && out && g.counts) ? g.swap_max : 0;
+  a.out_ptr = out;
   if (own && own->maps && own->hi > own->lo) {
     a.own_lo = own->lo;
     a.own_hi = own->hi;
     mb2 = gemm2 ? &own->maps->wd : &own->maps->wgu;
+    mbs2 = gemm2 ? &own->maps->wd : &own->maps->wgu_swap;
     if (f8) a.b_scale_base_own = own->base + (gemm2 ? f8->sd_off : f8->sgu_off);
   }
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
@@ -828,11 +1006,11 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
   const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
   if (f8) {  // FP8 experts: CTA pairs only
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2);
-    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
+    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
   } else if (ncta == 2) {
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s, mb2);
-    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s, mb2);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
+    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
   } else {
     if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 1>(a, ma, mb, mo, grid, s, mb2);
     else launch_mode<EPI_PLAIN, 1>(a, ma, mb, mo, grid, s, mb2);
@@ -927,7 +1105,7 @@ bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
   const int64_t ld = (int64_t)H * (f8 ? 1 : 2);
   const CUtensorMap& ma = f8 ? am.xq : am.xperm;
   launch_grouped(g, ma, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s,
-                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own);
+                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own, &wm.wgu_swap, act);
   (void)T;
   return true;
 }
@@ -936,7 +1114,7 @@ void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
                      int num_sms, cudaStream_t s, const F8Args* f8, const OwnShard* own) {
   const int bn = am.bn2;
   launch_grouped(g, f8 ? am.aq : am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s,
-                 nullptr, f8, true, nullptr, 0, own);
+                 nullptr, f8, true, nullptr, 0, own, &wm.wd, yperm);
 }
 
 // ------------------------------------------------------------------ dense GEMM (NEXT-3 projections)

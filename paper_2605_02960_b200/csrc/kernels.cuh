@@ -61,12 +61,12 @@ struct GroupedArgs {
   const int32_t* tile_start; // [E+1] prefix of ceil(n_e / kRowAlign)
   const int32_t* counts;     // [E] rows per expert
   int E;
-  int swap_max = 0;          // > 0: an expert's last row tile with <= swap_max rows runs swap-AB
-                             // (weights as M = 256, its tokens as N = rows rounded up to 16)
   int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
   int* sched = nullptr;      // [>= 3] dynamic tile counters, zeroed before each forward:
                              // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
   int group_mod = 0;         // > 0: group g uses expert g % group_mod of the weight blob
+  int swap_max = 0;          // > 0: an expert's last row tile with <= swap_max rows runs swap-AB
+                             // (weights as M = 256, its tokens as N = rows rounded up to 16)
 };
 // rows of the permuted buffers for T tokens: T*k + E*(kRowAlign-1), rounded up to kRowAlign
 inline int64_t perm_rows(int64_t T, int k, int E) {
