@@ -67,13 +67,17 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
 }
 
 // Swap-AB tail tiles of the grouped GEMMs (gemm_tc.cu): an expert's last 256-row tile holding at
-// most this many rows runs with the weights as M and its tokens as N.  ASYNCEP_SWAP_MAX: 0 = off.
-int swap_max_rows() {
-  static const int v = [] {
-    const char* e = getenv("ASYNCEP_SWAP_MAX");
-    return (e && *e) ? atoi(e) : 240;
-  }();
-  return v;
+// most this many rows runs with the weights as M and its tokens as N.  ASYNCEP_SWAP_MAX (GEMM1 and
+// BF16 GEMM2) / ASYNCEP_SWAP_MAX_F8G2 (FP8 GEMM2, whose short K = h bytes leaves the swap epilogue
+// exposed: +8 % GEMM2 at 240, profiles/r02/swap/); 0 = off.
+int env_rows(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+int swap_max_rows(bool fp8_gemm2) {
+  static const int g = env_rows("ASYNCEP_SWAP_MAX", 240);
+  static const int f = env_rows("ASYNCEP_SWAP_MAX_F8G2", 128);
+  return fp8_gemm2 ? f : g;
 }
 
 // NVTX ranges around the host-side enqueue of each call (the paper's gated per-layer hooks,
@@ -801,7 +805,9 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   }
   const aep::OwnShard* own = use_own ? &own_sh : nullptr;
   aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
-  g.swap_max = (cf.flags & ASYNCEP_FLAG_NO_SWAP_TAILS) ? 0 : swap_max_rows();
+  const bool swap_on = !(cf.flags & ASYNCEP_FLAG_NO_SWAP_TAILS);
+  g.swap_max = swap_on ? swap_max_rows(false) : 0;
+  g.swap_max2 = swap_on ? swap_max_rows(cf.expert_dtype == ASYNCEP_FP8_E4M3) : 0;
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

@@ -985,7 +985,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   const CUtensorMap* mb2 = nullptr;
   const CUtensorMap* mbs2 = nullptr;
   a.counts = g.counts;
-  a.swap_max = (ncta == 2 && out && g.counts) ? g.swap_max : 0;
+  a.swap_max = (ncta == 2 && out && g.counts) ? (gemm2 ? g.swap_max2 : g.swap_max) : 0;
   a.out_ptr = out;
   if (own && own->maps && own->hi > own->lo) {
     a.own_lo = own->lo;

@@ -66,7 +66,8 @@ struct GroupedArgs {
                              // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
   int group_mod = 0;         // > 0: group g uses expert g % group_mod of the weight blob
   int swap_max = 0;          // > 0: an expert's last row tile with <= swap_max rows runs swap-AB
-                             // (weights as M = 256, its tokens as N = rows rounded up to 16)
+                             // (weights as M = 256, its tokens as N = rows rounded up to 16): GEMM1
+  int swap_max2 = 0;         // the same for GEMM2
 };
 // rows of the permuted buffers for T tokens: T*k + E*(kRowAlign-1), rounded up to kRowAlign
 inline int64_t perm_rows(int64_t T, int k, int E) {
