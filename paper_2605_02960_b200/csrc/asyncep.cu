@@ -76,7 +76,7 @@ int env_rows(const char* name, int dflt) {
 }
 int swap_max_rows(bool fp8_gemm2) {
   static const int g = env_rows("ASYNCEP_SWAP_MAX", 240);
-  static const int f = env_rows("ASYNCEP_SWAP_MAX_F8G2", 128);
+  static const int f = env_rows("ASYNCEP_SWAP_MAX_F8G2", 0);
   return fp8_gemm2 ? f : g;
 }
 
