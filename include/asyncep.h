@@ -88,10 +88,11 @@ typedef struct {
  *   BF16:  [ W_gu : 2h x H bf16 | W_down : H x h bf16 ]
  *   FP8 :  [ W_gu : 2h x H e4m3 | W_down : H x h e4m3 | s_gu : 2h fp32 | s_down : H fp32 ]
  * both matrices row-major with the contraction dim (K) contiguous ("K-major").  W_gu rows
- * are gate/up interleaved per 128-row block: rows [256b, 256b+128) are gate rows
- * [128b, 128b+128), rows [256b+128, 256b+256) are the matching up rows, so one
- * 256-wide GEMM N-tile holds matching gate and up columns (SwiGLU fuses into its
- * epilogue).  FP8 scales are per output row (dequantised weight = code * scale).
+ * are gate/up interleaved in groups of 16: in 256-row block b, the 32-row group g holds gate
+ * rows j = 128b + 16g + [0, 16) followed by the matching up rows, so one 256-wide GEMM N-tile
+ * holds matching gate and up columns (SwiGLU fuses into its epilogue) and, with the weights as
+ * the MMA's M operand (swap-AB tail tiles), each 32-lane TMEM quadrant holds 16 gate rows and
+ * their up rows.  FP8 scales are per output row (dequantised weight = code * scale).
  * A layer is E blobs in expert order; rank r's shard is experts [r*E/N, (r+1)*E/N),
  * so the rank-major AllGather of shards IS the layer.
  */

@@ -265,16 +265,6 @@ AEP_DEV void tma_load_3d_pair(void* dst, const void* tmap, uint64_t* bar, int c0
       : "memory");
 }
 
-AEP_DEV void tma_load_5d_pair(void* dst, const void* tmap, uint64_t* bar, int c0, int c1, int c2, int c3, int c4,
-                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2),
-      "r"(c3), "r"(c4), "l"(policy)
-      : "memory");
-}
-
 // ----------------------------------------------------------------------------- tcgen05
 AEP_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 AEP_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

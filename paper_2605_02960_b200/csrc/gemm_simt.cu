@@ -43,14 +43,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GroupedArgs g, const bf1
     decode_mtile(mt, g.tile_start, g.offsets, g.counts, g.E, e, row0, row_end);
     const bf16* W = reinterpret_cast<const bf16*>(layer + (size_t)e * expert_bytes + b_off);
     // B rows for this CTA's output columns
-    int rg, ru = 0;
-    if (SWIGLU) {
-      const int blk = n0 / 128, q = n0 % 128;
-      rg = blk * 256 + q;
-      ru = rg + 128;
-    } else {
-      rg = n0;
-    }
+    // packed W_gu row of act column j: 256-row block j/128, 32-row group (j%128)/16, gate at
+    // offset j%16 and the matching up row 16 rows later (asyncep.h layout)
+    auto gate_row = [](int j) { return (j / 128) * 256 + ((j % 128) / 16) * 32 + (j % 16); };
     float acc[8][4], accu[SWIGLU ? 8 : 1][SWIGLU ? 4 : 1];
 #pragma unroll
     for (int a = 0; a < 8; ++a)
@@ -76,14 +71,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GroupedArgs g, const bf1
         const int r = tid / 4, kp = (tid % 4) * 4;
         const bool ok = (n0 + r) < Nout;
         uint2 v = make_uint2(0, 0);
-        if (ok) v = *reinterpret_cast<const uint2*>(W + (int64_t)(rg + r) * b_row_stride_elems + k0 + kp);
+        const int64_t rg = SWIGLU ? gate_row(n0 + r) : n0 + r;
+        if (ok) v = *reinterpret_cast<const uint2*>(W + rg * b_row_stride_elems + k0 + kp);
         Bg[kp][r] = bf16_lo(v.x);
         Bg[kp + 1][r] = bf16_hi(v.x);
         Bg[kp + 2][r] = bf16_lo(v.y);
         Bg[kp + 3][r] = bf16_hi(v.y);
         if (SWIGLU) {
           uint2 w = make_uint2(0, 0);
-          if (ok) w = *reinterpret_cast<const uint2*>(W + (int64_t)(ru + r) * b_row_stride_elems + k0 + kp);
+          if (ok) w = *reinterpret_cast<const uint2*>(W + (rg + 16) * b_row_stride_elems + k0 + kp);
           Bu[kp][r] = bf16_lo(w.x);
           Bu[kp + 1][r] = bf16_hi(w.x);
           Bu[kp + 2][r] = bf16_lo(w.y);

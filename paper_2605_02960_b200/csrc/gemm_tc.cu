@@ -313,7 +313,6 @@ template <int MODE, int NCTA, bool F8>
 __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCTA, MODE>::NTHR == 256 ? 224 : 168))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_b2,
-                   const __grid_constant__ CUtensorMap map_bs, const __grid_constant__ CUtensorMap map_bs2,
                    const TcArgs p) {
   using C = Cfg<NCTA, MODE>;
   constexpr int STAGES = C::STAGES;
@@ -435,7 +434,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
         const bool own_e = e >= p.own_lo && e < p.own_hi;
         const CUtensorMap* mb = own_e ? &map_b2 : &map_b;
-        const CUtensorMap* mbs = own_e ? &map_bs2 : &map_bs;
         if (own_e) e -= p.own_lo;
         // swap: this CTA's ntok/2 token rows go to the B stage, its 128 weight rows to the A stage
         const int row0 = ntok ? mt * TM + (int)rank * (ntok >> 1) : mt * TM + (int)rank * BM;
@@ -455,16 +453,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               if (p.pol_a == 3) tma_load_2d_pair(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d_pair_hint(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
-            if (do_b) {
-              if (ntok && MODE == EPI_SWIGLU) {  // 4 boxes of [16 gate | 16 up] rows: j = rank*64 + 16i + [0,16)
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  tma_load_5d_pair(dB + stage * A_BYTES + i * 4096, mbs, &full[stage], kb * KB_ELEMS,
-                                   (int)rank * 64 + 16 * i, 0, nt, e, pol_b);
-              } else {
-                tma_load_3d_pair(dB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
-              }
-            }
+            if (do_b) tma_load_3d_pair(dB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           } else {
             mbar_arrive_expect_tx(&full[stage], tx);
             if (do_a) {
@@ -679,7 +668,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       if ((MODE == EPI_SWIGLU || MODE == EPI_PLAIN) && ntok) {
         // Swap-AB tail tile: TMEM lane = weight row of this CTA, column c = token row mt*TM + c.
         // GEMM1: lanes [0,16) of the quadrant hold gate rows j = jq, lanes [16,32) the up rows of
-        // the same j (the [16 gate | 16 up] TMA boxes); GEMM2: lane = output column.  The values are
+        // the same j (the packed W_gu's 32-row groups, asyncep.h); GEMM2: lane = output column.  The values are
         // transposed through the warp's staging buffer and written to out_ptr row by row.
         const int trow0 = mt * TM;  // the tile's first (token) row
         const bool upper = lane >= 16;
@@ -786,7 +775,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         router_epilogue<MODE == EPI_ROUTER ? 8 : 16>(tb, p.E, p.top_k, p.norm_topk, row < p.dense_rows,
                                                      p.ids + (int64_t)row * p.top_k, p.w + (int64_t)row * p.top_k);
       } else if (MODE == EPI_SWIGLU) {
-        // accumulator columns [0,128) = gate, [128,256) = up of act columns nt*128 + [0,128)
+        // accumulator column 32g + i (g < 8, i < 16) = gate of act column nt*128 + 16g + i, column
+        // 32g + 16 + i = its up (the packed W_gu layout, asyncep.h)
         float sa = 1.f, amax = 0.f;
         const float* sb = nullptr;
         if (F8) {
@@ -800,33 +790,29 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           sb = stage_scales(sScl + ew * 256, sb, 256, lane);
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < 128; c0 += 64) {
+        for (int c0 = 0; c0 < 128; c0 += 64) {  // act columns c0 .. c0+63 = packed groups c0/16 .. +3
           uint32_t o[32];
           uint32_t amax2 = 0;  // |bf16| bit patterns of both halves: unsigned order = magnitude order
-          uint32_t gg[2][32], uu[2][32];  // the chunk's 64 gate + 64 up columns, one wait
+          uint32_t vv[4][32];  // the chunk's 4 groups of [16 gate | 16 up] columns, one wait
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            tmem_ld32(tb + c0 + 32 * half, gg[half]);
-            tmem_ld32(tb + 128 + c0 + 32 * half, uu[half]);
-          }
+          for (int grp = 0; grp < 4; ++grp) tmem_ld32(tb + 2 * c0 + 32 * grp, vv[grp]);
           tmem_ld_wait();
           if (c0 + 64 >= 128) release();  // last TMEM read of the tile
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            const uint32_t(&g)[32] = gg[half];
-            const uint32_t(&u)[32] = uu[half];
+          for (int grp = 0; grp < 4; ++grp) {
+            const uint32_t(&v)[32] = vv[grp];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {  // 4 columns per step
+            for (int q = 0; q < 4; ++q) {  // 4 act columns per step
               float gv[4], uv[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
-                gv[j] = __uint_as_float(g[4 * q + j]);
-                uv[j] = __uint_as_float(u[4 * q + j]);
+                gv[j] = __uint_as_float(v[4 * q + j]);
+                uv[j] = __uint_as_float(v[16 + 4 * q + j]);
               }
               if (F8) {  // dequantise: acc * (a row scale) * (w channel scale)
-                const int cc = c0 + 32 * half + 4 * q;
+                const int cc = 2 * c0 + 32 * grp + 4 * q;  // packed column of the gate values
                 const float4 sg = ld_shared_f4(smem_u32(sb) + 4 * cc);
-                const float4 su = ld_shared_f4(smem_u32(sb) + 4 * cc + 512);
+                const float4 su = ld_shared_f4(smem_u32(sb) + 4 * (cc + 16));
                 float s0, s1, s2, s3, t0, t1, t2, t3;
                 mul2(s0, s1, sa, sa, sg.x, sg.y);
                 mul2(s2, s3, sa, sa, sg.z, sg.w);
@@ -842,7 +828,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
                 float a0, a1;
                 mul2(a0, a1, silu_f(gv[2 * j]), silu_f(gv[2 * j + 1]), uv[2 * j], uv[2 * j + 1]);
                 const uint32_t pk = pack_bf16x2(a0, a1);
-                o[16 * half + 2 * q + j] = pk;
+                o[8 * grp + 2 * q + j] = pk;
                 if (F8) amax2 = __vmaxu2(amax2, pk & 0x7fff7fffu);
               }
             }
@@ -927,8 +913,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 
 template <int MODE, int NCTA, bool F8 = false>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
-                 cudaStream_t s, const CUtensorMap* mb2 = nullptr, const CUtensorMap* mbs = nullptr,
-                 const CUtensorMap* mbs2 = nullptr) {
+                 cudaStream_t s, const CUtensorMap* mb2 = nullptr) {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -946,8 +931,7 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const CUtensorMap& b2 = mb2 ? *mb2 : mb;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, b2, mbs ? *mbs : mb, mbs2 ? *mbs2 : b2, a);
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, mb2 ? *mb2 : mb, a);
 }
 
 // Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
@@ -965,7 +949,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
                     const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false,
                     const void* gather_src = nullptr, int64_t gather_ld = 0, const OwnShard* own = nullptr,
-                    const CUtensorMap* mbs = nullptr, bf16* out = nullptr) {
+                    bf16* out = nullptr) {
   static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
   TcArgs a{};
@@ -983,7 +967,6 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.gather_src = static_cast<const uint8_t*>(gather_src);
   a.gather_ld = gather_ld;
   const CUtensorMap* mb2 = nullptr;
-  const CUtensorMap* mbs2 = nullptr;
   a.counts = g.counts;
   a.swap_max = (ncta == 2 && out && g.counts) ? (gemm2 ? g.swap_max2 : g.swap_max) : 0;
   a.out_ptr = out;
@@ -991,7 +974,6 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
     a.own_lo = own->lo;
     a.own_hi = own->hi;
     mb2 = gemm2 ? &own->maps->wd : &own->maps->wgu;
-    mbs2 = gemm2 ? &own->maps->wd : &own->maps->wgu_swap;
     if (f8) a.b_scale_base_own = own->base + (gemm2 ? f8->sd_off : f8->sgu_off);
   }
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
@@ -1006,11 +988,11 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
   const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
   if (f8) {  // FP8 experts: CTA pairs only
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
-    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2);
   } else if (ncta == 2) {
-    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
-    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s, mb2, mbs, mbs2);
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 2>(a, ma, mb, mo, grid, s, mb2);
   } else {
     if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 1>(a, ma, mb, mo, grid, s, mb2);
     else launch_mode<EPI_PLAIN, 1>(a, ma, mb, mo, grid, s, mb2);
@@ -1076,15 +1058,6 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
     const uint32_t box[3] = {kb, (uint32_t)(256 / ncta), 1};
     if (!encode_tmap(&m.wgu, dt, 3, layer, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   }
-  if (ncta == 2 && h % 128 == 0) {
-    const uint64_t dims[5] = {(uint64_t)H, 128, 2, (uint64_t)(2 * h / 256), (uint64_t)E};
-    const uint64_t strides[4] = {(uint64_t)H * b, (uint64_t)128 * H * b, (uint64_t)256 * H * b,
-                                 (uint64_t)expert_bytes};
-    const uint32_t box[5] = {kb, 16, 2, 1, 1};
-    if (!encode_tmap(&m.wgu_swap, dt, 5, layer, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
-  } else {
-    m.wgu_swap = m.wgu;
-  }
   {
     const uint8_t* wd = reinterpret_cast<const uint8_t*>(layer) + (size_t)2 * h * H * b;
     const uint64_t dims[3] = {(uint64_t)h, (uint64_t)H, (uint64_t)E};
@@ -1105,7 +1078,7 @@ bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
   const int64_t ld = (int64_t)H * (f8 ? 1 : 2);
   const CUtensorMap& ma = f8 ? am.xq : am.xperm;
   launch_grouped(g, ma, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s,
-                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own, &wm.wgu_swap, act);
+                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own, act);
   (void)T;
   return true;
 }
@@ -1114,7 +1087,7 @@ void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
                      int num_sms, cudaStream_t s, const F8Args* f8, const OwnShard* own) {
   const int bn = am.bn2;
   launch_grouped(g, f8 ? am.aq : am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s,
-                 nullptr, f8, true, nullptr, 0, own, &wm.wd, yperm);
+                 nullptr, f8, true, nullptr, 0, own, yperm);
 }
 
 // ------------------------------------------------------------------ dense GEMM (NEXT-3 projections)

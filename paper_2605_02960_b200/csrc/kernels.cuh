@@ -83,10 +83,6 @@ void launch_gemm2_simt(const GroupedArgs& g, const bf16* act, const uint8_t* lay
 struct GemmMaps {
   CUtensorMap wgu;   // 3D {H, 2h, E}, box {128 B, 256/NCTA rows, 1}
   CUtensorMap wd;    // 3D {h, H, E},  box {128 B, BN2/NCTA rows, 1}
-  // swap-AB tail tiles of GEMM1 (weights as the MMA's M operand): W_gu viewed as
-  // 5D {H, 128 (j in block), 2 (gate/up), 2h/256 (block), E}, box {128 B, 16, 2, 1, 1} =
-  // 16 gate rows then the matching 16 up rows (one TMEM lane quadrant per box)
-  CUtensorMap wgu_swap;
   bool fp8 = false;
 };
 // Gathered layers: experts [lo, hi) (this rank's own shard) are read by the GEMMs straight from

@@ -1,6 +1,6 @@
 // pack.cu -- natural-layout expert weights -> packed expert blobs (layout in asyncep.h):
-//   W_gu [2h, H]: rows [256b, 256b+128) = gate rows [128b, 128b+128),
-//                 rows [256b+128, 256b+256) = up rows [128b, 128b+128);
+//   W_gu [2h, H]: 256-row blocks b of 8 groups g of 32 rows: rows [256b + 32g, 256b + 32g + 16)
+//                 = gate rows j = 128b + 16g + [0, 16), the next 16 rows = the matching up rows;
 //   W_down [H, h] as given.   One CTA per (expert, packed row); 16-B vector copies.
 #include "common.cuh"
 #include "kernels.cuh"
@@ -8,6 +8,12 @@
 namespace aep {
 
 namespace {
+// Packed W_gu row r -> (gate?, natural row): b = r / 256, q = r % 256, g = q / 32, w = q % 32.
+__device__ __forceinline__ int gu_src_row(int r, bool& is_gate) {
+  const int b = r / 256, q = r % 256, g = q / 32, w = q % 32;
+  is_gate = w < 16;
+  return b * 128 + g * 16 + (w & 15);
+}
 __global__ void pack_bf16_kernel(const bf16* __restrict__ gate, const bf16* __restrict__ up,
                                  const bf16* __restrict__ down, int H, int h, size_t expert_bytes,
                                  uint8_t* __restrict__ out) {
@@ -18,9 +24,9 @@ __global__ void pack_bf16_kernel(const bf16* __restrict__ gate, const bf16* __re
   uint4* dst;
   int nv;
   if (r < 2 * h) {
-    const int b = r / 256, q = r % 256;
-    const int srow = b * 128 + (q % 128);
-    const bf16* m = (q < 128) ? gate : up;
+    bool is_gate;
+    const int srow = gu_src_row(r, is_gate);
+    const bf16* m = is_gate ? gate : up;
     src = reinterpret_cast<const uint4*>(m + ((size_t)e * h + srow) * H);
     dst = reinterpret_cast<uint4*>(blob + (size_t)r * H * 2);
     nv = H / 8;
@@ -47,9 +53,8 @@ __global__ void pack_fp8_kernel(const uint8_t* __restrict__ gate, const uint8_t*
   uint4* dst;
   int nv;
   if (r < 2 * h) {
-    const int b = r / 256, q = r % 256;
-    const int srow = b * 128 + (q % 128);
-    const bool is_gate = q < 128;
+    bool is_gate;
+    const int srow = gu_src_row(r, is_gate);
     src = reinterpret_cast<const uint4*>((is_gate ? gate : up) + ((size_t)e * h + srow) * H);
     dst = reinterpret_cast<uint4*>(blob + (size_t)r * H);
     nv = H / 16;
