@@ -292,7 +292,8 @@ ASYNCEP_API asyncep_status asyncep_saturation_T(const asyncep_config* cfg, doubl
  * hooks).  Synchronises on the recorded events and returns, summed
  * over all forwards since the last reset, the milliseconds of each stage:
  *   [0] router  [1] permute  [2] exposed gather wait  [3] GEMM1 gate/up+SwiGLU
- *   [4] GEMM2 down  [5] combine   (n_stages <= 6), and the number of forwards counted.
+ *   [4] GEMM2 down (FP8: with the intermediate's quantisation pass)  [5] combine
+ *   (n_stages <= 6), and the number of forwards counted.
  */
 ASYNCEP_API asyncep_status asyncep_stage_times(asyncep_ctx* ctx, double* ms_out, int32_t n_stages,
                                    int64_t* forwards_out);

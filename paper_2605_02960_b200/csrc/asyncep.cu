@@ -820,9 +820,11 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     f8.layer = wl;
     aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const void*)(ws + c->L.xq) : nullptr, T, src_tok,
                          c->num_sms, st, &f8, own);
+    // stage boundary before the intermediate's quantisation: the GEMM1 stage is the GEMM1 kernel
+    // alone (the roofline's dominant kernel); act_quant is timed with GEMM2, whose A operand it makes
+    if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
                           (float*)(ws + c->L.ascale), st);
-    if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8, own);
     c->launches += 3;
   } else {
