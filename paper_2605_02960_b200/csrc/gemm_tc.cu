@@ -687,12 +687,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         if (lane == 0) bulk_wait_read0();  // earlier TMA stores have finished reading the staging buffer
         __syncwarp();
         if (MODE == EPI_SWIGLU) {
-          const int jq = (int)rank * 64 + quad * 16 + (lane & 15);  // act column within the N tile
-          float sg = 1.f, su = 1.f;
-          if (F8) {
-            sg = __ldg(wsc + jq);
-            su = __ldg(wsc + 128 + jq);
-          }
+          // FP8: each lane scales its own weight row (packed row rank*128 + quad*32 + lane of the
+          // N tile: the gate row for lane < 16, the up row for lane >= 16) before the exchange
+          const float swr = F8 ? __ldg(wsc + (int)rank * 128 + quad * 32 + lane) : 1.f;
           bf16* outc = p.out_ptr + nt * 128 + (int)rank * 64 + quad * 16;
 #pragma unroll 1
           for (int c0 = 0; c0 < ntok; c0 += 32) {
@@ -706,15 +703,16 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               float g[2], u[2];
 #pragma unroll
               for (int q2 = 0; q2 < 2; ++q2) {
-                const uint32_t send = upper ? v[i + q2] : v[16 + i + q2];
-                const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 16);
-                g[q2] = __uint_as_float(upper ? recv : v[i + q2]);
-                u[q2] = __uint_as_float(upper ? v[16 + i + q2] : recv);
+                // keep this lane's token column cb + i + q2, send the partner's (16 - cb) + i + q2
+                float keep = __uint_as_float(v[cb + i + q2]);
+                float send = __uint_as_float(v[16 - cb + i + q2]);
                 if (F8) {
-                  const float ts = tsc[c0 + cb + i + q2];
-                  g[q2] *= sg * ts;
-                  u[q2] *= su * ts;
+                  keep *= swr * tsc[c0 + cb + i + q2];
+                  send *= swr * tsc[c0 + 16 - cb + i + q2];
                 }
+                const float recv = __shfl_xor_sync(0xffffffffu, send, 16);
+                g[q2] = upper ? recv : keep;
+                u[q2] = upper ? keep : recv;
               }
               float a0, a1;
               mul2(a0, a1, silu_f(g[0]), silu_f(g[1]), u[0], u[1]);
