@@ -28,6 +28,7 @@ FLAG_SIMT_ROUTER = 0x8
 FLAG_XPERM = 0x10
 FLAG_OFFLOAD = 0x20
 FLAG_NO_SWAP_TAILS = 0x40
+FLAG_SWAP_TAILS = 0x80
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 
 

@@ -67,17 +67,21 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
 }
 
 // Swap-AB tail tiles of the grouped GEMMs (gemm_tc.cu): an expert's last 256-row tile holding at
-// most this many rows runs with the weights as M and its tokens as N.  ASYNCEP_SWAP_MAX (GEMM1 and
-// BF16 GEMM2) / ASYNCEP_SWAP_MAX_F8G2 (FP8 GEMM2, whose short K = h bytes leaves the swap epilogue
-// exposed: +8 % GEMM2 at 240, profiles/r02/swap/); 0 = off.
+// most this many rows runs with the weights as M and its tokens as N.  Same-process interleaved A/B
+// (profiles/ab_flags.py, profiles/r02/swap/ab_swap_*.jsonl): FP8 GEMM1 gains (stack +0.7 % at 32K,
+// +8 % at 16K, +23-25 % at 8K tokens/GPU); BF16 loses 0.5-1.7 % at 16-32K (a BF16 swap tile costs
+// more cycles than the padded tile it replaces, ncu r02/gemm1_ncu_full_16k_swap*.json) and the FP8
+// down GEMM (short K) loses 5-8 %.  Defaults: FP8 GEMM1 240 rows, the others off.
+// ASYNCEP_SWAP_MAX_BF16 / ASYNCEP_SWAP_MAX_FP8 / ASYNCEP_SWAP_MAX_F8G2 override (0 = off).
 int env_rows(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && *e) ? atoi(e) : dflt;
 }
-int swap_max_rows(bool fp8_gemm2) {
-  static const int g = env_rows("ASYNCEP_SWAP_MAX", 240);
-  static const int f = env_rows("ASYNCEP_SWAP_MAX_F8G2", 0);
-  return fp8_gemm2 ? f : g;
+int swap_max_rows(bool fp8, bool gemm2) {
+  static const int b = env_rows("ASYNCEP_SWAP_MAX_BF16", 0);
+  static const int f1 = env_rows("ASYNCEP_SWAP_MAX_FP8", 240);
+  static const int f2 = env_rows("ASYNCEP_SWAP_MAX_F8G2", 0);
+  return fp8 ? (gemm2 ? f2 : f1) : b;
 }
 
 // NVTX ranges around the host-side enqueue of each call (the paper's gated per-layer hooks,
@@ -806,8 +810,10 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   const aep::OwnShard* own = use_own ? &own_sh : nullptr;
   aep::GroupedArgs g{offsets, tile_start, counts, E, (int)(aep::perm_rows(T, k, E) / aep::kRowAlign), sched};
   const bool swap_on = !(cf.flags & ASYNCEP_FLAG_NO_SWAP_TAILS);
-  g.swap_max = swap_on ? swap_max_rows(false) : 0;
-  g.swap_max2 = swap_on ? swap_max_rows(cf.expert_dtype == ASYNCEP_FP8_E4M3) : 0;
+  const bool swap_all = (cf.flags & ASYNCEP_FLAG_SWAP_TAILS) != 0;
+  const bool fp8e = cf.expert_dtype == ASYNCEP_FP8_E4M3;
+  g.swap_max = !swap_on ? 0 : swap_all ? 240 : swap_max_rows(fp8e, false);
+  g.swap_max2 = !swap_on ? 0 : swap_all ? 240 : swap_max_rows(fp8e, true);
   bf16* yperm = xperm;
   if (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) {
     // Y_perm = X_perm (already in place)

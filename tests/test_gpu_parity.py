@@ -217,15 +217,18 @@ def test_config5_zipf_skewed_full_size_sampled():
     print(check_layer(f32(x)[idx], wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None))
 
 
+@pytest.mark.parametrize("swap", [False, True], ids=["padded_tails", "swap_tails"])
 @pytest.mark.parametrize("T", [1, 129, 5000])
-def test_fused_dispatch_bitwise(T):
+def test_fused_dispatch_bitwise(T, swap):
     """GEMM1 gathering token rows of x itself (default: cp.async warps through src_tok)
     computes exactly what the materialised X_perm path (FLAG_XPERM) computes: same A bytes,
-    same MMAs."""
+    same MMAs; with the swap-AB tail tiles the gathered rows land in the B (N) operand instead."""
+    from paper_2605_02960_b200 import asyncep as A
     wl = Workload(L=1, E=64, k=8, H=1024, h=768, seed=9)
     x = wl.tokens(T)
     outs = []
-    for flags in (0, 16):
+    sw = A.FLAG_SWAP_TAILS if swap else A.FLAG_NO_SWAP_TAILS
+    for flags in (sw, sw | A.FLAG_XPERM):
         st = wl.stack(max_tokens=8192, flags=flags)
         outs.append(run_layer(wl, st, 0, x)[0])
         del st
@@ -287,15 +290,16 @@ def test_router_tile_shapes(E, k):
 @pytest.mark.parametrize("T", [5, 333, 700, 2000])
 @pytest.mark.parametrize("fp8", [False, True], ids=["bf16", "fp8"])
 def test_swap_tail_tiles(T, fp8):
-    """Swap-AB tail tiles (default): every expert's last row tile with <= 240 rows runs with the
-    weights as the MMA's M and its tokens as N.  E = 16, k = 4: T = 5 / 333 / 700 / 2000 give tails
-    of ~1 / ~83 / ~175 / ~0-250 rows per expert.  Both the swap path and the padded-tile path
-    (FLAG_NO_SWAP_TAILS) pass the full acceptance procedure, and they agree to a bf16 rounding."""
+    """Swap-AB tail tiles (FLAG_SWAP_TAILS: both GEMMs; the default keeps them where they pay):
+    every expert's last row tile with <= 240 rows runs with the weights as the MMA's M and its
+    tokens as N.  E = 16, k = 4: T = 5 / 333 / 700 / 2000 give tails of ~1 / ~83 / ~175 / ~0-250 rows
+    per expert.  Both the swap path and the padded-tile path (FLAG_NO_SWAP_TAILS) pass the full
+    acceptance procedure, and they agree to a bf16 rounding."""
     from paper_2605_02960_b200 import asyncep as A
     wl = Workload(L=1, E=16, k=4, H=512, h=256, seed=31, fp8=fp8)
     x = wl.tokens(T)
     outs = []
-    for flags in (0, A.FLAG_NO_SWAP_TAILS):
+    for flags in (A.FLAG_SWAP_TAILS, A.FLAG_NO_SWAP_TAILS):
         st = wl.stack(max_tokens=2048, flags=flags)
         outs.append(run_layer(wl, st, 0, x))
         del st
