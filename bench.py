@@ -349,6 +349,11 @@ def main():
             stack.enable_p2p_gather()
         except Exception as e:  # recorded in the JSON line; NCCL remains
             p2p_error = f"{type(e).__name__}: {str(e)[:160]}"
+        # every rank must take the same transports (the probes and NCCL calls are collective)
+        ok = torch.tensor([0 if p2p_error else 1], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            p2p_error = p2p_error or "peer-shard mapping failed on another rank"
             A.asyncep_set_peer_shards(stack.ctx, None)
     if emu > 1 and args.link_gbs > 0:
         A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
