@@ -239,8 +239,8 @@ def self_launch(argv, n: int) -> int:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")           # communicator init (transport, NVLS, channels) to stderr
-    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    if "NCCL_DEBUG" not in env:  # communicator init (transports, NVLS, channels) into the log, not stdout
+        env.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE="/dev/stderr")
     env.setdefault("OMP_NUM_THREADS", "8")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
