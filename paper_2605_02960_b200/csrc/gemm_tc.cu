@@ -506,6 +506,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #if GEMM_WAITPROF
     const long long wp_t0 = clock64();
 #endif
+    const int gpol = p.pol_a == 1 || p.pol_a == 2 ? p.pol_a : 0;
     int t = next_tile(0);
     int32_t tok[16];
     int nrow = 16;
@@ -524,13 +525,15 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       for (int kb = 0; kb < nkb; ++kb) {
         WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
         const uint32_t dst = base + (uint32_t)(stage * A_BYTES);
+        // L2 policy of the gathered token rows: ASYNCEP_POL_A (0 normal, 1 evict_last, 2 evict_first)
+        const uint64_t gpolicy = make_policy(gpol);
         if (nrow == 16) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+          for (int i = 0; i < 16; ++i) cp_async16_hint(dst + i * 8 * 128, src[i] + kb * 128, gpolicy);
         } else {
 #pragma unroll
           for (int i = 0; i < 16; ++i)
-            if (i < nrow) cp_async16(dst + i * 8 * 128, src[i] + kb * 128);
+            if (i < nrow) cp_async16_hint(dst + i * 8 * 128, src[i] + kb * 128, gpolicy);
         }
         cp_async_mbar_arrive_noinc(&afull[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -704,8 +707,9 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #pragma unroll
               for (int q2 = 0; q2 < 2; ++q2) {
                 // keep this lane's token column cb + i + q2, send the partner's (16 - cb) + i + q2
-                float keep = __uint_as_float(v[cb + i + q2]);
-                float send = __uint_as_float(v[16 - cb + i + q2]);
+                // (selects between two static indices: a runtime index would put v[] in local memory)
+                float keep = __uint_as_float(upper ? v[16 + i + q2] : v[i + q2]);
+                float send = __uint_as_float(upper ? v[i + q2] : v[16 + i + q2]);
                 if (F8) {
                   keep *= swr * tsc[c0 + cb + i + q2];
                   send *= swr * tsc[c0 + 16 - cb + i + q2];

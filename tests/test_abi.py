@@ -51,6 +51,21 @@ def test_library_is_sm100a_code(A):
     assert "LDTM" in sass, "no TMEM loads in the binary"
 
 
+def test_hot_kernels_do_not_spill(A):
+    """The production-path kernels keep their state in registers (cuobjdump -res-usage STACK:0): a
+    local-memory spill in a tensor-core pipeline role (e.g. a runtime-indexed register array in an
+    epilogue) costs the GEMM its issue slots silently.  (Debug / fallback kernels -- the SIMT
+    router and GEMM, the destination-list FP8 quantisation -- may use local arrays.)"""
+    out = subprocess.run(["cuobjdump", "-res-usage", A.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = re.findall(r"Function (\S+):\s*\n\s*REG:(\d+) STACK:(\d+)", out)
+    assert funcs, out[:500]
+    hot = ("gemm_tc_kernel", "combine_kernel", "perm_hist", "perm_scan", "perm_scatter", "quant_tokens",
+           "act_quant", "gather_copy", "flash_attn4", "rmsnorm", "qk_rope", "v_transpose")
+    assert any(h in f for f, _, _ in funcs for h in hot)
+    spills = [(f, st) for f, reg, st in funcs if int(st) != 0 and any(h in f for h in hot)]
+    assert not spills, spills
+
+
 def test_sizes_and_config_validation(A):
     cfg = A.make_config(8, 128, 8, 4096, 1536, world_size=8, max_tokens=32768)
     assert A.asyncep_expert_bytes(cfg) == 3 * 4096 * 1536 * 2
