@@ -91,6 +91,7 @@ struct TcArgs {
   int ts_scale; // row tiles (of 128*NCTA rows) per tile_start unit (kRowAlign rows)
   int raster;   // 0: row-tile-major order; G > 0: groups of G row tiles walked row-first
   int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first, 3 none (A)
+  int pol_gather;    // L2 policy of the fused dispatch's cp.async row gathers: 0 normal, 1 evict_last, 2 evict_first
   // FP8 (kind::f8f6f4) scales: dequantised D[r][c] = acc * a_scale[r] * b_scale(e)[B row of c]
   const float* a_scale;
   const uint8_t* b_scale_base;  // layer base + offset of the scale block inside an expert blob
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
 #if GEMM_WAITPROF
     const long long wp_t0 = clock64();
 #endif
-    const int gpol = p.pol_a == 1 || p.pol_a == 2 ? p.pol_a : 0;
+    const int gpol = p.pol_gather == 1 || p.pol_gather == 2 ? p.pol_gather : 0;
     int t = next_tile(0);
     int32_t tok[16];
     int nrow = 16;
@@ -525,7 +526,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       for (int kb = 0; kb < nkb; ++kb) {
         WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
         const uint32_t dst = base + (uint32_t)(stage * A_BYTES);
-        // L2 policy of the gathered token rows: ASYNCEP_POL_A (0 normal, 1 evict_last, 2 evict_first)
+        // L2 policy of the gathered token rows (ASYNCEP_POL_GATHER; evict_last by default: ncu of the
+        // BF16 GEMM1 at 32K tokens, profiles/r02/l2policy/: 4.79 vs 4.89 ms at the same clock)
         const uint64_t gpolicy = make_policy(gpol);
         if (nrow == 16) {
 #pragma unroll
@@ -965,6 +967,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.raster = grouped_raster();
   a.pol_a = env_int("ASYNCEP_POL_A", 0);
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
+  a.pol_gather = env_int("ASYNCEP_POL_GATHER", 1);
   a.gather_rows = gather_rows;
   a.gather_src = static_cast<const uint8_t*>(gather_src);
   a.gather_ld = gather_ld;
