@@ -84,13 +84,6 @@ int swap_max_rows(bool fp8, bool gemm2) {
   return fp8 ? (gemm2 ? f2 : f1) : b;
 }
 
-// FP8 intermediate quantisation fused into the GEMM1 epilogue (default) or as the separate
-// act_quant pass (ASYNCEP_FUSED_ACT_QUANT=0; same arithmetic, bitwise the same codes).
-bool fused_act_quant() {
-  static const bool v = env_rows("ASYNCEP_FUSED_ACT_QUANT", 1) != 0;
-  return v;
-}
-
 // NVTX ranges around the host-side enqueue of each call (the paper's gated per-layer hooks,
 // PAPER.md:650-655); free when no tool is attached.
 struct NvtxRange {
@@ -169,7 +162,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
   size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, sched, xperm, act, total;
-  size_t xq, xscale, amax, aq, ascale, slices;  // FP8 experts only
+  size_t xq, xscale, amax, aq, ascale;  // FP8 experts only
 };
 WsLayout ws_layout(const asyncep_config& c) {
   WsLayout L{};
@@ -201,7 +194,6 @@ WsLayout ws_layout(const asyncep_config& c) {
     L.amax = take(Rp * 4);
     L.aq = take(Rp * (size_t)c.ffn);
     L.ascale = take(Rp * 4);
-    L.slices = take((Rp / 32 + 1) * 4);  // fused act quantisation: per-32-row slice tile counters
   }
   L.total = o;
   return L;
@@ -463,8 +455,7 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   const bool fp8 = cfg->expert_dtype == ASYNCEP_FP8_E4M3;
   const int64_t Rp = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
   if (cudaMemsetAsync(c->ws + c->L.done, 0, 4, c->cs) != cudaSuccess ||
-      (fp8 && cudaMemsetAsync(c->ws + c->L.amax, 0, (size_t)Rp * 4, c->cs) != cudaSuccess) ||
-      (fp8 && cudaMemsetAsync(c->ws + c->L.slices, 0, (size_t)(Rp / 32 + 1) * 4, c->cs) != cudaSuccess))
+      (fp8 && cudaMemsetAsync(c->ws + c->L.amax, 0, (size_t)Rp * 4, c->cs) != cudaSuccess))
     return bail(fail(ASYNCEP_ERR_CUDA, "cudaMemsetAsync failed"));
   // TMA descriptors: activations (fixed workspace addresses), each resident layer, both slots.
   const int64_t R = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
@@ -793,11 +784,6 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     f8.x_scale = (const float*)(ws + c->L.xscale);
     f8.act_scale = (const float*)(ws + c->L.ascale);
     f8.act_amax = (uint32_t*)(ws + c->L.amax);
-    if (fused_act_quant()) {  // the GEMM1 epilogue quantises each 32-row slice once it is complete
-      f8.slice_cnt = (int32_t*)(ws + c->L.slices);
-      f8.aq = ws + c->L.aq;
-      f8.act_scale_out = (float*)(ws + c->L.ascale);
-    }
     f8.expert_bytes = c->expert_bytes;
     f8.sgu_off = (size_t)3 * H * h;
     f8.sd_off = f8.sgu_off + (size_t)2 * h * 4;
@@ -841,13 +827,12 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? (const void*)(ws + c->L.xq) : nullptr, T, src_tok,
                          c->num_sms, st, &f8, own);
     // stage boundary before the intermediate's quantisation: the GEMM1 stage is the GEMM1 kernel
-    // (with the fused quantisation, default); a separate act_quant pass is timed with GEMM2
+    // alone (the roofline's dominant kernel); act_quant is timed with GEMM2, whose A operand it makes
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
-    if (!f8.slice_cnt)
-      aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
-                            (float*)(ws + c->L.ascale), st);
+    aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
+                          (float*)(ws + c->L.ascale), st);
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8, own);
-    c->launches += f8.slice_cnt ? 2 : 3;
+    c->launches += 3;
   } else {
     aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? x : nullptr, T, src_tok, c->num_sms, st, nullptr,
                          own);

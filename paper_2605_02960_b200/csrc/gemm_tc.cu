@@ -120,61 +120,7 @@ struct TcArgs {
   const int32_t* counts;
   int swap_max;
   bf16* out_ptr;
-  // FP8 GEMM1 with the intermediate's quantisation fused (R6 per-row rule): slice_cnt[r / 32] counts
-  // the tiles that have written (and atomicMax'ed) 32-row slice r/32; the warp completing a slice
-  // quantises it from L2 into aq_out / ascale_out (the act_quant pass's arithmetic) and re-arms
-  // act_amax and the counter.  nullptr: the separate act_quant kernel runs.
-  int32_t* slice_cnt;
-  uint8_t* aq_out;
-  float* ascale_out;
 };
-
-// R6 per-row quantisation of 32 act rows [row0, row0 + 32) of width h (bf16, L2-resident) into
-// e4m3 codes + fp32 row scales -- the arithmetic of act_quant_kernel (permute.cu), lane-parallel
-// over each row's columns; then re-arms the rows' amax and the slice counter.
-__device__ __noinline__ void quant_act_slice(const bf16* act, int h, uint32_t* amax_g, uint8_t* aq, float* ascale,
-                                             int32_t* slice_cnt, int64_t row0, int lane) {
-  for (int rr = 0; rr < 32; ++rr) {
-    const int64_t r = row0 + rr;
-    const float amax = __uint_as_float(__ldcg(amax_g + r));
-    const float inv = amax > 0.f ? 448.0f / amax : 0.f;
-    const uint4* src = reinterpret_cast<const uint4*>(act + r * h);
-    uint2* dst = reinterpret_cast<uint2*>(aq + r * h);
-    for (int v = lane; v < h / 8; v += 32) {
-      const uint4 u = __ldcg(src + v);
-      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-      uint2 o;
-      o.x = (uint32_t)e4m3x2(bf16_lo(w[0]) * inv, bf16_hi(w[0]) * inv) |
-            ((uint32_t)e4m3x2(bf16_lo(w[1]) * inv, bf16_hi(w[1]) * inv) << 16);
-      o.y = (uint32_t)e4m3x2(bf16_lo(w[2]) * inv, bf16_hi(w[2]) * inv) |
-            ((uint32_t)e4m3x2(bf16_lo(w[3]) * inv, bf16_hi(w[3]) * inv) << 16);
-      dst[v] = o;
-    }
-    if (lane == 0) {
-      ascale[r] = amax / 448.0f;
-      amax_g[r] = 0u;  // re-armed for the next forward
-    }
-  }
-  if (lane == 0) slice_cnt[row0 >> 5] = 0;
-}
-
-// After a warp's act rows of a tile are in global memory (TMA stores complete / plain stores) and
-// their amax atomics issued: release them, count the slice, quantise it if this was its last tile.
-__device__ __forceinline__ void act_slice_done(const TcArgs& p, int64_t row0, int target, int lane) {
-  if (lane == 0) {
-    bulk_wait0();                                                  // this warp's TMA stores performed
-    asm volatile("fence.proxy.async.global;" ::: "memory");        // async-proxy writes -> generic
-  }
-  __syncwarp();
-  __threadfence();                                                 // release act + amax (all lanes)
-  int last = 0;
-  if (lane == 0) last = atomicAdd(p.slice_cnt + (row0 >> 5), 1) == target - 1;
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (last) {
-    __threadfence();                                               // acquire the other tiles' rows
-    quant_act_slice(p.out_ptr, p.n_out, p.amax_out, p.aq_out, p.ascale_out, p.slice_cnt, row0, lane);
-  }
-}
 
 // linear tile index -> (row tile, n tile)
 __device__ __forceinline__ void decode_tile(int t, int n_tiles, int total_rt, int raster, int& mt, int& nt) {
@@ -797,9 +743,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
             }
             __syncwarp();
           }
-          // every warp of both CTAs wrote 16 columns of each 32-row slice: 8 x n_tiles per slice
-          if (F8 && p.slice_cnt)
-            for (int c0 = 0; c0 < ntok; c0 += 32) act_slice_done(p, trow0 + c0, 8 * p.n_tiles, lane);
         } else {
           const int ncol = (int)rank * 128 + quad * 32 + lane;  // output column within the N tile
           const float sw = F8 ? __ldg(wsc + ncol) : 1.f;
@@ -902,7 +845,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           if (F8) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
         }
         if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
-        if (F8 && p.slice_cnt) act_slice_done(p, wrow0, p.n_tiles, lane);  // one warp per slice per N tile
       } else {
         float sa = 1.f;
         const float* sb = nullptr;
@@ -1046,11 +988,6 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
     a.b_scale_base = f8->layer + (gemm2 ? f8->sd_off : f8->sgu_off);
     a.expert_bytes = f8->expert_bytes;
     a.amax_out = gemm2 ? nullptr : f8->act_amax;
-    if (!gemm2 && f8->slice_cnt) {
-      a.slice_cnt = f8->slice_cnt;
-      a.aq_out = f8->aq;
-      a.ascale_out = f8->act_scale_out;
-    }
   }
   const int units = num_sms / ncta;
   const int upper = g.max_m_tiles * a.ts_scale * n_tiles;

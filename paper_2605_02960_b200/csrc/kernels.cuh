@@ -101,11 +101,6 @@ struct F8Args {
   const uint8_t* layer;    // packed FP8 layer (E blobs)
   size_t expert_bytes;
   size_t sgu_off, sd_off;  // byte offsets of s_gu [2h] / s_down [H] inside a blob
-  // fused intermediate quantisation (GEMM1 epilogue): zeroed per-32-row slice counters, the e4m3
-  // act codes and row scales it writes (nullptr slice_cnt: launch_act_quant runs instead)
-  int32_t* slice_cnt = nullptr;
-  uint8_t* aq = nullptr;
-  float* act_scale_out = nullptr;
 };
 struct ActMaps {
   CUtensorMap xq;        // FP8: 2D {H, R_max} e4m3, box {128, 128}  (GEMM1 A)

@@ -41,9 +41,8 @@ def test_bench_line_contract(fp8):
     e = d["e2e"]
     assert e["value"] > 0 and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] == 4096 * 4096 * 2 and e["d2h_bytes_per_step"] == 4096 * 4096 * 2
-    # our kernels launched inside the timed region: 7 per BF16 layer, 8 per FP8 layer (token
-    # quantisation added; the intermediate's quantisation is fused into GEMM1)
-    assert d["gpu_launches"] == 2 * 2 * (8 if fp8 else 7)
+    # our kernels launched inside the timed region: 7 per BF16 layer, 9 per FP8 layer
+    assert d["gpu_launches"] == 2 * 2 * (9 if fp8 else 7)
 
 
 def test_bench_self_launches_two_ranks_on_one_gpu():
