@@ -2,8 +2,6 @@
 // outputs"; reading R9 for the residual):
 //     y_t = r_t + sum_{j=0..k-1} w_tj * Y_perm[dest(t, j)]     (fp32 accumulate, j order)
 // One warp per token, 16-B vectors (8 bf16 per lane per step); HBM-bound.
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -85,15 +83,15 @@ __global__ void spin_ns_kernel(uint64_t ns) {
 // so a chunk takes max(copy, link) time, and ns_per_round > 0: every CTA paces itself -- round r of its strided share
 // may start only ns_per_round * r after the kernel started -- so the copy streams smoothly at the
 // emulated link rate over the whole chunk, like a remote read, instead of bursting at HBM speed.
-template <int THREADS, int UNROLL>
-__global__ void __launch_bounds__(THREADS) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                                              size_t n16, uint64_t ns_per_round, uint64_t min_ns) {
+constexpr int kCopyUnroll = 8;
+__global__ void __launch_bounds__(128) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                          size_t n16, uint64_t ns_per_round, uint64_t min_ns) {
   uint64_t t0 = 0;
   if (ns_per_round || min_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  const size_t stride = (size_t)gridDim.x * THREADS;
-  size_t i = (size_t)blockIdx.x * THREADS + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * 128;
+  size_t i = (size_t)blockIdx.x * 128 + threadIdx.x;
   uint64_t round = 0;
-  for (; i + (UNROLL - 1) * stride < n16; i += UNROLL * stride) {
+  for (; i + (kCopyUnroll - 1) * stride < n16; i += kCopyUnroll * stride) {
     if (ns_per_round) {
       for (;;) {
         uint64_t t;
@@ -103,11 +101,11 @@ __global__ void __launch_bounds__(THREADS) gather_copy_kernel(uint4* __restrict_
       }
       ++round;
     }
-    uint4 v[UNROLL];
+    uint4 v[kCopyUnroll];
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) v[u] = __ldcs(src + i + u * stride);
+    for (int u = 0; u < kCopyUnroll; ++u) v[u] = __ldcs(src + i + u * stride);
 #pragma unroll
-    for (int u = 0; u < UNROLL; ++u) __stcs(dst + i + u * stride, v[u]);
+    for (int u = 0; u < kCopyUnroll; ++u) __stcs(dst + i + u * stride, v[u]);
   }
   for (; i < n16; i += stride) __stcs(dst + i, __ldcs(src + i));
   if (min_ns && blockIdx.x == 0 && threadIdx.x == 0)  // the chunk takes max(copy, link) time
@@ -118,34 +116,19 @@ __global__ void __launch_bounds__(THREADS) gather_copy_kernel(uint4* __restrict_
       __nanosleep(500);
     }
 }
-
-template <int THREADS, int UNROLL>
-void launch_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns) {
-  const size_t n16 = bytes / 16;
-  // pacing: the chunk must take min_ns; a CTA's share is split into rounds of THREADS x UNROLL x 16 B
-  const size_t per_round = (size_t)ctas * THREADS * UNROLL;
-  const uint64_t rounds = (n16 + per_round - 1) / per_round;
-  const uint64_t ns_per_round = (min_ns && rounds) ? min_ns / rounds : 0;
-  gather_copy_kernel<THREADS, UNROLL><<<ctas, THREADS, 0, s>>>(static_cast<uint4*>(dst),
-                                                              static_cast<const uint4*>(src), n16, ns_per_round,
-                                                              min_ns);
-}
 }  // namespace
 
 void launch_spin_ns(uint64_t ns, cudaStream_t s) { spin_ns_kernel<<<1, 1, 0, s>>>(ns); }
 
 void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns) {
   if (!bytes) return;
-  // CTA shape (ASYNCEP_GATHER_THREADS): 128 threads x 8 x 16 B in flight (default), or one / two
-  // warps with 16 in flight each -- fewer warps beside the GEMM's epilogue and gather warps
-  static const int threads = [] {
-    const char* e = getenv("ASYNCEP_GATHER_THREADS");
-    const int v = (e && *e) ? atoi(e) : 128;
-    return (v == 32 || v == 64) ? v : 128;
-  }();
-  if (threads == 32) launch_copy<32, 16>(dst, src, bytes, ctas, s, min_ns);
-  else if (threads == 64) launch_copy<64, 16>(dst, src, bytes, ctas, s, min_ns);
-  else launch_copy<128, 8>(dst, src, bytes, ctas, s, min_ns);
+  const size_t n16 = bytes / 16;
+  // pacing: the chunk must take min_ns; a CTA's share is split into rounds of 128 x kCopyUnroll x 16 B
+  const size_t per_round = (size_t)ctas * 128 * kCopyUnroll;
+  const uint64_t rounds = (n16 + per_round - 1) / per_round;
+  const uint64_t ns_per_round = (min_ns && rounds) ? min_ns / rounds : 0;
+  gather_copy_kernel<<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+                                         ns_per_round, min_ns);
 }
 
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,
