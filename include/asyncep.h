@@ -311,6 +311,27 @@ ASYNCEP_API asyncep_status asyncep_forward_times(asyncep_ctx* ctx, double* ms_ou
                                                  int32_t* n_out);
 
 /*
+ * Event timeline of the schedule (the per-layer view an nsys trace would give; nsys is not part of
+ * this toolchain): asyncep_timeline_begin records an epoch on the compute stream (the comm stream
+ * waits for it), then every forward (ASYNCEP_FLAG_STAGE_TIMING) and every gather is recorded until
+ * asyncep_timeline_read, which synchronises, writes up to n records in issue order -- forwards
+ * first as they flush, then gathers -- and ends the capture; n_out = records available.
+ *   FORWARD: t0 = start (router), t1 = GEMM1 start (after the wait for the slot), t2 = end (combine)
+ *   GATHER : t0 = start of the layer's gather on the comm stream, t1 = t2 = its end (ag_done)
+ * Times are ms since the epoch.  Errors: INVALID_ARG (no timing flag / no begin), CUDA.
+ */
+#define ASYNCEP_TL_FORWARD 0
+#define ASYNCEP_TL_GATHER 1
+typedef struct {
+  int32_t kind;  /* ASYNCEP_TL_* */
+  int32_t layer;
+  float t0, t1, t2;
+} asyncep_timeline_rec;
+ASYNCEP_API asyncep_status asyncep_timeline_begin(asyncep_ctx* ctx);
+ASYNCEP_API asyncep_status asyncep_timeline_read(asyncep_ctx* ctx, asyncep_timeline_rec* out, int32_t n,
+                                                 int32_t* n_out);
+
+/*
  * Calibrated saturation threshold, App. B.4 Eq. 3:
  *   T = gamma * (t_e / t_c) * C_dummy  [FLOPs],  collapsing to gamma * C_dummy when t_e <= t_c,
  * with t_c = wall time of the resident layer 0 and t_e = max wall time of the gathered layers

@@ -89,6 +89,8 @@ def lib() -> ctypes.CDLL:
             "asyncep_prefetch_layer_local": ([P, I32, P], I32),
             "asyncep_set_gather_transport": ([P, I32, I32], I32),
             "asyncep_set_gather_copy_ctas": ([P, I32], I32),
+            "asyncep_timeline_begin": ([P], I32),
+            "asyncep_timeline_read": ([P, P, I32, ctypes.POINTER(I32)], I32),
             "asyncep_probe_gather": ([P, I32, P, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
             "asyncep_moe_forward": ([P, I32, P, I64, P, P, P, P, P], I32),
             "asyncep_saturation_T": ([CP, D, D, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
@@ -345,6 +347,23 @@ def asyncep_calibrate_T(ctx: Context, gamma: float, n_ref: int):
     out = [ctypes.c_double() for _ in range(4)]
     _check(lib().asyncep_calibrate_T(ctx.handle, float(gamma), int(n_ref), *[ctypes.byref(o) for o in out]))
     return dict(zip(("T_flops", "T_tokens", "t_c_ms", "t_e_ms"), (o.value for o in out)))
+
+
+class TimelineRec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("layer", ctypes.c_int32), ("t0", ctypes.c_float),
+                ("t1", ctypes.c_float), ("t2", ctypes.c_float)]
+
+
+def asyncep_timeline_begin(ctx: Context) -> None:
+    _check(lib().asyncep_timeline_begin(ctx.handle))
+
+
+def asyncep_timeline_read(ctx: Context, n: int = 4096):
+    """-> [(kind 'forward'|'gather', layer, t0, t1, t2)] in ms since asyncep_timeline_begin."""
+    buf = (TimelineRec * n)()
+    m = ctypes.c_int32()
+    _check(lib().asyncep_timeline_read(ctx.handle, buf, n, ctypes.byref(m)))
+    return [("forward" if r.kind == 0 else "gather", r.layer, r.t0, r.t1, r.t2) for r in buf[:min(n, m.value)]]
 
 
 def asyncep_reset_stage_times(ctx: Context) -> None:

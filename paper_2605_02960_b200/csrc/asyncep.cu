@@ -267,6 +267,12 @@ struct asyncep_ctx {
   int64_t fwd_count = 0;
   std::vector<int32_t> ev_layer;                 // layer of the forward in each ring slot
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
+  // event timeline (asyncep_timeline_begin / _read): epoch on both streams, then per forward
+  // (start, GEMM1 start = after the gather wait, end) and per gather (start, end), ms since epoch
+  cudaEvent_t epoch = nullptr;
+  bool timeline = false;
+  std::vector<asyncep_timeline_rec> tl;                          // flushed records
+  std::vector<std::pair<int32_t, std::pair<cudaEvent_t, cudaEvent_t>>> tl_gather;  // pending gathers
   int64_t launches = 0;
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
   std::vector<const void*> peer;  // P2P gather: [layer * N + rank] peer-mapped shard pointers (empty: NCCL)
@@ -332,6 +338,13 @@ asyncep_status flush_timing(asyncep_ctx* c, bool blocking = true) {
     float tot = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&tot, e[0], e[kStages]));
     c->recent.emplace_back(c->ev_layer[(size_t)c->ev_head], (double)tot);
+    if (c->timeline && c->epoch) {
+      float t0 = 0.f, t3 = 0.f, t6 = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t0, c->epoch, e[0]));
+      CUDA_TRY(cudaEventElapsedTime(&t3, c->epoch, e[3]));
+      CUDA_TRY(cudaEventElapsedTime(&t6, c->epoch, e[kStages]));
+      c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_FORWARD, c->ev_layer[(size_t)c->ev_head], t0, t3, t6});
+    }
     if (c->recent.size() > 4096) c->recent.erase(c->recent.begin(), c->recent.begin() + 2048);
     c->ev_head = (c->ev_head + 1) % kMaxPendingFwd;
     --c->ev_used;
@@ -514,6 +527,12 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     CUDA_TRY(cudaStreamWaitEvent(c->ms, c->h2d_done[wi], 0));
     own = c->window[wi];
   }
+  cudaEvent_t tg0 = nullptr, tg1 = nullptr;
+  if (c->timeline) {
+    CUDA_TRY(cudaEventCreate(&tg0));
+    CUDA_TRY(cudaEventCreate(&tg1));
+    CUDA_TRY(cudaEventRecord(tg0, c->ms));
+  }
   if (!shards && tr != ASYNCEP_GATHER_NCCL) {  // P2P gather over the IPC-mapped peer shards
     if (c->peer.empty()) return fail(ASYNCEP_ERR_INVALID_ARG, "copy transport without peer shards (asyncep_set_peer_shards)");
     shards = c->peer.data() + (size_t)layer * c->cfg.world_size;
@@ -546,6 +565,10 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       return fail(ASYNCEP_ERR_NCCL, "ncclAllGather: %s", c->nccl.errstr ? c->nccl.errstr(r) : "error");
   }
   CUDA_TRY(cudaEventRecord(c->ag_done[s], c->ms));
+  if (tg1) {
+    CUDA_TRY(cudaEventRecord(tg1, c->ms));
+    c->tl_gather.push_back({layer, {tg0, tg1}});
+  }
   if (wi >= 0) {  // the gather has read the window buffer: it may be re-staged
     CUDA_TRY(cudaEventRecord(c->win_free[wi], c->ms));
     c->win_consumed[wi] = true;
@@ -1104,6 +1127,47 @@ asyncep_status asyncep_forward_times(asyncep_ctx* c, double* ms_out, int32_t* la
   return ASYNCEP_OK;
 }
 
+asyncep_status asyncep_timeline_begin(asyncep_ctx* c) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (!(c->cfg.flags & ASYNCEP_FLAG_STAGE_TIMING))
+    return fail(ASYNCEP_ERR_INVALID_ARG, "timeline needs a context created with ASYNCEP_FLAG_STAGE_TIMING");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  for (auto& g : c->tl_gather) {
+    cudaEventDestroy(g.second.first);
+    cudaEventDestroy(g.second.second);
+  }
+  c->tl_gather.clear();
+  c->tl.clear();
+  if (!c->epoch) CUDA_TRY(cudaEventCreate(&c->epoch));
+  CUDA_TRY(cudaEventRecord(c->epoch, c->cs));
+  if (c->ms) CUDA_TRY(cudaStreamWaitEvent(c->ms, c->epoch, 0));  // no gather starts before the epoch
+  c->timeline = true;
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_timeline_read(asyncep_ctx* c, asyncep_timeline_rec* out, int32_t n, int32_t* n_out) {
+  if (!c || n < 0 || (n > 0 && !out)) return fail(ASYNCEP_ERR_INVALID_ARG, "bad arguments");
+  if (!c->timeline) return fail(ASYNCEP_ERR_INVALID_ARG, "asyncep_timeline_begin was not called");
+  asyncep_status st = flush_timing(c);
+  if (st) return st;
+  for (auto& g : c->tl_gather) {
+    CUDA_TRY(cudaEventSynchronize(g.second.second));
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&a, c->epoch, g.second.first));
+    CUDA_TRY(cudaEventElapsedTime(&b, c->epoch, g.second.second));
+    c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_GATHER, g.first, a, b, b});
+    cudaEventDestroy(g.second.first);
+    cudaEventDestroy(g.second.second);
+  }
+  c->tl_gather.clear();
+  const int32_t m = (int32_t)std::min<size_t>((size_t)n, c->tl.size());
+  for (int32_t i = 0; i < m; ++i) out[i] = c->tl[(size_t)i];
+  if (n_out) *n_out = (int32_t)c->tl.size();
+  c->timeline = false;
+  return ASYNCEP_OK;
+}
+
 asyncep_status asyncep_calibrated_T(double gamma, double t_e, double t_c, double c_dummy, double* flops_out) {
   if (!(gamma >= 1.0) || !(t_c > 0) || !(t_e >= 0) || !(c_dummy >= 0))
     return fail(ASYNCEP_ERR_INVALID_ARG, "calibrated_T: need gamma >= 1, t_c > 0, t_e >= 0, C_dummy >= 0");
@@ -1276,6 +1340,11 @@ asyncep_status asyncep_destroy(asyncep_ctx* c) {
   }
   for (auto& e : c->ev_pool)
     if (e) cudaEventDestroy(e);
+  for (auto& g : c->tl_gather) {
+    cudaEventDestroy(g.second.first);
+    cudaEventDestroy(g.second.second);
+  }
+  if (c->epoch) cudaEventDestroy(c->epoch);
   for (auto& e : c->h2d_done)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->win_free)

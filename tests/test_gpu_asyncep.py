@@ -293,3 +293,30 @@ def test_stack_output_fed_back_as_input(L):
     ref = wl.stack(max_tokens=T).run(y1_copy).clone()
     torch.cuda.synchronize()
     assert torch.equal(_bits(y2), _bits(ref))
+
+
+def test_timeline_orders_gather_before_its_gemms():
+    """asyncep_timeline: every gathered layer's GEMM1 starts after its gather ended (the event order
+    the slot's ag_done wait enforces), the resident layer 0 has no gather, and forwards follow each
+    other on the compute stream."""
+    wl = Workload(L=4, E=16, k=4, H=256, h=256, seed=19)
+    T = 1024
+    x = wl.tokens(T)
+    st = wl.stack(max_tokens=T, world_size=4, flags=A.FLAG_STAGE_TIMING)
+    sh = st.peer_shards()
+    st.run(x, local_shards=sh)
+    A.asyncep_timeline_begin(st.ctx)
+    st.run(x, local_shards=sh)
+    torch.cuda.synchronize()
+    recs = A.asyncep_timeline_read(st.ctx)
+    fwd = {l: (a, b, c) for k, l, a, b, c in recs if k == "forward"}
+    gat = {l: (a, b) for k, l, a, b, _ in recs if k == "gather"}
+    assert sorted(fwd) == [0, 1, 2, 3] and sorted(gat) == [1, 2, 3]
+    for l in (1, 2, 3):
+        assert gat[l][0] <= gat[l][1] <= fwd[l][1] + 1e-3   # GEMM1 waits for the slot
+    for l in range(4):
+        assert fwd[l][0] <= fwd[l][1] <= fwd[l][2]
+        if l:
+            assert fwd[l - 1][2] <= fwd[l][0] + 1e-3
+    with pytest.raises(A.AsyncEPError):
+        A.asyncep_timeline_read(st.ctx)   # the capture ended
