@@ -316,8 +316,9 @@ ASYNCEP_API asyncep_status asyncep_forward_times(asyncep_ctx* ctx, double* ms_ou
  * waits for it), then every forward (ASYNCEP_FLAG_STAGE_TIMING) and every gather is recorded until
  * asyncep_timeline_read, which synchronises, writes up to n records in issue order -- forwards
  * first as they flush, then gathers -- and ends the capture; n_out = records available.
- *   FORWARD: t0 = start (router), t1 = GEMM1 start (after the wait for the slot), t2 = end (combine)
- *   GATHER : t0 = start of the layer's gather on the comm stream, t1 = t2 = its end (ag_done)
+ *   FORWARD: t0 = start (router), t1 = dispatch done (the wait for the slot begins), t2 = GEMM1
+ *            start (the wait ended), t3 = end (combine)
+ *   GATHER : t0 = start of the layer's gather on the comm stream, t1 = t2 = t3 = its end (ag_done)
  * Times are ms since the epoch.  Errors: INVALID_ARG (no timing flag / no begin), CUDA.
  */
 #define ASYNCEP_TL_FORWARD 0
@@ -325,7 +326,7 @@ ASYNCEP_API asyncep_status asyncep_forward_times(asyncep_ctx* ctx, double* ms_ou
 typedef struct {
   int32_t kind;  /* ASYNCEP_TL_* */
   int32_t layer;
-  float t0, t1, t2;
+  float t0, t1, t2, t3;
 } asyncep_timeline_rec;
 ASYNCEP_API asyncep_status asyncep_timeline_begin(asyncep_ctx* ctx);
 ASYNCEP_API asyncep_status asyncep_timeline_read(asyncep_ctx* ctx, asyncep_timeline_rec* out, int32_t n,

@@ -351,7 +351,7 @@ def asyncep_calibrate_T(ctx: Context, gamma: float, n_ref: int):
 
 class TimelineRec(ctypes.Structure):
     _fields_ = [("kind", ctypes.c_int32), ("layer", ctypes.c_int32), ("t0", ctypes.c_float),
-                ("t1", ctypes.c_float), ("t2", ctypes.c_float)]
+                ("t1", ctypes.c_float), ("t2", ctypes.c_float), ("t3", ctypes.c_float)]
 
 
 def asyncep_timeline_begin(ctx: Context) -> None:
@@ -359,11 +359,13 @@ def asyncep_timeline_begin(ctx: Context) -> None:
 
 
 def asyncep_timeline_read(ctx: Context, n: int = 4096):
-    """-> [(kind 'forward'|'gather', layer, t0, t1, t2)] in ms since asyncep_timeline_begin."""
+    """-> [(kind 'forward'|'gather', layer, t0, t1, t2, t3)] in ms since asyncep_timeline_begin:
+    forward = (start, dispatch done, GEMM1 start, end), gather = (start, end, end, end)."""
     buf = (TimelineRec * n)()
     m = ctypes.c_int32()
     _check(lib().asyncep_timeline_read(ctx.handle, buf, n, ctypes.byref(m)))
-    return [("forward" if r.kind == 0 else "gather", r.layer, r.t0, r.t1, r.t2) for r in buf[:min(n, m.value)]]
+    return [("forward" if r.kind == 0 else "gather", r.layer, r.t0, r.t1, r.t2, r.t3)
+            for r in buf[:min(n, m.value)]]
 
 
 def asyncep_reset_stage_times(ctx: Context) -> None:

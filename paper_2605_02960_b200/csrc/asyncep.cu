@@ -339,11 +339,12 @@ asyncep_status flush_timing(asyncep_ctx* c, bool blocking = true) {
     CUDA_TRY(cudaEventElapsedTime(&tot, e[0], e[kStages]));
     c->recent.emplace_back(c->ev_layer[(size_t)c->ev_head], (double)tot);
     if (c->timeline && c->epoch) {
-      float t0 = 0.f, t3 = 0.f, t6 = 0.f;
+      float t0 = 0.f, t2 = 0.f, t3 = 0.f, t6 = 0.f;
       CUDA_TRY(cudaEventElapsedTime(&t0, c->epoch, e[0]));
+      CUDA_TRY(cudaEventElapsedTime(&t2, c->epoch, e[2]));
       CUDA_TRY(cudaEventElapsedTime(&t3, c->epoch, e[3]));
       CUDA_TRY(cudaEventElapsedTime(&t6, c->epoch, e[kStages]));
-      c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_FORWARD, c->ev_layer[(size_t)c->ev_head], t0, t3, t6});
+      c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_FORWARD, c->ev_layer[(size_t)c->ev_head], t0, t2, t3, t6});
     }
     if (c->recent.size() > 4096) c->recent.erase(c->recent.begin(), c->recent.begin() + 2048);
     c->ev_head = (c->ev_head + 1) % kMaxPendingFwd;
@@ -1156,7 +1157,7 @@ asyncep_status asyncep_timeline_read(asyncep_ctx* c, asyncep_timeline_rec* out, 
     float a = 0.f, b = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&a, c->epoch, g.second.first));
     CUDA_TRY(cudaEventElapsedTime(&b, c->epoch, g.second.second));
-    c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_GATHER, g.first, a, b, b});
+    c->tl.push_back(asyncep_timeline_rec{ASYNCEP_TL_GATHER, g.first, a, b, b, b});
     cudaEventDestroy(g.second.first);
     cudaEventDestroy(g.second.second);
   }

@@ -1,7 +1,8 @@
 """Per-layer event timeline of one step of the 8-layer Qwen3-235B stack with the N-rank gather
 emulated on one B200 (asyncep_timeline_begin / _read: the view an nsys trace would give).  For each
 layer: forward start, GEMM1 start (after the wait for the gathered slot), end; and the gather of
-that layer on the comm stream.  JSON to stdout, plus an ASCII chart on stderr.
+that layer on the comm stream.  JSON to stdout, plus an ASCII chart on stderr ('=' compute,
+'.' waiting for the gathered slot, '|' GEMM1 start, '#' the gather).
 
     python profiles/timeline.py [--fp8] [--tokens 32768] [--N 8] [--link-gbs 770]
 """
@@ -47,22 +48,24 @@ def main():
     st.run(x, out=out, local_shards=shards)
     torch.cuda.synchronize()
     recs = A.asyncep_timeline_read(st.ctx)
-    fwd = {l: (a, b, c) for k, l, a, b, c in recs if k == "forward"}
-    gat = {l: (a, b) for k, l, a, b, _ in recs if k == "gather"}
+    fwd = {l: (a, b, c, d) for k, l, a, b, c, d in recs if k == "forward"}
+    gat = {l: (a, b) for k, l, a, b, _, _ in recs if k == "gather"}
     layers = []
     for l in range(L):
         f = fwd[l]
         g = gat.get(l)
-        layers.append({"layer": l, "forward_start": f[0], "gemm1_start": f[1], "forward_end": f[2],
-                       "gather_start": g[0] if g else None, "gather_end": g[1] if g else None,
-                       "wait_ms": max(0.0, (g[1] if g else 0.0) - (f[1] if g else 0.0)) if g else 0.0})
+        layers.append({"layer": l, "forward_start": f[0], "dispatch_done": f[1], "gemm1_start": f[2],
+                       "forward_end": f[3], "gather_start": g[0] if g else None, "gather_end": g[1] if g else None,
+                       "wait_ms": f[2] - f[1]})
     print(json.dumps({"fp8": args.fp8, "tokens": args.tokens, "N": args.N, "link_gbs": args.link_gbs,
-                      "step_ms": fwd[L - 1][2] - fwd[0][0], "layers": layers}), flush=True)
-    scale = 100.0 / (fwd[L - 1][2] + 1e-9)
+                      "step_ms": fwd[L - 1][3] - fwd[0][0], "layers": layers}), flush=True)
+    scale = 100.0 / (fwd[L - 1][3] + 1e-9)
     for d in layers:
         row = [" "] * 101
         for t in range(int(d["forward_start"] * scale), int(d["forward_end"] * scale) + 1):
             row[min(t, 100)] = "="
+        for t in range(int(d["dispatch_done"] * scale), int(d["gemm1_start"] * scale) + 1):
+            row[min(t, 100)] = "."
         row[min(int(d["gemm1_start"] * scale), 100)] = "|"
         print(f"L{d['layer']} fwd {''.join(row)}", file=sys.stderr)
         if d["gather_start"] is not None:

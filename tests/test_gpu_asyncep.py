@@ -309,14 +309,14 @@ def test_timeline_orders_gather_before_its_gemms():
     st.run(x, local_shards=sh)
     torch.cuda.synchronize()
     recs = A.asyncep_timeline_read(st.ctx)
-    fwd = {l: (a, b, c) for k, l, a, b, c in recs if k == "forward"}
-    gat = {l: (a, b) for k, l, a, b, _ in recs if k == "gather"}
+    fwd = {l: (a, b, c, d) for k, l, a, b, c, d in recs if k == "forward"}
+    gat = {l: (a, b) for k, l, a, b, _, _ in recs if k == "gather"}
     assert sorted(fwd) == [0, 1, 2, 3] and sorted(gat) == [1, 2, 3]
     for l in (1, 2, 3):
-        assert gat[l][0] <= gat[l][1] <= fwd[l][1] + 1e-3   # GEMM1 waits for the slot
+        assert gat[l][0] <= gat[l][1] <= fwd[l][2] + 1e-3   # GEMM1 waits for the slot
     for l in range(4):
-        assert fwd[l][0] <= fwd[l][1] <= fwd[l][2]
+        assert fwd[l][0] <= fwd[l][1] <= fwd[l][2] <= fwd[l][3]
         if l:
-            assert fwd[l - 1][2] <= fwd[l][0] + 1e-3
+            assert fwd[l - 1][3] <= fwd[l][0] + 1e-3
     with pytest.raises(A.AsyncEPError):
         A.asyncep_timeline_read(st.ctx)   # the capture ended
