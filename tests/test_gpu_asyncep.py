@@ -320,3 +320,19 @@ def test_timeline_orders_gather_before_its_gemms():
             assert fwd[l - 1][3] <= fwd[l][0] + 1e-3
     with pytest.raises(A.AsyncEPError):
         A.asyncep_timeline_read(st.ctx)   # the capture ended
+
+
+@pytest.mark.parametrize("fp8", [False, True], ids=["bf16", "fp8"])
+def test_sharded_stack_with_swap_tails_bitwise(fp8):
+    """Swap-AB tail tiles on gathered layers: this rank's own experts come through the second weight
+    map (own shard in place), the others through the slot -- both in the swapped orientation; the
+    4-rank emulated stack stays bitwise equal to the resident one (both with FLAG_SWAP_TAILS)."""
+    wl = Workload(L=3, E=16, k=4, H=512, h=256, seed=29, fp8=fp8)
+    T = 700  # ~175-row tails per expert: every expert's last tile is a swap tile
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T, flags=A.FLAG_SWAP_TAILS).run(x).clone()
+    for rank in (0, 3):
+        st = wl.stack(max_tokens=T, world_size=4, rank=rank, flags=A.FLAG_SWAP_TAILS)
+        out = st.run(x, local_shards=st.peer_shards()).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(_bits(out), _bits(ref)), rank
