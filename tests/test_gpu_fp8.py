@@ -79,3 +79,26 @@ def test_fp8_fused_dispatch_bitwise(T):
         outs.append(run_layer(wl, st, 0, x)[0])
         del st
     assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
+@pytest.mark.parametrize("shape,T,zipf", [((128, 8, 2048, 768), 16384, 0.0), ((128, 8, 4096, 1536), 32768, 0.35)],
+                         ids=["qwen3_30b_16k", "qwen3_235b_zipf"])
+def test_fp8_other_configs_sampled(shape, T, zipf):
+    """FP8 experts on the other BASELINE workloads: the Qwen3-30B layer shape (config 2) and the
+    Zipf-skewed routing of config 5 (s = 0.35, reading R14) -- 48 sampled tokens against both oracles,
+    the counts against the histogram of the GPU ids over all tokens."""
+    E, k, H, h = shape
+    wl = Workload(L=1, E=E, k=k, H=H, h=h, seed=3, fp8=True, zipf_s=zipf)
+    st = wl.stack(max_tokens=T)
+    x = wl.tokens(T)
+    y, ids, w, counts = run_layer(wl, st, 0, x, residual=False)
+    assert np.array_equal(counts, np.bincount(ids.ravel(), minlength=E)) and counts.sum() == T * k
+    if zipf:
+        assert counts.max() / max(counts.min(), 1) >= 8
+    del st
+    torch.cuda.empty_cache()
+    idx = np.unique(np.concatenate([[0, T - 1], np.random.default_rng(4).choice(T, 46, replace=False)]))
+    wr, g, u, d = wl.host_layer_subset(0, ids[idx].ravel())
+    xs = f32(x)[idx]
+    check_layer(xs, wr, g, u, d, k, y[idx], ids[idx], w[idx], None, residual=False, tol=6e-2)
+    check_layer(xs, wr, g, u, d, k, y[idx], ids[idx], w[idx], None, residual=False, tol=1e-2, act_quant=True)
