@@ -528,11 +528,18 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     CUDA_TRY(cudaStreamWaitEvent(c->ms, c->h2d_done[wi], 0));
     own = c->window[wi];
   }
-  cudaEvent_t tg0 = nullptr, tg1 = nullptr;
+  // timeline events of this gather, released on every early return (kept on success)
+  struct TlEvents {
+    cudaEvent_t a = nullptr, b = nullptr;
+    ~TlEvents() {
+      if (a) cudaEventDestroy(a);
+      if (b) cudaEventDestroy(b);
+    }
+  } tg;
   if (c->timeline) {
-    CUDA_TRY(cudaEventCreate(&tg0));
-    CUDA_TRY(cudaEventCreate(&tg1));
-    CUDA_TRY(cudaEventRecord(tg0, c->ms));
+    CUDA_TRY(cudaEventCreate(&tg.a));
+    CUDA_TRY(cudaEventCreate(&tg.b));
+    CUDA_TRY(cudaEventRecord(tg.a, c->ms));
   }
   if (!shards && tr != ASYNCEP_GATHER_NCCL) {  // P2P gather over the IPC-mapped peer shards
     if (c->peer.empty()) return fail(ASYNCEP_ERR_INVALID_ARG, "copy transport without peer shards (asyncep_set_peer_shards)");
@@ -566,9 +573,10 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       return fail(ASYNCEP_ERR_NCCL, "ncclAllGather: %s", c->nccl.errstr ? c->nccl.errstr(r) : "error");
   }
   CUDA_TRY(cudaEventRecord(c->ag_done[s], c->ms));
-  if (tg1) {
-    CUDA_TRY(cudaEventRecord(tg1, c->ms));
-    c->tl_gather.push_back({layer, {tg0, tg1}});
+  if (tg.b) {
+    CUDA_TRY(cudaEventRecord(tg.b, c->ms));
+    c->tl_gather.push_back({layer, {tg.a, tg.b}});
+    tg.a = tg.b = nullptr;  // owned by the context now
   }
   if (wi >= 0) {  // the gather has read the window buffer: it may be re-staged
     CUDA_TRY(cudaEventRecord(c->win_free[wi], c->ms));
