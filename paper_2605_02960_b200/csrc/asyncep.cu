@@ -268,7 +268,8 @@ struct asyncep_ctx {
   std::vector<int32_t> ev_layer;                 // layer of the forward in each ring slot
   std::vector<std::pair<int32_t, double>> recent;  // (layer, total ms) of flushed forwards
   // event timeline (asyncep_timeline_begin / _read): epoch on both streams, then per forward
-  // (start, GEMM1 start = after the gather wait, end) and per gather (start, end), ms since epoch
+  // (start, dispatch done, GEMM1 start = after the slot wait, end) and per gather (start, end),
+  // ms since the epoch
   cudaEvent_t epoch = nullptr;
   bool timeline = false;
   std::vector<asyncep_timeline_rec> tl;                          // flushed records
