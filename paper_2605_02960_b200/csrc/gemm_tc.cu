@@ -92,7 +92,6 @@ struct TcArgs {
   int raster;   // 0: row-tile-major order; G > 0: groups of G row tiles walked row-first
   int pol_a, pol_b;  // L2 policy of the A / B loads: 0 normal, 1 evict_last, 2 evict_first, 3 none (A)
   int pol_gather;    // L2 policy of the fused dispatch's cp.async row gathers: 0 normal, 1 evict_last, 2 evict_first
-  int gather_pf;     // > 0: the pair starting N tile 0 of row tile mt L2-prefetches the token rows of row tile mt + gather_pf
   // FP8 (kind::f8f6f4) scales: dequantised D[r][c] = acc * a_scale[r] * b_scale(e)[B row of c]
   const float* a_scale;
   const uint8_t* b_scale_base;  // layer base + offset of the scale block inside an expert blob
@@ -524,20 +523,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       const uint8_t* src[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) src[i] = p.gather_src + (int64_t)tok[i] * p.gather_ld + ch * 16;
-      if (p.gather_pf > 0) {
-        // one CTA pair per row tile (the one taking N tile 0) pulls the token rows of a row tile
-        // gather_pf ahead into L2: this CTA's 128 rows there, 2 rows per gather thread
-        int mt, nt;
-        decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
-        const int mp = mt + p.gather_pf;
-        if (nt == 0 && mp < total_rt) {
-          const int r0 = mp * TM + (int)rank * BM + gt * 2;
-#pragma unroll
-          for (int q = 0; q < 2; ++q)
-            prefetch_l2_bulk(p.gather_src + (int64_t)__ldg(p.gather_rows + r0 + q) * p.gather_ld,
-                             (uint32_t)p.gather_ld);
-        }
-      }
       for (int kb = 0; kb < nkb; ++kb) {
         WP_WAIT(wp_e, mbar_wait(&empty[stage], phase ^ 1))
         const uint32_t dst = base + (uint32_t)(stage * A_BYTES);
@@ -983,7 +968,6 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.pol_a = env_int("ASYNCEP_POL_A", 0);
   a.pol_b = env_int("ASYNCEP_POL_B", 1);
   a.pol_gather = env_int("ASYNCEP_POL_GATHER", 1);
-  a.gather_pf = env_int("ASYNCEP_GATHER_PF", 0);
   a.gather_rows = gather_rows;
   a.gather_src = static_cast<const uint8_t*>(gather_src);
   a.gather_ld = gather_ld;
