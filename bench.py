@@ -295,6 +295,9 @@ def main():
                     help="prompt length of the packed batch with --attn (tokens/GPU split into prompts)")
     ap.add_argument("--fp8", action="store_true",
                     help="FP8 e4m3 experts (BASELINE config 4) instead of BF16 (config 3)")
+    ap.add_argument("--graph", action="store_true",
+                    help="N=1 resident stack only: capture one step into a CUDA graph and time its replays "
+                         "(no per-stage events inside a graph, so no stage times / roofline)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -332,14 +335,18 @@ def main():
                 raise SystemExit("--gather nccl / --ep need the NCCL backend")
     L, T = args.layers, args.tokens
     seed = 0
-    flags = A.FLAG_STAGE_TIMING | (A.FLAG_SIMT_GEMM if args.simt else 0) | (A.FLAG_XPERM if args.xperm else 0)
+    if args.graph and (world > 1 or args.emulate_gather or args.ep or args.offload):
+        raise SystemExit("--graph: resident single-GPU stacks only (the gather's events cross steps)")
+    flags = (0 if args.graph else A.FLAG_STAGE_TIMING) | (A.FLAG_SIMT_GEMM if args.simt else 0) | \
+        (A.FLAG_XPERM if args.xperm else 0)
+    graph_stream = torch.cuda.Stream(dev) if args.graph else None
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
     emu = args.emulate_gather if world == 1 else 0
     router_fn = lambda l: synth.router_weight(E_, H_, seed, l, device=dev, zipf_s=args.zipf)
     expert_fn = lambda l, ex: gen(E_, H_, h_, seed, l, device=dev, experts=ex)
     stack = MoEStack(L, E_, K_, H_, h_, T, router_fn, expert_fn,
                      world_size=emu or world, rank=rank, replicate_layer0=True, flags=flags, device=dev,
-                     nccl_comm=comm, fp8=args.fp8, offload_window=args.offload)
+                     nccl_comm=comm, fp8=args.fp8, offload_window=args.offload, compute_stream=graph_stream)
     local_shards = stack.peer_shards() if emu > 1 else None
     gathered = (world > 1 or emu > 1) and not args.ep
     reserve_nccl = int(os.environ.get("ASYNCEP_RESERVE_SMS", "16"))
@@ -443,6 +450,21 @@ def main():
             chosen = cands[0]
         A.asyncep_set_gather_transport(stack.ctx, chosen, reserve_nccl if chosen == A.GATHER_NCCL else 0)
 
+    if args.graph:  # one step captured on the stack's (non-default) compute stream, replayed per step
+        with torch.cuda.stream(cs):
+            _run(x, out)
+            cs.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=cs):
+                stack.run(x, out=out, cu_seqlens=cu)
+        _eager = _run
+
+        def _run(xin, o):  # the captured buffers replay the graph on cs; others (e2e) run eagerly
+            if xin is x and o is out:
+                with torch.cuda.stream(cs):
+                    graph.replay()
+            else:
+                _eager(xin, o)
     for _ in range(args.warmup):
         _run(x, out)
     barrier()
@@ -640,6 +662,8 @@ def main():
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
                    "parallelism": par, "gather": gather_desc,
+                   "launch": ("one step captured as a CUDA graph, replayed per timed step (e2e runs eagerly)"
+                              if args.graph else "eager stream launches"),
                    "l2": (f"inputs larger than L2 ({L * E_ * 3 * H_ * h_ * (1 if args.fp8 else 2) / 1e9:.1f} GB expert "
                           f"weights + {T * K_ * H_ * 2 / 1e6:.0f} MB Y_perm per layer streamed each step, "
                           f"{T * H_ * 2 / 1e6:.0f} MB token activations); no flush")},
