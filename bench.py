@@ -455,8 +455,10 @@ def main():
             _run(x, out)
             cs.synchronize()
             graph = torch.cuda.CUDAGraph()
+            l0 = A.asyncep_kernel_launches(stack.ctx)
             with torch.cuda.graph(graph, stream=cs):
                 stack.run(x, out=out, cu_seqlens=cu)
+            graph_launches = A.asyncep_kernel_launches(stack.ctx) - l0  # kernels inside one replay
         _eager = _run
 
         def _run(xin, o):  # the captured buffers replay the graph on cs; others (e2e) run eagerly
@@ -484,6 +486,8 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     launches = A.asyncep_kernel_launches(stack.ctx) - launches0
+    if args.graph:
+        launches = graph_launches * args.steps
     stages, nfwd = A.asyncep_stage_times(stack.ctx)
     ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
