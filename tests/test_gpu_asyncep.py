@@ -195,6 +195,19 @@ def test_nccl_allgather_path_with_borrowed_torch_comm():
         assert torch.equal(st.slots[1][:half], st.shards[1])
         assert torch.equal(st.slots[1][:half], full.shards[1][:half])
         assert torch.all(st.slots[1][half:] == 0xAB)  # the absent rank's half is untouched
+        # the explicit NCCL transport with SMs reserved for NCCL's kernels, and the startup probe
+        A.asyncep_set_gather_transport(st.ctx, A.GATHER_NCCL, 16)
+        st.slots[0].fill_(0xCD)
+        ms, nbytes = A.asyncep_probe_gather(st.ctx, 2)
+        torch.cuda.synchronize()
+        assert ms > 0 and nbytes == half  # (N - 1) x shard bytes
+        assert torch.equal(st.slots[0][:half], st.shards[2])
+        A.asyncep_prefetch_layer(st.ctx, 2)     # the probe handed the slot back
+        st.forward(2, x, y=torch.empty_like(x))
+        torch.cuda.synchronize()
+        with pytest.raises(A.AsyncEPError):
+            A.asyncep_set_gather_transport(st.ctx, A.GATHER_COPY_KERNEL, 0)
+            A.asyncep_prefetch_layer(st.ctx, 1)  # copy transport without peer shards
     finally:
         dist.destroy_process_group()
 
