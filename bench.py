@@ -486,6 +486,14 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     launches = A.asyncep_kernel_launches(stack.ctx) - launches0
+    # NEXT-1 (App. B.4): T from the last timed step as the profile pass -- t_c = the
+    # resident layer 0, t_e = the slowest gathered layer, C_dummy = f_tok x tokens (in the library)
+    calib = None
+    if not args.graph and not args.ep and L > 1:
+        try:
+            calib = A.asyncep_calibrate_T(stack.ctx, 1.2, T)
+        except A.AsyncEPError as e:
+            calib = {"error": str(e)[:200]}
     if args.graph:
         launches = graph_launches * args.steps
     stages, nfwd = A.asyncep_stage_times(stack.ctx)
@@ -688,6 +696,7 @@ def main():
         "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
                          "flops_per_s": f_gemm, "ag_bytes_per_s": bw, "ag_bandwidth_source": bw_src,
                          "note": "Eq. 1 per layer, F = measured grouped-GEMM rate of this run"},
+        "calibrated_T": calib,
         "layer_ms": step_layer_ms,
         "exposed_ag": exposed,
         "gather_transports": transports or None,
