@@ -434,7 +434,7 @@ def main():
             A.asyncep_set_gather_transport(stack.ctx, tr, reserve_nccl if tr == A.GATHER_NCCL else 0)
             barrier()
             probe = None
-            if probe_layer >= 1:
+            if probe_layer >= 1 and not args.offload:  # (offload: a gather follows its H2D stage)
                 ms_p, nbytes = A.asyncep_probe_gather(stack.ctx, probe_layer,
                                                       local_shards(probe_layer) if local_shards else None)
                 ms_p = max_over_ranks(ms_p)
