@@ -585,6 +585,10 @@ def main():
     # and tokens, every layer resident in the second stack; step by step, interleaved.
     exposed = {"ms_per_layer": 0.0, "frac_of_layer": 0.0, "wait_ms_per_layer": per_layer_ms["gather_wait"],
                "note": "N=1: every layer resident, nothing gathered"}
+    if gathered or args.offload:
+        exposed = {"ms_per_layer": None, "frac_of_layer": None, "wait_ms_per_layer": per_layer_ms["gather_wait"],
+                   "note": "resident-vs-gathered A/B not run (--no-ab, or a one-layer stack); the wait for the "
+                           "slot (or the H2D window) before GEMM1 only"}
     if gathered and not args.no_ab and L > 1:
         res = MoEStack(L, E_, K_, H_, h_, T, router_fn, expert_fn, world_size=1, rank=0, replicate_layer0=True,
                        flags=flags & ~A.FLAG_STAGE_TIMING, device=dev, fp8=args.fp8,
