@@ -488,8 +488,8 @@ def main():
     launches = A.asyncep_kernel_launches(stack.ctx) - launches0
     # NEXT-1 (App. B.4): T from the last timed step as the profile pass -- t_c = the
     # resident layer 0, t_e = the slowest gathered layer, C_dummy = f_tok x tokens (in the library)
-    calib = None
-    if not args.graph and not args.ep and L > 1:
+    calib = None  # (N = 1 without offload: nothing is transferred, Eq. 3 has no t_EP to calibrate)
+    if not args.graph and not args.ep and L > 1 and (gathered or args.offload):
         try:
             calib = A.asyncep_calibrate_T(stack.ctx, 1.2, T)
         except A.AsyncEPError as e:
