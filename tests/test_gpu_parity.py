@@ -314,3 +314,25 @@ def test_swap_tail_tiles(T, fp8):
     assert np.array_equal(ia, ib)
     diff = np.abs(ya - yb).max() / max(np.abs(yb).max(), 1e-30)
     assert diff <= (2e-2 if fp8 else 1e-2), diff
+
+
+@pytest.mark.parametrize("fp8", [False, True], ids=["bf16", "fp8"])
+def test_qwen3_235b_64k_tokens_sampled(fp8):
+    """The largest per-GPU batch of the BASELINE sweeps (64K tokens/GPU, Qwen3-235B layer): ~2x the
+    bench's row offsets and tile tables (524K permuted rows, ~2,100 pair row tiles); counts =
+    histogram of the GPU ids over all tokens, 32 sampled tokens through the acceptance procedure
+    (FP8 also against the emulating oracle)."""
+    T = 65536
+    wl = Workload(L=1, E=128, k=8, H=4096, h=1536, seed=8, fp8=fp8)
+    st = wl.stack(max_tokens=T)
+    x = wl.tokens(T)
+    y, ids, w, counts = run_layer(wl, st, 0, x)
+    assert np.array_equal(counts, np.bincount(ids.ravel(), minlength=wl.E)) and counts.sum() == T * wl.k
+    del st
+    torch.cuda.empty_cache()
+    idx = np.unique(np.concatenate([[0, T - 1], np.random.default_rng(11).choice(T, 30, replace=False)]))
+    wr, g, u, d = wl.host_layer_subset(0, ids[idx].ravel())
+    xs = f32(x)[idx]
+    check_layer(xs, wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None, tol=6e-2 if fp8 else 2e-2)
+    if fp8:
+        check_layer(xs, wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None, tol=1e-2, act_quant=True)
