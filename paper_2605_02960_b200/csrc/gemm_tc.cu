@@ -1155,21 +1155,15 @@ bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E) {
   const uint64_t strides[2] = {(uint64_t)H * 2, (uint64_t)H * 2 * E};
   const uint32_t box[3] = {BK, (uint32_t)rt.E_pad, 1};
   const uint32_t box2[3] = {BK, (uint32_t)rt.E_pad / 2, 1};
-  const uint32_t box128[3] = {BK, 128, 1};
-  static const bool swap_ok = env_int("ASYNCEP_ROUTER_SWAP", 1) != 0;
-  rt.swap = swap_ok && router_swap_ok(E, H);
   return encode_tmap(&rt.map_wr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box,
                      CU_TENSOR_MAP_SWIZZLE_128B) &&
          encode_tmap(&rt.map_wr2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box2,
-                     CU_TENSOR_MAP_SWIZZLE_128B) &&
-         encode_tmap(&rt.map_wr128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, wr, dims, strides, box128,
                      CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
                       int32_t* ids, float* w, int num_sms, cudaStream_t s, int* sched) {
   if (T <= 0) return true;
-  if (rt.swap) return launch_router_swap(rt.map_wr128, x, T, H, E, k, norm_topk, ids, w, s);
   CUtensorMap map_x;
   const uint64_t dims[2] = {(uint64_t)H, (uint64_t)T};
   const uint64_t strides[1] = {(uint64_t)H * 2};

@@ -27,16 +27,11 @@ struct RouterTc {
   CUtensorMap map_wr2; // same, box {64, E_pad / 2, 1}: the half each CTA of a pair loads
   int E_pad;           // E rounded up to a multiple of 16 (MMA N)
   bool pair;           // E_pad >= 64 (and a multiple of 32): CTA-pair router, 256 tokens per tile
-  CUtensorMap map_wr128;  // box {64, 128 rows}: the experts-as-M router (rows >= E zero-filled)
-  bool swap;           // E <= 128: experts-as-M router (launch_router_swap), one wave of 256-token tiles
 };
 bool make_router_wmap(RouterTc& rt, const bf16* wr, int H, int E);
 // x map is built per call (x is the caller's buffer): [T, H] bf16, box {64, 128}
 bool launch_router_tc(const RouterTc& rt, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
                       int32_t* ids, float* w, int num_sms, cudaStream_t s, int* sched = nullptr);
-bool router_swap_ok(int E, int H);
-bool launch_router_swap(const CUtensorMap& map_wr128, const bf16* x, int64_t T, int H, int E, int k, int norm_topk,
-                        int32_t* ids, float* w, cudaStream_t s);
 
 // Step (2): permute / dispatch.
 void launch_perm_hist(const int32_t* ids, int64_t T, int k, int E, int32_t* blk_counts, cudaStream_t s);

@@ -271,13 +271,12 @@ def test_qwen3_235b_eight_layer_stack_sampled(fp8):
         del wr, g, u, d
 
 
-@pytest.mark.parametrize("E,k", [(64, 12), (96, 8), (80, 8), (128, 8), (256, 8), (144, 6)],
-                         ids=["swap_router_top12", "swap_router_E96", "swap_router_E80", "swap_router_E128",
-                              "pair_router_E256", "cta_router_E144"])
+@pytest.mark.parametrize("E,k", [(64, 12), (96, 8), (80, 8)], ids=["pair_router_top12", "pair_router_E96",
+                                                                   "cta_router_E80"])
 def test_router_tile_shapes(E, k):
-    """Router paths: experts-as-M tiles (E <= 128; the 16-wide top-k for k = 12, E not a multiple of
-    16 or 32 -> zero-filled weight rows), CTA pairs (E = 256) and the 1-CTA fallback (E_pad = 144 is
-    not a multiple of 32); 700 tokens = 2 full 256-token tiles + a ragged one."""
+    """Router paths: CTA pairs with the 16-wide top-k epilogue (E=64, k=12), pairs with N = 96, and the
+    1-CTA fallback (E_pad = 80 is not a multiple of 32); 700 tokens = 2 full 256-token pair tiles + a
+    ragged one."""
     wl = Workload(L=1, E=E, k=k, H=512, h=256, seed=13)
     st = wl.stack(max_tokens=700)
     x = wl.tokens(700)
