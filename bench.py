@@ -429,6 +429,9 @@ def main():
                 cands.append(A.GATHER_NCCL)
         if not cands:
             raise SystemExit(f"no gather transport available (p2p: {p2p_error}, nccl comm: {comm is not None})")
+        if A.GATHER_NCCL in cands:  # NCCL's gather kernels confined to the SMs the GEMMs leave free
+            _gather_pg, gather_comm = A.nccl_gather_group(reserve_nccl)
+            A.asyncep_set_gather_comm(stack.ctx, gather_comm)
         probe_layer = 1 if L > 1 else 0
         for tr in cands:
             A.asyncep_set_gather_transport(stack.ctx, tr, reserve_nccl if tr == A.GATHER_NCCL else 0)
@@ -443,7 +446,8 @@ def main():
                 _run(x, out)
             ms_tr = timed_steps(2) if len(cands) > 1 else None
             transports[A.GATHER_NAMES[tr]] = {"probe": probe, "ms_per_step": ms_tr,
-                                              "reserve_sms": reserve_nccl if tr == A.GATHER_NCCL else 0}
+                                              "reserve_sms": reserve_nccl if tr == A.GATHER_NCCL else 0,
+                                              **({"nccl_max_ctas": reserve_nccl} if tr == A.GATHER_NCCL else {})}
         if len(cands) > 1:
             chosen = min(cands, key=lambda t: transports[A.GATHER_NAMES[t]]["ms_per_step"])
         else:

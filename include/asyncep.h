@@ -202,6 +202,11 @@ ASYNCEP_API asyncep_status asyncep_set_peer_shards(asyncep_ctx* ctx, const void*
 #define ASYNCEP_GATHER_NCCL 2
 ASYNCEP_API asyncep_status asyncep_set_gather_transport(asyncep_ctx* ctx, int32_t transport, int32_t reserve_sms);
 
+/* Communicator of the NCCL gather (ASYNCEP_GATHER_NCCL): e.g. a dedicated one whose NCCL config
+ * caps its kernels at the SMs the GEMMs leave free (maxCTAs = reserve_sms); NULL = the context's
+ * communicator.  Borrowed: it must outlive its use.  Errors: INVALID_ARG, NCCL (no NCCL loaded). */
+ASYNCEP_API asyncep_status asyncep_set_gather_comm(asyncep_ctx* ctx, void* nccl_comm);
+
 /* Measurement knob: CTAs of the co-resident copy kernel (0 = default: ASYNCEP_GATHER_CTAS, else
  * 1 per SM).  More CTAs keep more warps beside the GEMMs; NVLink latency needs ~1 MB in flight. */
 ASYNCEP_API asyncep_status asyncep_set_gather_copy_ctas(asyncep_ctx* ctx, int32_t ctas);

@@ -89,6 +89,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_prefetch_layer_local": ([P, I32, P], I32),
             "asyncep_set_gather_transport": ([P, I32, I32], I32),
             "asyncep_set_gather_copy_ctas": ([P, I32], I32),
+            "asyncep_set_gather_comm": ([P, P], I32),
             "asyncep_timeline_begin": ([P], I32),
             "asyncep_timeline_read": ([P, P, I32, ctypes.POINTER(I32)], I32),
             "asyncep_probe_gather": ([P, I32, P, ctypes.POINTER(D), ctypes.POINTER(D)], I32),
@@ -277,6 +278,23 @@ GATHER_NAMES = {GATHER_COPY_KERNEL: "copy_kernel", GATHER_COPY_ENGINE: "copy_eng
 
 def asyncep_set_gather_transport(ctx: Context, transport: int, reserve_sms: int = 0) -> None:
     _check(lib().asyncep_set_gather_transport(ctx.handle, int(transport), int(reserve_sms)))
+
+
+def asyncep_set_gather_comm(ctx: Context, nccl_comm) -> None:
+    """ncclComm_t (int) for the NCCL gather, or None for the context's communicator."""
+    _check(lib().asyncep_set_gather_comm(ctx.handle, nccl_comm))
+
+
+def nccl_gather_group(max_ctas: int):
+    """A dedicated NCCL process group over all ranks for the weight gather, its kernels capped at
+    max_ctas CTAs (the SMs the grouped GEMMs leave free); eagerly initialised.  -> (group, comm)."""
+    import torch.distributed as dist
+    opts = dist.ProcessGroupNCCL.Options()
+    opts.config.max_ctas = int(max_ctas)
+    opts.config.min_ctas = 1
+    g = dist.new_group(ranks=list(range(dist.get_world_size())), backend="nccl", pg_options=opts)
+    dist.all_reduce(torch.ones(1, device="cuda"), group=g)
+    return g, nccl_comm_ptr(g)
 
 
 def asyncep_set_gather_copy_ctas(ctx: Context, ctas: int) -> None:

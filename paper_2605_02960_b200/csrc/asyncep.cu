@@ -236,6 +236,7 @@ constexpr int kMaxPendingFwd = 512;
 struct asyncep_ctx {
   asyncep_config cfg;
   void* comm = nullptr;
+  void* gather_comm = nullptr;  // communicator of the NCCL gather (default: comm)
   NcclApi nccl;
   cudaStream_t cs = nullptr, ms = nullptr;
   std::vector<const void*> router_w, shard;
@@ -300,13 +301,17 @@ bool layer_resident(const asyncep_ctx* c, int l) {
 // An asynchronous NCCL fault (a peer died, a network error) surfaces at the next call instead of
 // as a hang (ncclCommGetAsyncError; ncclInProgress = 7 is not an error).
 asyncep_status check_nccl_async(asyncep_ctx* c) {
-  if (!c->comm || !c->nccl.async_err) return ASYNCEP_OK;
-  int e = 0;
-  const int r = c->nccl.async_err(c->comm, &e);
-  if (r == 0 && (e == 0 || e == 7)) return ASYNCEP_OK;
-  const int code = r ? r : e;
-  return fail(ASYNCEP_ERR_NCCL, "NCCL asynchronous error on the borrowed communicator: %s (%d)",
-              c->nccl.errstr ? c->nccl.errstr(code) : "?", code);
+  if (!c->nccl.async_err) return ASYNCEP_OK;
+  for (void* comm : {c->comm, c->gather_comm}) {
+    if (!comm) continue;
+    int e = 0;
+    const int r = c->nccl.async_err(comm, &e);
+    if (r == 0 && (e == 0 || e == 7)) continue;
+    const int code = r ? r : e;
+    return fail(ASYNCEP_ERR_NCCL, "NCCL asynchronous error on a borrowed communicator: %s (%d)",
+                c->nccl.errstr ? c->nccl.errstr(code) : "?", code);
+  }
+  return ASYNCEP_OK;
 }
 
 // the gather transport a prefetch uses
@@ -568,8 +573,9 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
       }
     }
   } else {
-    if (!c->comm) return fail(ASYNCEP_ERR_NCCL, "no NCCL communicator (use asyncep_prefetch_layer_local)");
-    const int r = c->nccl.allgather(own, c->slot[s], c->shard_bytes, kNcclUint8, c->comm, c->ms);
+    void* gcomm = c->gather_comm ? c->gather_comm : c->comm;
+    if (!gcomm) return fail(ASYNCEP_ERR_NCCL, "no NCCL communicator (use asyncep_prefetch_layer_local)");
+    const int r = c->nccl.allgather(own, c->slot[s], c->shard_bytes, kNcclUint8, gcomm, c->ms);
     if (r != 0)
       return fail(ASYNCEP_ERR_NCCL, "ncclAllGather: %s", c->nccl.errstr ? c->nccl.errstr(r) : "error");
   }
@@ -671,13 +677,21 @@ asyncep_status asyncep_set_gather_transport(asyncep_ctx* c, int32_t transport, i
   if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
   if (transport < -1 || transport > ASYNCEP_GATHER_NCCL)
     return fail(ASYNCEP_ERR_INVALID_ARG, "unknown gather transport %d", transport);
-  if (transport == ASYNCEP_GATHER_NCCL && !c->comm)
+  if (transport == ASYNCEP_GATHER_NCCL && !c->comm && !c->gather_comm)
     return fail(ASYNCEP_ERR_NCCL, "NCCL transport without a communicator");
   if (reserve_sms < 0 || reserve_sms >= c->dev_sms - 2)
     return fail(ASYNCEP_ERR_INVALID_ARG, "reserve_sms %d out of range", reserve_sms);
   c->transport = transport;
   if (transport == ASYNCEP_GATHER_COPY_KERNEL || transport == ASYNCEP_GATHER_COPY_ENGINE) c->copy_mode = transport;
   c->num_sms = c->dev_sms - (reserve_sms & ~1);  // the grouped GEMMs' persistent grid (CTA pairs)
+  return ASYNCEP_OK;
+}
+
+asyncep_status asyncep_set_gather_comm(asyncep_ctx* c, void* nccl_comm) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  if (nccl_comm && !c->nccl.allgather && !resolve_nccl(c->nccl))
+    return fail(ASYNCEP_ERR_NCCL, "ncclAllGather not found in the process");
+  c->gather_comm = nccl_comm;
   return ASYNCEP_OK;
 }
 

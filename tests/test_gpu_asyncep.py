@@ -195,7 +195,11 @@ def test_nccl_allgather_path_with_borrowed_torch_comm():
         assert torch.equal(st.slots[1][:half], st.shards[1])
         assert torch.equal(st.slots[1][:half], full.shards[1][:half])
         assert torch.all(st.slots[1][half:] == 0xAB)  # the absent rank's half is untouched
-        # the explicit NCCL transport with SMs reserved for NCCL's kernels, and the startup probe
+        # the explicit NCCL transport with SMs reserved for NCCL's kernels, on a dedicated gather
+        # communicator whose NCCL config caps its kernels at those SMs, and the startup probe
+        _g, gcomm = A.nccl_gather_group(16)
+        assert gcomm and gcomm != comm
+        A.asyncep_set_gather_comm(st.ctx, gcomm)
         A.asyncep_set_gather_transport(st.ctx, A.GATHER_NCCL, 16)
         st.slots[0].fill_(0xCD)
         ms, nbytes = A.asyncep_probe_gather(st.ctx, 2)
