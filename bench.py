@@ -736,6 +736,13 @@ def main():
         v = n_tok * n_samp / dt / L_
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": orc.threads, "kind": "oracle",
                                 "sample": f"{n_samp} x " + runs[0][2] + f"; {dt:.1f} s of CPU work"}
+        # also a one-thread figure (512 tokens: one full 32-row block per expert)
+        import oracle
+        oracle.set_num_threads(1)
+        v1, dt1, _ = orc.run(512, sample=99)
+        oracle.set_num_threads(orc.threads)
+        line["cpu_baseline"]["single_thread"] = {"value": v1, "unit": "tokens/s", "cores": 1,
+                                                 "sample": f"512 tokens, 1 thread, {dt1:.1f} s"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
