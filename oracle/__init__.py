@@ -61,6 +61,8 @@ def _load():
             lib.oracle_e4m3_decode_array.restype = None
             lib.oracle_to_bf16_array.argtypes = [P, I64, P]
             lib.oracle_to_bf16_array.restype = None
+            lib.oracle_quant_row_mx.argtypes = [P, I32, P]
+            lib.oracle_quant_row_mx.restype = None
             lib.oracle_eq1_threshold.argtypes = [D, D, D]
             lib.oracle_eq1_threshold.restype = D
             lib.oracle_saturation_T.argtypes = [I32, I32, I32, I32, D, I32, D, D, D, P, P]
@@ -126,12 +128,13 @@ def router(x, wr, k: int, norm_topk: bool = True, ids_in=None):
 
 
 def moe_layer(x, wr, wg, wu, wd, k: int, norm_topk: bool = True, residual: bool = True,
-              identity_experts: bool = False, ids_in=None, act_quant: bool = False):
+              identity_experts: bool = False, ids_in=None, act_quant=False):
     """One MoE FFN layer by definition (R1-R5, R9, R15).
 
     x [T,H]; wr [E,H]; wg, wu [E,h,H]; wd [E,H,h] (natural layout, fp32 holding exact
     bf16/e4m3-dequantised values).  act_quant emulates the FP8 path's activation
-    quantisation (R6: per-token e4m3 x, bf16 then per-row e4m3 intermediate).
+    quantisation (R6: per-token e4m3 x, bf16 then per-row e4m3 intermediate); act_quant="mx"
+    the MX variant (R6b: per-token e4m3 x, bf16 then 1x32 blocks with E8M0 scales).
     Returns dict(y [T,H] f64, ids, w, logits, gap).
     """
     x, wr = _f32(x), _f32(wr)
@@ -154,7 +157,7 @@ def moe_layer(x, wr, wg, wu, wd, k: int, norm_topk: bool = True, residual: bool 
         ids_in = np.ascontiguousarray(ids_in, dtype=np.int32)
     rc = _load().oracle_moe_layer(_ptr(x), _ptr(wr), wg_p, wu_p, wd_p, T, H, E, k, h,
                                   int(norm_topk), int(residual), int(identity_experts),
-                                  int(act_quant), _ptr(ids_in), _ptr(y), _ptr(ids), _ptr(w), _ptr(logits), _ptr(gap))
+                                  2 if act_quant == "mx" else int(bool(act_quant)), _ptr(ids_in), _ptr(y), _ptr(ids), _ptr(w), _ptr(logits), _ptr(gap))
     if rc:
         raise ValueError(f"oracle_moe_layer rc={rc}")
     return dict(y=y, ids=ids, w=w, logits=logits, gap=gap)
@@ -174,6 +177,15 @@ def to_bf16(v) -> np.ndarray:
     v = np.ascontiguousarray(v, dtype=np.float64)
     out = np.empty(v.shape, np.float32)
     _load().oracle_to_bf16_array(_ptr(v), v.size, _ptr(out))
+    return out
+
+
+def quant_row_mx(v) -> np.ndarray:
+    """The MX intermediate rule (R6b) over one row (length a multiple of 32), fp64 result."""
+    v = _f32(v).ravel()
+    assert v.size % 32 == 0
+    out = np.empty(v.shape, np.float64)
+    _load().oracle_quant_row_mx(_ptr(v), v.size, _ptr(out))
     return out
 
 

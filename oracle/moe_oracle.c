@@ -160,6 +160,7 @@ int oracle_router(const float *x, const float *wr, int64_t T, int H, int E, int 
  */
 #define NB 32
 static void quant_row_e4m3(const float *v, int n, double *out);
+static void quant_row_mx(const float *v, int n, double *out);
 static float to_bf16(double v);
 
 static void expert_block(const float *wg, const float *wu, const float *wd, int H, int h, int nb,
@@ -180,12 +181,14 @@ static void expert_block(const float *wg, const float *wu, const float *wd, int 
         }
         for (int b = 0; b < NB; ++b) at[(size_t)r * NB + b] = silu(g[b]) * u[b];
     }
-    if (act_quant) {  /* emulate the GPU: intermediate -> bf16 -> per-row e4m3 (R5, R6) */
+    if (act_quant) {  /* emulate the GPU: intermediate -> bf16 -> per-row e4m3 (R5, R6), or
+                         act_quant == 2: -> bf16 -> MX 1x32 blocks with E8M0 scales (R6b) */
         float *row = (float *)malloc(sizeof(float) * (size_t)h);
         double *dq = (double *)malloc(sizeof(double) * (size_t)h);
         for (int b = 0; b < nb; ++b) {
             for (int r = 0; r < h; ++r) row[r] = to_bf16(at[(size_t)r * NB + b]);
-            quant_row_e4m3(row, h, dq);
+            if (act_quant == 2) quant_row_mx(row, h, dq);
+            else quant_row_e4m3(row, h, dq);
             for (int r = 0; r < h; ++r) at[(size_t)r * NB + b] = dq[r];
         }
         free(row); free(dq);
@@ -412,6 +415,29 @@ static void quant_row_e4m3(const float *v, int n, double *out) {
         out[i] = oracle_e4m3_decode(oracle_e4m3_encode_fast((double)p)) * (double)sc;
     }
 }
+
+/*
+ * MX intermediate quantisation (reading R6b, S3; OCP MX layout: blocks of 32
+ * consecutive elements along the contraction, one power-of-two E8M0 scale per block):
+ *   per block of 32:  amax = max |v_i| (the bf16 values, exact);
+ *                     e = the smallest integer with amax <= 448 * 2^e, clamped to [-127, 127];
+ *                     result_i = decode(RNE_satfinite_e4m3(v_i / 2^e)) * 2^e.
+ * (The smallest such e maps the block's amax into (224, 448]: no element saturates.)
+ * n must be a multiple of 32 (the FFN width is a multiple of 128).
+ */
+static void quant_row_mx(const float *v, int n, double *out) {
+    for (int b0 = 0; b0 < n; b0 += 32) {
+        double amax = 0.0;
+        for (int i = b0; i < b0 + 32 && i < n; ++i) { const double a = fabs((double)v[i]); if (a > amax) amax = a; }
+        int e = -127;
+        while (e < 127 && amax > ldexp(448.0, e)) ++e;
+        for (int i = b0; i < b0 + 32 && i < n; ++i)
+            out[i] = ldexp(oracle_e4m3_decode(oracle_e4m3_encode_fast(ldexp((double)v[i], -e))), e);
+    }
+}
+
+/* Exported for the pins: the MX rule over one row of n values (n a multiple of 32). */
+void oracle_quant_row_mx(const float *v, int n, double *out) { quant_row_mx(v, n, out); }
 
 /* ---------------- Saturation threshold, Eq. 1 ---------------- */
 

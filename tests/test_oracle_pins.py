@@ -369,3 +369,90 @@ def test_act_quant_full_expert_path(E, k):
     # the order matters: quantising before the bf16 rounding (or skipping it) gives another answer
     plain = oracle.moe_layer(x, wr, wg, wu, wd, k, residual=False, act_quant=False)["y"]
     assert np.abs(plain - r["y"]).max() > 1e-4 * np.abs(plain).max()
+
+
+# ------------------------------------------------------------------ MX intermediate (R6b)
+
+def _mx_block_brute(v32):
+    """R6b by brute force: e = the smallest integer in [-127, 127] with amax <= 448 * 2^e found by
+    scanning every candidate, each element encoded by the nearest-code search, decoded, rescaled."""
+    v = [float(a) for a in np.asarray(v32, np.float32)]
+    amax = max(abs(a) for a in v)
+    e = next((c for c in range(-127, 128) if amax <= math.ldexp(448.0, c)), 127)
+    return np.array([math.ldexp(oracle.e4m3_decode_one(oracle.e4m3_encode_one(math.ldexp(a, -e))), e) for a in v]), e
+
+
+def _q_mx(row):
+    row = np.asarray(row, np.float32)
+    return np.concatenate([_mx_block_brute(row[b:b + 32])[0] for b in range(0, row.size, 32)])
+
+
+def test_mx_block_rule_against_brute_force():
+    """The MX rule (R6b, S3) against the brute-force scale search and nearest-code encoder,
+    on blocks spanning 60 decades, all-zero blocks, blocks whose amax sits exactly on 448 * 2^j
+    (scale 2^j) or one bf16 ulp above it (2^(j+1)), mixed tiny/large blocks and the clamp at 2^-127."""
+    rng = np.random.default_rng(21)
+    blocks = []
+    for d in range(-30, 31, 3):
+        blocks.append(_rand((32,), 10.0 ** d, 100 + d))
+    blocks.append(np.zeros(32, np.float32))
+    for j in (-20, -3, 0, 5, 30):
+        b = _rand((32,), 1.0, 200 + j) * np.float32(2.0 ** j)
+        b[7] = np.float32(448.0 * 2.0 ** j)
+        blocks.append(b)
+        c = b.copy()
+        c[7:8] = (c[7:8].view(np.uint32) + np.uint32(0x10000)).view(np.float32)  # next bf16 above
+        blocks.append(c)
+    mix = _rand((32,), 1e-6, 300)
+    mix[0] = np.float32(1000.0)
+    blocks.append(mix)
+    blocks.append(np.full(32, np.float32(2.0 ** -133)))  # below 448 * 2^-127 / 2^... -> e clamps at -127
+    row = np.concatenate(blocks).astype(np.float32)
+    got = oracle.quant_row_mx(row)
+    want = np.concatenate([_mx_block_brute(row[b:b + 32])[0] for b in range(0, row.size, 32)])
+    assert np.array_equal(got, want)
+    # the scale each block took: exactly 2^j on the boundary, 2^(j+1) one ulp above it
+    for j in (-20, -3, 0, 5, 30):
+        b = _rand((32,), 1.0, 200 + j) * np.float32(2.0 ** j)
+        b[7] = np.float32(448.0 * 2.0 ** j)
+        assert _mx_block_brute(b)[1] == j
+        assert oracle.quant_row_mx(b)[7] == 448.0 * 2.0 ** j   # the amax element is exact
+        b[7:8] = (b[7:8].view(np.uint32) + np.uint32(0x10000)).view(np.float32)
+        assert _mx_block_brute(b)[1] == j + 1
+    assert _mx_block_brute(np.full(32, np.float32(2.0 ** -133)))[1] == -127
+    # invariants: no element saturates; every block's largest code lies in (224, 448] * 2^e
+    for b0 in range(0, row.size, 32):
+        q, e = _mx_block_brute(row[b0:b0 + 32])
+        if np.abs(row[b0:b0 + 32]).max() > math.ldexp(448.0, -127):
+            assert 224.0 * 2.0 ** e <= np.abs(q).max() <= 448.0 * 2.0 ** e
+    # e4m3-representable values times a power of two come back exactly
+    codes = np.array([oracle.e4m3_decode_one(c) for c in range(0, 0x7F)], np.float64)
+    exact = (rng.choice(codes, 64) * rng.choice([-1, 1], 64) * 2.0 ** 7).astype(np.float32)
+    exact[3] = 448.0 * 2.0 ** 7
+    exact[40] = -448.0 * 2.0 ** 7
+    assert np.array_equal(oracle.quant_row_mx(exact), exact.astype(np.float64))
+
+
+@pytest.mark.parametrize("E,k", [(1, 1), (4, 2)])
+def test_act_quant_mx_full_expert_path(E, k):
+    """act_quant="mx" with real experts: per token, x -> per-token e4m3 (R6), g/u by numpy matmul,
+    silu(g)*u -> bf16 (nearest-neighbour rule) -> MX blocks of 32 (brute force), W_down, weighted sum
+    with the oracle's routing weights.  E=1, k=1 is one dense FP8-emulated SwiGLU FFN."""
+    T, H, h = 16, 64, 96
+    x, wr, wg, wu, wd = _layer(T=T, H=H, E=E, k=k, h=h, seed=9)
+    r = oracle.moe_layer(x, wr, wg, wu, wd, k, residual=False, act_quant="mx")
+    for t in range(T):
+        xq = _q_row(x[t])
+        y = np.zeros(H)
+        for j in range(k):
+            e = int(r["ids"][t, j])
+            g = wg[e].astype(np.float64) @ xq
+            u = wu[e].astype(np.float64) @ xq
+            a = g / (1.0 + np.exp(-g)) * u
+            ab = np.array([_bf16_nearest(v) for v in a], np.float32)
+            y += r["w"][t, j] * (wd[e].astype(np.float64) @ _q_mx(ab))
+        np.testing.assert_allclose(r["y"][t], y, rtol=1e-12, atol=1e-12 * np.abs(y).max())
+    # a different rule from the per-row one (R6), and both close to the unquantised intermediate
+    row = oracle.moe_layer(x, wr, wg, wu, wd, k, residual=False, act_quant=True)["y"]
+    assert np.abs(row - r["y"]).max() > 1e-6 * np.abs(row).max()
+    assert np.abs(row - r["y"]).max() < 0.1 * np.abs(row).max()
