@@ -69,6 +69,12 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
                                                FP8 gate/up GEMM; S6)                     */
 #define ASYNCEP_FLAG_SWAP_TAILS      0x80 /* swap-AB tail tiles (<= 240 rows) in both GEMMs and both
                                                dtypes (A/B and tests)                               */
+#define ASYNCEP_FLAG_MX_ACT         0x100 /* FP8 experts: the intermediate is quantised MX-style (e4m3,
+                                               one E8M0 power-of-two scale per 32 columns, DESIGN.md
+                                               R6b) inside the gate/up GEMM's epilogue and the down
+                                               GEMM runs block-scaled MMAs (kind::mxf8f6f4); no
+                                               separate quantisation pass.  Default: per-row scales
+                                               (R6).  Requires expert_dtype == ASYNCEP_FP8_E4M3.     */
 
 typedef struct {
   int32_t num_layers;      /* L                                                         */

@@ -162,7 +162,7 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 struct WsLayout {
   size_t ids, w, dest, src_tok, blk, offsets, tile_start, counts, done, sched, xperm, act, total;
-  size_t xq, xscale, amax, aq, ascale;  // FP8 experts only
+  size_t xq, xscale, amax, aq, ascale, asf;  // FP8 experts only (asf: MX scale chunks)
 };
 WsLayout ws_layout(const asyncep_config& c) {
   WsLayout L{};
@@ -194,6 +194,7 @@ WsLayout ws_layout(const asyncep_config& c) {
     L.amax = take(Rp * 4);
     L.aq = take(Rp * (size_t)c.ffn);
     L.ascale = take(Rp * 4);
+    L.asf = take(Rp * (size_t)c.ffn / 32);  // one E8M0 byte per 32 intermediate values
   }
   L.total = o;
   return L;
@@ -212,6 +213,8 @@ asyncep_status check_config(const asyncep_config* c) {
   if (c->ffn <= 0 || c->ffn % 128) return fail(ASYNCEP_ERR_INVALID_ARG, "ffn must be a multiple of 128");
   if (c->expert_dtype != ASYNCEP_BF16 && c->expert_dtype != ASYNCEP_FP8_E4M3)
     return fail(ASYNCEP_ERR_UNSUPPORTED, "expert_dtype %d not supported by this build", c->expert_dtype);
+  if ((c->flags & ASYNCEP_FLAG_MX_ACT) && c->expert_dtype != ASYNCEP_FP8_E4M3)
+    return fail(ASYNCEP_ERR_INVALID_ARG, "ASYNCEP_FLAG_MX_ACT needs FP8 experts");
   if (c->expert_dtype == ASYNCEP_FP8_E4M3 && (c->flags & ASYNCEP_FLAG_SIMT_GEMM))
     return fail(ASYNCEP_ERR_UNSUPPORTED, "the SIMT reference GEMM is BF16 only");
   if (c->expert_dtype == ASYNCEP_FP8_E4M3 && c->hidden < 256)
@@ -480,7 +483,8 @@ asyncep_status asyncep_init(const asyncep_config* cfg, void* nccl_comm, void* co
   // TMA descriptors: activations (fixed workspace addresses), each resident layer, both slots.
   const int64_t R = aep::perm_rows(cfg->max_tokens, cfg->top_k, cfg->num_experts);
   if (!aep::make_act_maps(c->act_maps, (const bf16*)(c->ws + c->L.xperm), (const bf16*)(c->ws + c->L.act), R,
-                          cfg->hidden, cfg->ffn, fp8 ? c->ws + c->L.xq : nullptr, fp8 ? c->ws + c->L.aq : nullptr))
+                          cfg->hidden, cfg->ffn, fp8 ? c->ws + c->L.xq : nullptr, fp8 ? c->ws + c->L.aq : nullptr,
+                          fp8 ? (const uint32_t*)(c->ws + c->L.asf) : nullptr))
     return bail(fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
   c->layer_maps.resize(L);
   c->resident.assign(L, 0);
@@ -834,6 +838,8 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     f8.expert_bytes = c->expert_bytes;
     f8.sgu_off = (size_t)3 * H * h;
     f8.sd_off = f8.sgu_off + (size_t)2 * h * 4;
+    f8.mx = (cf.flags & ASYNCEP_FLAG_MX_ACT) != 0;
+    f8.act_sf = (uint32_t*)(ws + c->L.asf);
     aep::launch_perm_quant((const bf16*)x, gather_a ? nullptr : dest, T, H, k, ws + c->L.xq,
                            (float*)(ws + c->L.xscale), st);
     c->launches += 1;
@@ -876,10 +882,13 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     // stage boundary before the intermediate's quantisation: the GEMM1 stage is the GEMM1 kernel
     // alone (the roofline's dominant kernel); act_quant is timed with GEMM2, whose A operand it makes
     if (timing) CUDA_TRY(cudaEventRecord(ev[4], st));
-    aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
-                          (float*)(ws + c->L.ascale), st);
+    if (!f8.mx) {  // MX: GEMM1 already wrote the e4m3 intermediate and its block scales
+      aep::launch_act_quant(act, f8.act_amax, offsets, E, aep::perm_rows(T, k, E), h, ws + c->L.aq,
+                            (float*)(ws + c->L.ascale), st);
+      c->launches += 1;
+    }
     aep::launch_gemm2_tc(g, c->act_maps, wm, H, h, yperm, c->num_sms, st, &f8, own);
-    c->launches += 3;
+    c->launches += 2;
   } else {
     aep::launch_gemm1_tc(g, c->act_maps, wm, H, h, act, gather_a ? x : nullptr, T, src_tok, c->num_sms, st, nullptr,
                          own);

@@ -319,6 +319,31 @@ AEP_DEV void mma_bf16_2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_
       : "memory");
 }
 
+// Block-scaled FP8 (MX): D (+)= (A . sfa) * (B . sfb)^T with E8M0 scale factors in TMEM, one per 32
+// elements of K; the instruction descriptor's sf-id bits pick the k-step's byte of each 4-byte group.
+AEP_DEV void mma_mx_2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sfa_tmem,
+                      uint32_t sfb_tmem, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(sfa_tmem), "r"(sfb_tmem), "r"(accum)
+      : "memory");
+}
+// smem -> TMEM copy of one 512-B scale-factor chunk (128 rows x 4 bytes; row m at byte
+// (m % 32) * 16 + (m / 32) * 4) into 4 TMEM columns of each CTA of the pair (issued by the leader;
+// each CTA copies from its own shared memory at the same address).  Ordered with the MMAs.
+AEP_DEV void tc_cp_sf_2(uint32_t tmem, uint32_t saddr) {
+  const uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+  asm volatile("tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;" ::"r"(tmem), "l"(d) : "memory");
+}
+// Instruction descriptor of kind::mxf8f6f4.block_scale: E4M3 A and B (formats 0), K-major,
+// [4,6) B scale-factor id, [17,23) N >> 3, [23] scale format E8M0, [24,29) M >> 4, [29,31) A sf id.
+__host__ __device__ constexpr uint32_t make_idesc_mx(int M, int N, int sf_id) {
+  return ((uint32_t)sf_id << 4) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24) |
+         ((uint32_t)sf_id << 29);
+}
+
 // tcgen05.commit: the mbarrier gets one arrive when all prior MMAs of this thread finish.
 AEP_DEV void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(

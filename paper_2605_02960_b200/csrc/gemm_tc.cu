@@ -67,7 +67,9 @@ enum { EPI_PLAIN = 0, EPI_SWIGLU = 1, EPI_ROUTER = 2, EPI_ROUTER16 = 3 };  // ro
 // Shared memory plan per (CTA group, epilogue mode): S-stage operand ring, one 32-row staging
 // buffer and one 256-scale buffer per epilogue warp, barriers, the tile_start prefix.
 // (Measured and dropped, S6: double-buffered staging, 8 epilogue warps.)
-template <int NCTA, int MODE>
+// MX block-scaled GEMM2 (MXIN): per stage one 512-B chunk of A scale factors (E8M0, the
+// tcgen05.cp 32x128b.warpx4 layout), plus one constant 512-B chunk of B scale factors (1.0).
+template <int NCTA, int MODE, bool MXIN = false>
 struct Cfg {
   static constexpr int B_BYTES_MAX = (256 / NCTA) * BK * 2;  // B rows per CTA <= 256 / NCTA
   static constexpr int STAGES = NCTA == 2 ? 6 : 4;
@@ -75,10 +77,16 @@ struct Cfg {
   static constexpr int NTHR = 128 + 32 * EW;  // warps 0-3 roles, then EW epilogue warps
   static constexpr int NSTG = 1;
   static constexpr int NSCL = SCL_BYTES;
-  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + EW * NSTG * STG_BYTES +
+  static constexpr int SF_BYTES = MXIN ? (STAGES * 512 + 512 + 1023) / 1024 * 1024 : 0;
+  static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_BYTES + B_BYTES_MAX) + SF_BYTES + EW * NSTG * STG_BYTES +
                                  EW * NSCL + 512 + (2 * kMaxExperts + 1) * sizeof(int32_t);
   static_assert(SMEM <= 232448, "shared memory budget");
 };
+// MX GEMM2 TMEM columns: accumulator 0 [0, 256) for 256-wide N tiles, accumulator 1 [256, 480) for
+// 224-wide ones, the B scale factors [480, 488), four A scale-factor slots [488, 504).
+constexpr int kMxSfbCol = 480;
+constexpr int kMxSfaCol = 488;
+constexpr int kMxWide = 256, kMxNarrow = 224, kMxPeriod = kMxWide + kMxNarrow;
 
 struct TcArgs {
   const int32_t* tile_start;  // grouped mode: [E+1] prefix of row tiles (rows padded to 128*NCTA)
@@ -98,6 +106,10 @@ struct TcArgs {
   size_t expert_bytes;
   uint32_t* amax_out;           // GEMM1 FP8: per-row max |act| (fp32 bits, atomicMax)
   int* sched;                   // dynamic tile counter (zeroed before the launch)
+  int n_tiles2;                 // MX GEMM2: 224-wide N tiles per row tile (n_tiles: 256-wide ones)
+  uint32_t* mx_sf_out;          // MX GEMM1: E8M0 scale chunks of the e4m3 intermediate
+  int mx_nkb;                   // MX: 128-column k-blocks of the intermediate (h / 128)
+  int mx_sf_warp;               // MXIN: the warp issuing the scale-chunk loads (0: with A, 2: its own)
   int group_mod;                // > 0: B expert = group % group_mod (EP contrast: groups are
                                 // (source rank, local expert) pairs over a shard of group_mod experts)
   // fused dispatch: non-null gather_rows = A rows are gathered by warps 2-3 (cp.async) from the
@@ -153,6 +165,31 @@ __device__ __forceinline__ int swap_ntok(const int32_t* s_ts, const int32_t* s_c
   if (swap_max <= 0 || mt != s_ts[e + 1] - 1) return 0;
   const int r = s_cnt[e] - (mt - s_ts[e]) * TM;
   return (r > 0 && r <= swap_max) ? (r + 15) & ~15 : 0;
+}
+
+// MX GEMM2 tile geometry.  The output columns are covered by alternating 256- and 224-wide N
+// tiles (period 480; the last ones clipped to n_out), so the two accumulators (256 + 224 TMEM
+// columns) leave room for the scale factors.  Tile ids [0, totalW) are the 256-wide tiles
+// (n_wide per row tile), [totalW, total) the 224-wide ones (n_narrow per row tile); each width
+// class always uses its own accumulator (buf).
+struct TileGeo {
+  int mt, col0, width, buf;
+};
+__device__ __forceinline__ TileGeo tile_geo_mx(int t, int totalW, int n_wide, int n_narrow, int n_out) {
+  TileGeo g;
+  if (t < totalW) {
+    g.mt = t / n_wide;
+    g.col0 = (t - g.mt * n_wide) * kMxPeriod;
+    g.width = min(kMxWide, n_out - g.col0);
+    g.buf = 0;
+  } else {
+    const int u = t - totalW;
+    g.mt = u / n_narrow;
+    g.col0 = (u - g.mt * n_narrow) * kMxPeriod + kMxWide;
+    g.width = min(kMxNarrow, n_out - g.col0);
+    g.buf = 1;
+  }
+  return g;
 }
 
 // Router epilogue, one thread = one token row of the logits tile (E <= 256 fp32 columns
@@ -256,6 +293,28 @@ __device__ __forceinline__ void stage_and_store(const uint32_t (&o)[32], uint8_t
   }
 }
 
+// MX quantisation of one block of 32 intermediate values (reading R6b), 16 packed bf16 words in
+// column order -> 8 words of e4m3 codes (q), returns the E8M0 scale byte.  e is the smallest
+// integer with amax <= 448 * 2^e: amax = 1.m * 2^E gives e = E - 8, plus 1 when 1.m > 1.75
+// (448 = 1.75 * 2^8); the clamp at -127 is the E8M0 range (finite bf16 values give e <= 120).
+// The codes are RNE(v * 2^-e) (an exact power-of-two product), never saturated.
+__device__ __forceinline__ uint32_t mx_block(const uint32_t* o, uint32_t* q) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m = __vmaxu2(m, o[i] & 0x7fff7fffu);
+  const uint32_t a = max(m & 0xffffu, m >> 16) << 16;  // fp32 bits of the block's max |v|
+  const int e = max((int)(a >> 23) - 135 + ((a & 0x7fffffu) > 0x600000u ? 1 : 0), -127);
+  const float inv = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float x0, x1, x2, x3;
+    mul2(x0, x1, bf16_lo(o[2 * i]), bf16_hi(o[2 * i]), inv, inv);
+    mul2(x2, x3, bf16_lo(o[2 * i + 1]), bf16_hi(o[2 * i + 1]), inv, inv);
+    q[i] = (uint32_t)e4m3x2(x0, x1) | ((uint32_t)e4m3x2(x2, x3) << 16);
+  }
+  return (uint32_t)(e + 127);
+}
+
 // Dynamic tile scheduler.  The leader CTA's producer thread takes the next tile id from a
 // global atomic counter (so the tiles in flight on the whole GPU always form one contiguous
 // window: no drift between persistent CTAs, which kept L2 reuse of the A row-tiles and the
@@ -270,12 +329,35 @@ struct TileRing {
 };
 
 // scheduler side (leader producer thread): fetch + publish the id of tile number seq
+// MX GEMM2 (MxSched::nw > 0): the counter hands out units (row tile, j) in row-tile-major
+// order; a unit is the 256-wide tile j followed by its 224-wide sibling (when j < nn), published
+// back to back, so a pair's consecutive tiles alternate accumulators (except after a unit without
+// a sibling) and the wide and narrow tiles of a row tile are read at the same time (L2).
+struct MxSched {
+  int nw = 0, nn = 0, totalW = 0, total = 0;
+  int pending = -1;  // the narrow sibling still to publish
+  int units = 0;     // units taken (static schedule)
+};
 template <int NCTA>
-__device__ __forceinline__ int sched_publish(const TileRing& r, int* sched, int seq, int unit, int nunits) {
+__device__ __forceinline__ int sched_publish(const TileRing& r, int* sched, int seq, int unit, int nunits,
+                                             MxSched* mx = nullptr) {
   const int slot = seq % RING;
   const uint32_t ph = (uint32_t)(seq / RING) & 1u;
   mbar_wait(&r.sempty[slot], ph ^ 1u);
-  const int t = sched ? atomicAdd(sched, 1) : unit + seq * nunits;
+  int t;
+  if (mx && mx->pending >= 0) {
+    t = mx->pending;
+    mx->pending = -1;
+  } else {
+    if (mx) {  // unit u = the wide tile of the same id (ids run row-tile-major in both classes)
+      t = sched ? atomicAdd(sched, 1) : unit + (mx->units++) * nunits;
+      const int mt = t / mx->nw, j = t - mt * mx->nw;
+      if (t >= mx->totalW) t = mx->total;
+      else if (j < mx->nn) mx->pending = mx->totalW + mt * mx->nn + j;
+    } else {
+      t = sched ? atomicAdd(sched, 1) : unit + seq * nunits;
+    }
+  }
   r.ring[slot] = t;
   mbar_arrive(&r.sfull[slot]);
   if (NCTA == 2) st_async_u32(&r.ring[slot], &r.sfull[slot], 1, (uint32_t)t);
@@ -310,18 +392,25 @@ __device__ __forceinline__ const float* stage_scales(float* dst, const float* sr
 // copy CTAs (128 threads x 32 registers) co-reside with it and the next layer's gather makes
 // progress during the GEMM (without the cap the FP8 SwiGLU kernel took 250 registers/thread,
 // the whole register file, and the gather stalled for its entire duration).
-template <int MODE, int NCTA, bool F8>
+// MX (FP8 experts, MX intermediate, reading R6b): with MODE == EPI_SWIGLU (MXOUT) the GEMM1
+// epilogue writes the intermediate as e4m3 with one E8M0 scale per 32 columns (map_out = the
+// e4m3 act map, p.mx_sf_out the scale chunks); with MODE == EPI_PLAIN (MXIN) GEMM2 runs
+// kind::mxf8f6f4.block_scale MMAs on it (map_sf: the A scale chunks) over 256/224-wide N tiles.
+template <int MODE, int NCTA, bool F8, bool MX = false>
 __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCTA, MODE>::NTHR == 256 ? 224 : 168))
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_out, const __grid_constant__ CUtensorMap map_b2,
-                   const TcArgs p) {
-  using C = Cfg<NCTA, MODE>;
+                   const __grid_constant__ CUtensorMap map_sf, const TcArgs p) {
+  constexpr bool MXIN = MX && MODE == EPI_PLAIN && F8 && NCTA == 2;
+  constexpr bool MXOUT = MX && MODE == EPI_SWIGLU && F8 && NCTA == 2;
+  using C = Cfg<NCTA, MODE, MXIN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + STAGES * A_BYTES;
-  uint8_t* sStg = sB + STAGES * C::B_BYTES_MAX;
+  uint8_t* sSF = sB + STAGES * C::B_BYTES_MAX;  // MXIN: STAGES A scale chunks, then the B chunk
+  uint8_t* sStg = sSF + C::SF_BYTES;
   float* sScl = reinterpret_cast<float*>(sStg + C::EW * C::NSTG * STG_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(sStg + C::EW * C::NSTG * STG_BYTES + C::EW * C::NSCL);
   uint64_t* empty = full + STAGES;
@@ -356,6 +445,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   const int swap_max = (NCTA == 2 && (MODE == EPI_SWIGLU || MODE == EPI_PLAIN) && p.dense_rows <= 0 &&
                         p.BN == 256 && p.group_mod == 0) ? p.swap_max : 0;
   const bool gather = p.gather_rows != nullptr;
+  const bool sf_w2 = MXIN && !gather && p.mx_sf_warp == 2;  // warp 2 is a third producer (scales)
   if (warp == 0 && lane == 0) {
     if (!gather) tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
@@ -363,7 +453,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     if (MODE == EPI_PLAIN || MODE == EPI_SWIGLU) tma_prefetch_desc(&map_out);
     for (int s = 0; s < STAGES; ++s) {
       // leader: own expect_tx arrive + peer producer's arrive (+ peer's gathered-A forward)
-      mbar_init(&full[s], (PROD2 && !gather ? 2 : 1) * NCTA + (gather && NCTA == 2 ? 1 : 0));
+      mbar_init(&full[s], (PROD2 && !gather ? 2 : 1) * NCTA + (gather && NCTA == 2 ? 1 : 0) + (sf_w2 ? NCTA : 0));
       mbar_init(&empty[s], 1);
       mbar_init(&afull[s], 64);  // one .noinc cp.async arrival per gather thread
     }
@@ -376,7 +466,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       // consumers of a tile id: leader {MMA thread, 4 epilogue warps} + peer {producer, 4 epilogue
       // warps}; fused dispatch adds the 2 gather warps of each CTA and the peer's forwarder
       mbar_init(&sempty[r], (1 + C::EW) * NCTA + (gather ? 2 * NCTA + (NCTA == 2 ? 1 : 0) : 0) +
-                                (PROD2 && !gather ? NCTA : 0));
+                                (PROD2 && !gather ? NCTA : 0) + (sf_w2 ? NCTA : 0));
     }
     fence_barrier_init();
   }
@@ -384,25 +474,35 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     if (NCTA == 2) tmem_alloc2(tmem_slot, TMEM_COLS);
     else tmem_alloc(tmem_slot, TMEM_COLS);
   }
+  if (MXIN) {  // B scale factors: E8M0 1.0 (0x7F) for every row and k (the weights keep their
+               // per-row fp32 scale, applied in the epilogue)
+    for (int i = threadIdx.x; i < 128; i += C::NTHR)
+      reinterpret_cast<uint32_t*>(sSF + STAGES * 512)[i] = 0x7F7F7F7Fu;
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   if (NCTA == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int total_rt = s_ts[G];
-  const int total = total_rt * p.n_tiles;
+  const int totalW = total_rt * p.n_tiles;  // MXIN: the 256-wide tiles come first
+  const int total = MXIN ? totalW + total_rt * p.n_tiles2 : totalW;
   constexpr int KB_ELEMS = F8 ? 128 : BK;  // elements per 128-B k-block row
   const int nkb = p.K / KB_ELEMS;
   const int bn_cta = p.BN / NCTA;  // B rows loaded by this CTA
   const TileRing ring{sfull, sempty, sring};
 
-  if (warp == 0 || (PROD2 && !gather && warp == 3)) {
+  if (warp == 0 || (PROD2 && !gather && warp == 3) || (sf_w2 && warp == 2)) {
     // Producer warp, lane 0: arms the stage barrier and loads B (and A unless it is gathered).
-    // PROD2 without the gather: warp 0 loads A (and runs the scheduler), warp 3 loads B.
+    // PROD2 without the gather: warp 0 loads A (and runs the scheduler), warp 3 loads B; MXIN:
+    // the A scale chunks with A, or from warp 2 (ASYNCEP_MX_SF_WARP=2).
     const bool do_a = !gather && (!PROD2 || warp == 0);
     const bool do_b = !PROD2 || gather || warp == 3;
+    const bool do_sf = MXIN && (sf_w2 ? warp == 2 : warp == 0);
     const bool sched_lead = warp == 0;
     if (lane == 0) {
-      const uint32_t tx = (uint32_t)NCTA * ((do_a ? (uint32_t)A_BYTES : 0u) + (do_b ? (uint32_t)bn_cta * BK * 2 : 0u));
+      const uint32_t tx = (uint32_t)NCTA * ((do_a ? (uint32_t)A_BYTES : 0u) + (do_sf ? 512u : 0u) +
+                                            (do_b ? (uint32_t)bn_cta * BK * 2 : 0u));
       const uint64_t pol_a = make_policy(p.pol_a), pol_b = make_policy(p.pol_b);
       int stage = 0;
       uint32_t phase = 0;
@@ -416,20 +516,33 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       // tile's row indices while they copy the current tile (in the peer CTA a gather warp is
       // then the consumer that arms the ring slot for the st.async; without the gather the peer
       // producer arms it -- a complete_tx that lands before the arm leaves the phase pending).
-      int t_next = (leader && sched_lead) ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits) : 0;
+      MxSched mxs;
+      mxs.nw = p.n_tiles;
+      mxs.nn = p.n_tiles2;
+      mxs.totalW = totalW;
+      mxs.total = total;
+      MxSched* const mxp = MXIN ? &mxs : nullptr;
+      int t_next = (leader && sched_lead) ? sched_publish<NCTA>(ring, p.sched, 0, unit, nunits, mxp) : 0;
       for (int seq = 0;; ++seq) {
         int t;
         if (!sched_lead) {
           WP_WAIT(wp_s, t = sched_consume<NCTA>(ring, seq, leader, false))
         } else if (leader) {
           t = t_next;
-          if (t < total) WP_WAIT(wp_s, t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits))
+          if (t < total) WP_WAIT(wp_s, t_next = sched_publish<NCTA>(ring, p.sched, seq + 1, unit, nunits, mxp))
         } else {
           WP_WAIT(wp_s, t = sched_consume<NCTA>(ring, seq, false, !gather))
         }
         if (t >= total) break;
-        int mt, nt;
-        decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+        int mt, nt = 0, brow;
+        if (MXIN) {
+          const TileGeo g = tile_geo_mx(t, totalW, p.n_tiles, p.n_tiles2, p.n_out);
+          mt = g.mt;
+          brow = g.col0 + (int)rank * (g.width >> 1);  // B box: bn_cta rows (over-fetch on narrow tiles)
+        } else {
+          decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+          brow = nt * p.BN + (int)rank * bn_cta;
+        }
         int e = find_expert(s_ts, G, mt);
         const int ntok = swap_ntok(s_ts, s_cnt, e, mt, TM, swap_max);
         if (p.group_mod > 0) e %= p.group_mod;  // group (source rank, local expert) -> expert
@@ -438,7 +551,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         if (own_e) e -= p.own_lo;
         // swap: this CTA's ntok/2 token rows go to the B stage, its 128 weight rows to the A stage
         const int row0 = ntok ? mt * TM + (int)rank * (ntok >> 1) : mt * TM + (int)rank * BM;
-        const int brow = nt * p.BN + (int)rank * bn_cta;
         uint8_t* const dA = ntok ? sB : sA;  // token operand
         uint8_t* const dB = ntok ? sA : sB;  // weight operand
         for (int kb = 0; kb < nkb; ++kb) {
@@ -454,6 +566,8 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               if (p.pol_a == 3) tma_load_2d_pair(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0);
               else tma_load_2d_pair_hint(dA + stage * A_BYTES, &map_a, &full[stage], kb * KB_ELEMS, row0, pol_a);
             }
+            // the k-block's 512-B chunk of this CTA's 128 A rows' scale factors
+            if (do_sf) tma_load_2d_pair(sSF + stage * 512, &map_sf, &full[stage], 0, (mt * 2 + (int)rank) * p.mx_nkb + kb);
             if (do_b) tma_load_3d_pair(dB + stage * C::B_BYTES_MAX, mb, &full[stage], kb * KB_ELEMS, brow, e, pol_b);
           } else {
             mbar_arrive_expect_tx(&full[stage], tx);
@@ -576,24 +690,37 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       const uint64_t b_desc0 = make_smem_desc_sw128(smem_u32(sB));
       int stage = 0;
       uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
+      uint32_t uses0 = 0, uses1 = 0;  // tiles issued into accumulator 0 / 1 (barrier parity)
       WP_DECL(wp_f) WP_DECL(wp_a) WP_DECL(wp_t) WP_DECL(wp_s)
 #if GEMM_WAITPROF
       const long long wp_t0 = clock64();
 #endif
+      if (MXIN) {  // the constant B scale factors of both 128-row halves of an N tile
+        if (elect_one()) {
+          tc_cp_sf_2(tmem_base + kMxSfbCol, smem_u32(sSF + STAGES * 512));
+          tc_cp_sf_2(tmem_base + kMxSfbCol + 4, smem_u32(sSF + STAGES * 512));
+        }
+        __syncwarp();
+      }
       for (int seq = 0;; ++seq) {
         int t = 0;
         WP_WAIT(wp_s, if (lane == 0) t = sched_consume<NCTA>(ring, seq, true, false))
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= total) break;
         uint32_t id = idesc;
+        int acc = seq & 1;
+        if (MXIN) {
+          const TileGeo g = tile_geo_mx(t, totalW, p.n_tiles, p.n_tiles2, p.n_out);
+          acc = g.buf;
+          id = make_idesc_mx(TM, g.width, 0);
+        }
         if (swap_max > 0) {  // swap-AB tail: M = 256 weight rows, N = the tile's tokens
           int mt, nt;
           decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
           const int ntok = swap_ntok(s_ts, s_cnt, find_expert(s_ts, G, mt), mt, TM, swap_max);
           if (ntok) id = make_idesc(TM, ntok, !F8);
         }
+        const uint32_t acc_phase = (acc ? uses1 : uses0) & 1u;
         WP_WAIT(wp_t, mbar_wait(&tempty[acc], acc_phase ^ 1))
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * 256);
@@ -605,10 +732,17 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           const uint64_t ad = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
           const uint64_t bd = b_desc0 + (uint64_t)((stage * C::B_BYTES_MAX) >> 4);
           if (elect_one()) {
+            // MX: the k-block's A scale factors into one of 4 TMEM slots (tcgen05.cp and
+            // tcgen05.mma execute in issue order, so the slot's previous MMAs have read it)
+            const uint32_t sfa = tmem_base + kMxSfaCol + 4u * (uint32_t)(kb & 3);
+            if (MXIN) tc_cp_sf_2(sfa, smem_u32(sSF + stage * 512));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {  // 4 MMAs of 32 B of K (16 bf16 / 32 e4m3) per 128-B k-block
               const uint32_t acc_on = (kb | k) != 0 ? 1u : 0u;
-              if (F8) {
+              if (MXIN) {
+                mma_mx_2(d, ad + 2 * k, bd + 2 * k, id | ((uint32_t)k << 4) | ((uint32_t)k << 29), sfa,
+                         tmem_base + kMxSfbCol, acc_on);
+              } else if (F8) {
                 if (NCTA == 2) mma_f8_2(d, ad + 2 * k, bd + 2 * k, id, acc_on);
                 else mma_f8(d, ad + 2 * k, bd + 2 * k, id, acc_on);
               } else {
@@ -627,8 +761,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
           else tc_commit(&tfull[acc]);
         }
         __syncwarp();
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (acc) ++uses1; else ++uses0;
       }
 #if GEMM_WAITPROF
       if (lane == 0) printf("WPM %d %lld %lld %lld %lld %lld\n", (int)blockIdx.x, clock64() - wp_t0, wp_f, wp_a, wp_t, wp_s);
@@ -640,8 +773,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
     const int quad = warp & 3;         // TMEM lanes [32*quad, 32*quad+32): this warp's rows
     uint8_t* stg = sStg + ew * C::NSTG * STG_BYTES;
     uint32_t chunk = 0;  // stores issued by this warp (staging buffer parity)
-    int acc = 0;
-    uint32_t acc_phase = 0;
+    uint32_t uses0 = 0, uses1 = 0;  // tiles read out of accumulator 0 / 1 (barrier parity)
     WP_DECL(wp_f) WP_DECL(wp_s) WP_DECL(wp_store_acc)
 #if GEMM_WAITPROF
     const long long wp_t0 = clock64();
@@ -651,8 +783,18 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
       WP_WAIT(wp_s, if (lane == 0) t = sched_consume<NCTA>(ring, seq, leader, false))
       t = __shfl_sync(0xffffffffu, t, 0);
       if (t >= total) break;
-      int mt, nt;
-      decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+      int mt, nt = 0, acc = seq & 1, col0 = 0, width = 0;  // col0 / width: MXIN tile columns
+      if (MXIN) {
+        const TileGeo g = tile_geo_mx(t, totalW, p.n_tiles, p.n_tiles2, p.n_out);
+        mt = g.mt;
+        acc = g.buf;
+        col0 = g.col0;
+        width = g.width;
+      } else {
+        decode_tile(t, p.n_tiles, total_rt, p.raster, mt, nt);
+      }
+      const uint32_t acc_phase = (acc ? uses1 : uses0) & 1u;
+      if (acc) ++uses1; else ++uses0;
       const int wrow0 = mt * TM + (int)rank * BM + quad * 32;  // first row of this warp's slice
       WP_WAIT(wp_f, mbar_wait(&tfull[acc], acc_phase))
       tc_fence_after();
@@ -793,6 +935,11 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
                nt * 256;
           sb = stage_scales(sScl + ew * 256, sb, 256, lane);
         }
+        uint32_t sfw = 0;  // MXOUT: the row's 4 E8M0 scale bytes of this 128-column k-block
+        if (MXOUT) {
+          if (lane == 0) bulk_wait_read0();  // the warp's previous store has read the staging buffer
+          __syncwarp();
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < 128; c0 += 64) {  // act columns c0 .. c0+63 = packed groups c0/16 .. +3
           uint32_t o[32];
@@ -833,35 +980,83 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
                 mul2(a0, a1, silu_f(gv[2 * j]), silu_f(gv[2 * j + 1]), uv[2 * j], uv[2 * j + 1]);
                 const uint32_t pk = pack_bf16x2(a0, a1);
                 o[8 * grp + 2 * q + j] = pk;
-                if (F8) amax2 = __vmaxu2(amax2, pk & 0x7fff7fffu);
+                if (F8 && !MXOUT) amax2 = __vmaxu2(amax2, pk & 0x7fff7fffu);
               }
             }
           }
-          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * 128 + c0, wrow0
+          if (MXOUT) {
+            // two MX blocks (act columns c0 .. c0+31, c0+32 .. c0+63) -> 64 e4m3 bytes = 16-B chunks
+            // 4h .. 4h+3 (h = c0 / 64) of the row's 128-B line in the 128-B-swizzled staging buffer
+            uint32_t qa[8], qb[8];
+            const uint32_t ea = mx_block(o, qa), eb = mx_block(o + 16, qb);
+            const int hf = c0 >> 6;
+            sfw |= (ea | (eb << 8)) << (16 * hf);
+            const uint32_t base = smem_u32(stg) + lane * 128;
+            st_shared_v4(base + (((4 * hf + 0) ^ (lane & 7)) << 4), qa[0], qa[1], qa[2], qa[3]);
+            st_shared_v4(base + (((4 * hf + 1) ^ (lane & 7)) << 4), qa[4], qa[5], qa[6], qa[7]);
+            st_shared_v4(base + (((4 * hf + 2) ^ (lane & 7)) << 4), qb[0], qb[1], qb[2], qb[3]);
+            st_shared_v4(base + (((4 * hf + 3) ^ (lane & 7)) << 4), qb[4], qb[5], qb[6], qb[7]);
+          } else {
+            stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * 128 + c0, wrow0
 #if GEMM_WAITPROF
-                                  , wp_store_acc
+                                    , wp_store_acc
 #endif
-                                  );
-          if (F8) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
+                                    );
+          }
+          if (F8 && !MXOUT) amax = fmaxf(amax, fmaxf(bf16_lo(amax2), bf16_hi(amax2)));
         }
-        if (F8) atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
+        if (MXOUT) {
+          // the tile's 128 e4m3 columns x 32 rows in one TMA store; the scale word of row m of the
+          // CTA's 128-row block at word (m % 32) * 4 + m / 32 of the block's chunk for k-block nt
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_out, stg, nt * 128, wrow0);
+            bulk_commit();
+          }
+          p.mx_sf_out[((size_t)(mt * 2 + (int)rank) * p.mx_nkb + nt) * 128 + lane * 4 + quad] = sfw;
+        } else if (F8) {
+          atomicMax(p.amax_out + wrow0 + lane, __float_as_uint(amax));
+        }
       } else {
-        float sa = 1.f;
+        float sa = 1.f;  // MXIN: the A scales were applied by the block-scaled MMA
         const float* sb = nullptr;
+        const int ocol = MXIN ? col0 : nt * p.BN;  // the tile's first output column
         if (F8) {
-          sa = p.a_scale[wrow0 + lane];
+          if (!MXIN) sa = p.a_scale[wrow0 + lane];
           int ge = find_expert(s_ts, G, mt);
           if (p.group_mod > 0) ge %= p.group_mod;
           sb = reinterpret_cast<const float*>(
                    (ge >= p.own_lo && ge < p.own_hi ? p.b_scale_base_own + (size_t)(ge - p.own_lo) * p.expert_bytes
                                                     : p.b_scale_base + (size_t)ge * p.expert_bytes)) +
-               nt * p.BN;
-          sb = stage_scales(sScl + ew * 256, sb, p.BN, lane);
+               ocol;
+          sb = stage_scales(sScl + ew * 256, sb, MXIN ? width : p.BN, lane);
         }
         const int cbeg = 0;
-        const int cend = min(p.BN, max(p.n_out - nt * p.BN, 0));
+        const int cend = MXIN ? width : min(p.BN, max(p.n_out - nt * p.BN, 0));
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cend; c0 += 64) {
+          if (MXIN && c0 + 32 == cend) {
+            // a 32-column remainder (224-wide tiles): 64 B of this thread's row, stored directly
+            uint32_t r[32];
+            tmem_ld32(tb + c0, r);
+            tmem_ld_wait();
+            release();
+            uint32_t o[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 sv = ld_shared_f4(smem_u32(sb) + 4 * (c0 + 4 * q));
+              float v0, v1, v2, v3;
+              mul2(v0, v1, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), sv.x, sv.y);
+              mul2(v2, v3, __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), sv.z, sv.w);
+              o[2 * q] = pack_bf16x2(v0, v1);
+              o[2 * q + 1] = pack_bf16x2(v2, v3);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(p.out_ptr + (int64_t)(wrow0 + lane) * p.n_out + ocol + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_uint4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            break;
+          }
           uint32_t o[32];
           uint32_t rr[2][32];  // the chunk's 64 columns, one wait
           tmem_ld32(tb + c0, rr[0]);
@@ -889,7 +1084,7 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
               o[16 * half + 2 * q + 1] = pack_bf16x2(v[2], v[3]);
             }
           }
-          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, nt * p.BN + c0, wrow0
+          stage_and_store<C::NSTG>(o, stg + (chunk++ % C::NSTG) * STG_BYTES, lane, &map_out, ocol + c0, wrow0
 #if GEMM_WAITPROF
                                   , wp_store_acc
 #endif
@@ -897,8 +1092,6 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
         }
       }
       if (!released) release();  // router epilogue, or no stored columns
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
 #if GEMM_WAITPROF
     if (lane == 0 && warp == 4) printf("WPE %d %d %lld %lld %lld %lld\n", (int)blockIdx.x, (int)rank, clock64() - wp_t0, wp_f, wp_s, g_wp_store);
@@ -915,18 +1108,19 @@ __global__ void __launch_bounds__(Cfg<NCTA, MODE>::NTHR, 1) __maxnreg__((Cfg<NCT
   }
 }
 
-template <int MODE, int NCTA, bool F8 = false>
+template <int MODE, int NCTA, bool F8 = false, bool MX = false>
 void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mo, int grid,
-                 cudaStream_t s, const CUtensorMap* mb2 = nullptr) {
+                 cudaStream_t s, const CUtensorMap* mb2 = nullptr, const CUtensorMap* msf = nullptr) {
+  using C = Cfg<NCTA, MODE, MX && MODE == EPI_PLAIN>;
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Cfg<NCTA, MODE>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<MODE, NCTA, F8, MX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::SMEM);
   });
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(Cfg<NCTA, MODE>::NTHR);
-  cfg.dynamicSmemBytes = Cfg<NCTA, MODE>::SMEM;
+  cfg.blockDim = dim3(C::NTHR);
+  cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -935,7 +1129,7 @@ void launch_mode(const TcArgs& a, const CUtensorMap& ma, const CUtensorMap& mb, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8>, ma, mb, mo, mb2 ? *mb2 : mb, a);
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<MODE, NCTA, F8, MX>, ma, mb, mo, mb2 ? *mb2 : mb, msf ? *msf : mb, a);
 }
 
 // Grouped GEMMs run as CTA pairs by default.  ASYNCEP_GEMM_NCTA=1 selects the 1-CTA
@@ -953,9 +1147,10 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
                     int K, int BN, int n_tiles, int mode, int n_out, int num_sms, cudaStream_t s,
                     const int32_t* gather_rows = nullptr, const F8Args* f8 = nullptr, bool gemm2 = false,
                     const void* gather_src = nullptr, int64_t gather_ld = 0, const OwnShard* own = nullptr,
-                    bf16* out = nullptr) {
+                    bf16* out = nullptr, const CUtensorMap* msf = nullptr) {
   static const bool dyn = env_int("ASYNCEP_STATIC_SCHED", 0) == 0;
   const int ncta = f8 ? 2 : grouped_ncta();
+  const bool mx = f8 && f8->mx;
   TcArgs a{};
   a.tile_start = g.tile_start;
   a.E = g.E;
@@ -973,7 +1168,7 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   a.gather_ld = gather_ld;
   const CUtensorMap* mb2 = nullptr;
   a.counts = g.counts;
-  a.swap_max = (ncta == 2 && out && g.counts) ? (gemm2 ? g.swap_max2 : g.swap_max) : 0;
+  a.swap_max = (ncta == 2 && out && g.counts && !mx) ? (gemm2 ? g.swap_max2 : g.swap_max) : 0;
   a.out_ptr = out;
   if (own && own->maps && own->hi > own->lo) {
     a.own_lo = own->lo;
@@ -983,6 +1178,18 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
   }
   a.sched = (dyn && g.sched) ? g.sched + (gemm2 ? 2 : 1) : nullptr;
   a.group_mod = g.group_mod;
+  int tiles_per_rt = n_tiles;
+  if (mx && gemm2) {  // 256- and 224-wide N tiles, alternating (period 480) over the n_out columns
+    a.n_tiles = (n_out + kMxPeriod - 1) / kMxPeriod;
+    a.n_tiles2 = n_out > kMxWide ? (n_out - kMxWide + kMxPeriod - 1) / kMxPeriod : 0;
+    a.mx_nkb = K / 128;
+    static const int sfw = env_int("ASYNCEP_MX_SF_WARP", 2);
+    a.mx_sf_warp = sfw;
+    tiles_per_rt = a.n_tiles + a.n_tiles2;
+  } else if (mx) {
+    a.mx_sf_out = f8->act_sf;
+    a.mx_nkb = n_tiles;  // GEMM1 N tile nt = GEMM2 k-block nt (128 act columns)
+  }
   if (f8) {
     a.a_scale = gemm2 ? f8->act_scale : f8->x_scale;
     a.b_scale_base = f8->layer + (gemm2 ? f8->sd_off : f8->sgu_off);
@@ -990,9 +1197,12 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
     a.amax_out = gemm2 ? nullptr : f8->act_amax;
   }
   const int units = num_sms / ncta;
-  const int upper = g.max_m_tiles * a.ts_scale * n_tiles;
+  const int upper = g.max_m_tiles * a.ts_scale * tiles_per_rt;
   const int grid = ncta * (upper < units ? (upper > 0 ? upper : 1) : units);
-  if (f8) {  // FP8 experts: CTA pairs only
+  if (f8 && mx) {  // FP8 experts with the MX intermediate
+    if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true, true>(a, ma, mb, mo, grid, s, mb2);
+    else launch_mode<EPI_PLAIN, 2, true, true>(a, ma, mb, mo, grid, s, mb2, msf);
+  } else if (f8) {  // FP8 experts: CTA pairs only
     if (mode == EPI_SWIGLU) launch_mode<EPI_SWIGLU, 2, true>(a, ma, mb, mo, grid, s, mb2);
     else launch_mode<EPI_PLAIN, 2, true>(a, ma, mb, mo, grid, s, mb2);
   } else if (ncta == 2) {
@@ -1008,8 +1218,21 @@ void launch_grouped(const GroupedArgs& g, const CUtensorMap& ma, const CUtensorM
 int gemm2_bn(int H) { return H >= 256 ? 256 : H; }
 
 bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h, const uint8_t* xq,
-                   const uint8_t* aq) {
+                   const uint8_t* aq, const uint32_t* asf) {
   const uint32_t box[2] = {BK, BM};
+  if (aq && asf) {  // MX intermediate: e4m3 store map {128 cols, 32 rows}; scale chunks as [chunks][128] u32
+    const uint32_t sbox[2] = {128, 32};
+    const uint64_t d1[2] = {(uint64_t)h, (uint64_t)R_max};
+    const uint64_t s1[1] = {(uint64_t)h};
+    if (!encode_tmap(&m.aq_out, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, aq, d1, s1, sbox, CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const uint32_t fbox[2] = {128, 1};
+    const uint64_t d2[2] = {128, (uint64_t)(R_max / 128) * (uint64_t)(h / 128)};
+    const uint64_t s2[1] = {512};
+    if (!encode_tmap(&m.sfa, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, asf, d2, s2, fbox, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return false;
+    m.mx = true;
+  }
   if (xq && aq) {  // FP8 operands: 128 e4m3 = 128 B per k-block row
     const uint32_t qbox[2] = {128, BM};
     const uint64_t d1[2] = {(uint64_t)H, (uint64_t)R_max};
@@ -1077,13 +1300,14 @@ bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E
 bool launch_gemm1_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm, int H, int h, bf16* act,
                      const void* x_gather, int64_t T, const int32_t* src_tok, int num_sms, cudaStream_t s,
                      const F8Args* f8, const OwnShard* own) {
+  if (f8 && f8->mx && !am.mx) return false;
   // N tiles of 256 packed W_gu rows = 128 gate + 128 up columns -> 128 act columns.
   // x_gather != nullptr: dispatch fused into the A load (rows gathered from the token-major
   // x / x_q through src_tok); the A map is then unused.
   const int64_t ld = (int64_t)H * (f8 ? 1 : 2);
   const CUtensorMap& ma = f8 ? am.xq : am.xperm;
-  launch_grouped(g, ma, wm.wgu, am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h, num_sms, s,
-                 x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own, act);
+  launch_grouped(g, ma, wm.wgu, (f8 && f8->mx) ? am.aq_out : am.act_out, H, 256, (2 * h) / 256, EPI_SWIGLU, h,
+                 num_sms, s, x_gather ? src_tok : nullptr, f8, false, x_gather, ld, own, act);
   (void)T;
   return true;
 }
@@ -1092,7 +1316,7 @@ void launch_gemm2_tc(const GroupedArgs& g, const ActMaps& am, const GemmMaps& wm
                      int num_sms, cudaStream_t s, const F8Args* f8, const OwnShard* own) {
   const int bn = am.bn2;
   launch_grouped(g, f8 ? am.aq : am.act, wm.wd, am.yperm_out, h, bn, (H + bn - 1) / bn, EPI_PLAIN, H, num_sms, s,
-                 nullptr, f8, true, nullptr, 0, own, yperm);
+                 nullptr, f8, true, nullptr, 0, own, yperm, &am.sfa);
 }
 
 // ------------------------------------------------------------------ dense GEMM (NEXT-3 projections)

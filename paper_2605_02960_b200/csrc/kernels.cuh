@@ -62,8 +62,9 @@ struct GroupedArgs {
   const int32_t* counts;     // [E] rows per expert
   int E;
   int max_m_tiles;           // host upper bound on tile_start[E] (row tiles of kRowAlign)
-  int* sched = nullptr;      // [>= 3] dynamic tile counters, zeroed before each forward:
-                             // [0] router, [1] GEMM1, [2] GEMM2 (nullptr: static schedule)
+  int* sched = nullptr;      // [4] dynamic tile counters, zeroed before each forward:
+                             // [0] router, [1] GEMM1, [2] GEMM2, [3] MX GEMM2's 224-wide tiles
+                             // (nullptr: static schedule)
   int group_mod = 0;         // > 0: group g uses expert g % group_mod of the weight blob
   int swap_max = 0;          // > 0: an expert's last row tile with <= swap_max rows runs swap-AB
                              // (weights as M = 256, its tokens as N = rows rounded up to 16): GEMM1
@@ -101,6 +102,8 @@ struct F8Args {
   const uint8_t* layer;    // packed FP8 layer (E blobs)
   size_t expert_bytes;
   size_t sgu_off, sd_off;  // byte offsets of s_gu [2h] / s_down [H] inside a blob
+  bool mx = false;         // MX intermediate (R6b): GEMM1 writes e4m3 act + E8M0 scales (act_sf),
+  uint32_t* act_sf = nullptr;  // GEMM2 runs block-scaled; act_scale / act_amax unused
 };
 struct ActMaps {
   CUtensorMap xq;        // FP8: 2D {H, R_max} e4m3, box {128, 128}  (GEMM1 A)
@@ -109,12 +112,16 @@ struct ActMaps {
   CUtensorMap act;       // 2D {h, R_max}, box {64, 128}  (GEMM2 A)
   CUtensorMap act_out;   // 2D {h, R_max}, box {64, 32}   (GEMM1 epilogue TMA store)
   CUtensorMap yperm_out; // 2D {H, R_max}, box {64, 32}   (GEMM2 epilogue TMA store)
+  CUtensorMap aq_out;    // MX: 2D {h, R_max} e4m3, box {128, 32} (GEMM1 epilogue TMA store)
+  CUtensorMap sfa;       // MX: the intermediate's scale chunks, 2D u32 {128, R_max/128 * h/128}, box {128, 1}
   int bn2;               // GEMM2 N tile
+  bool mx = false;       // aq_out / sfa are valid
 };
 bool make_weight_maps(GemmMaps& m, const void* layer, size_t expert_bytes, int E, int H, int h, int bn2, bool fp8);
 // xq / aq: FP8 operand buffers (nullable when the experts are BF16)
+// asf (nullable): the MX scale chunks ((R_max / 128) * (h / 128) chunks of 512 B): MX maps too
 bool make_act_maps(ActMaps& m, const bf16* xperm, const bf16* act, int64_t R_max, int H, int h, const uint8_t* xq,
-                   const uint8_t* aq);
+                   const uint8_t* aq, const uint32_t* asf = nullptr);
 int gemm2_bn(int H);
 // x_gather != nullptr: A rows are gathered from the token-major x [T, H] (bf16, or the e4m3
 // x_q with f8) through src_tok by cp.async warps inside the GEMM, i.e. the dispatch is fused
