@@ -33,14 +33,16 @@ def main():
     ap.add_argument("--flags-a", type=lambda v: int(v, 0), default=0)
     ap.add_argument("--flags-b", type=lambda v: int(v, 0), default=A.FLAG_NO_SWAP_TAILS)
     ap.add_argument("--pairs", type=int, default=10)
+    ap.add_argument("--reverse-create", action="store_true", help="create context b before context a")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     T = args.tokens
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
     rf = lambda l: synth.router_weight(E, H, 0, l, device=dev)
     ef = lambda l, ex: gen(E, H, h, 0, l, device=dev, experts=ex)
+    order = (("b", args.flags_b), ("a", args.flags_a)) if args.reverse_create else (("a", args.flags_a), ("b", args.flags_b))
     st = {n: MoEStack(L, E, K, H, h, T, rf, ef, flags=A.FLAG_STAGE_TIMING | f, device=dev, fp8=args.fp8)
-          for n, f in (("a", args.flags_a), ("b", args.flags_b))}
+          for n, f in order}
     x = synth.tokens(T, H, 17, device=dev)
     out = {n: torch.empty_like(x) for n in st}
     cs = torch.cuda.current_stream()

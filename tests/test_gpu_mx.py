@@ -78,3 +78,31 @@ def test_mx_baseline_configs_sampled(shape, T, zipf):
     print("plain", check_layer(xs, wr, g, u, d, k, y[idx], ids[idx], w[idx], None, residual=False, tol=6e-2))
     print("mx", check_layer(xs, wr, g, u, d, k, y[idx], ids[idx], w[idx], None, residual=False, tol=1e-2,
                             act_quant="mx"))
+
+
+@pytest.mark.parametrize("rank", [0, 3])
+def test_mx_sharded_stack_bitwise(rank):
+    """MX on gathered layers: this rank's experts through its own shard's weight map, the others
+    through the slot; the 4-rank emulated stack equals the resident MX stack bitwise."""
+    from test_gpu_asyncep import _bits
+    wl = Workload(L=3, E=16, k=4, H=512, h=256, seed=29, fp8=True)
+    T = 700
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T, flags=MX).run(x).clone()
+    st = wl.stack(max_tokens=T, world_size=4, rank=rank, flags=MX)
+    out = st.run(x, local_shards=st.peer_shards()).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
+
+
+def test_mx_deterministic_and_empty():
+    """Two runs give the same bits (no atomics on outputs, dynamic tile order notwithstanding); a
+    zero-token forward is a no-op."""
+    wl = Workload(L=2, E=32, k=8, H=1024, h=384, seed=13, fp8=True)
+    st = wl.stack(max_tokens=3000, flags=MX)
+    x = wl.tokens(2999)
+    a = st.run(x).clone()
+    b = st.run(x).clone()
+    assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+    y0 = st.forward(0, x[:0], y=torch.empty_like(x[:0]))  # empty batch is a no-op
+    assert y0.shape[0] == 0
