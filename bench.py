@@ -281,6 +281,8 @@ def main():
     ap.add_argument("--no-ab", action="store_true",
                     help="skip the resident-vs-gathered interleaved measurement of exposed AllGather")
     ap.add_argument("--ab-steps", type=int, default=0, help="interleaved A/B pairs (default: max(steps, 6))")
+    ap.add_argument("--no-ab-control", action="store_true",
+                    help="no second resident stack in the exposed-AllGather A/B (its noise-floor control)")
     ap.add_argument("--ep", action="store_true",
                     help="contrast baseline: the same stack as synchronous DP x EP (two on-path AllToAlls "
                          "per layer, PAPER.md:196-199) instead of AsyncEP")
@@ -602,17 +604,42 @@ def main():
                                  ATT_HQ, ATT_HKV, max_prompts=int(cu.numel() - 1))
         run_res = lambda xin, o: res.run(xin, out=o, cu_seqlens=cu)
         out_r = torch.empty_like(x)
+        # control: a second resident stack (same weights and tokens, its own memory).  Two identical
+        # contexts can differ by a few % on some boxes (profiles/r02/mx: A/B harness control), so the
+        # resident time is the pooled median of both and their difference is reported as the noise.
+        ctl = None
+        if not args.no_ab_control:
+            ctl = MoEStack(L, E_, K_, H_, h_, T, router_fn, expert_fn, world_size=1, rank=0, replicate_layer0=True,
+                           flags=flags & ~A.FLAG_STAGE_TIMING, device=dev, fp8=args.fp8, compute_stream=cs)
+            if args.attn:
+                ctl.enable_attention(lambda l: synth.attn_weights(H_, ATT_HQ, ATT_HKV, 128, seed, l, device=dev),
+                                     ATT_HQ, ATT_HKV, max_prompts=int(cu.numel() - 1))
+        run_ctl = (lambda xin, o: ctl.run(xin, out=o, cu_seqlens=cu)) if ctl is not None else None
+        out_c = torch.empty_like(x)
         for _ in range(2):
             run_res(x, out_r)
             _run(x, out)
+            if run_ctl:
+                run_ctl(x, out_c)
         n_ab = args.ab_steps or max(args.steps, 6)
         clocks_ab = ClockSampler(dev_idx).start()
-        t_res, t_gat = [], []
-        for _ in range(n_ab):
-            t_res.append(timed_steps(1, run_res, x, out_r))
-            t_gat.append(timed_steps(1))
+        t_res, t_gat, t_ctl = [], [], []
+        mhz = {"r": [], "g": [], "c": []}  # per-leg median SM clock (is the interference the clock?)
+
+        def leg(tag, store, *a):
+            ck = ClockSampler(dev_idx, period=0.005).start()
+            store.append(timed_steps(1, *a))
+            mhz[tag].append(ck.stop().get("sm_mhz"))
+
+        legs = [("r", lambda: leg("r", t_res, run_res, x, out_r)), ("g", lambda: leg("g", t_gat))]
+        if run_ctl:
+            legs.append(("c", lambda: leg("c", t_ctl, run_ctl, x, out_c)))
+        for i in range(n_ab):  # rotate the order of the legs step by step
+            for j in range(len(legs)):
+                legs[(i + j) % len(legs)][1]()
         clk_ab = clocks_ab.stop()
-        med_r, med_g = float(np.median(t_res)), float(np.median(t_gat))
+        med_g = float(np.median(t_gat))
+        med_r = float(np.median(t_res + t_ctl))   # pooled resident legs
         bitwise = bool(torch.equal(out.view(torch.int16), out_r.view(torch.int16)))
         exp_layer = (med_g - med_r) / (L - 1)
         exposed = {
@@ -620,10 +647,20 @@ def main():
             "wait_ms_per_layer": per_layer_ms["gather_wait"],
             "step_ms_gathered": med_g, "step_ms_resident": med_r, "pairs": n_ab, "clocks": clk_ab,
             "output_bitwise_equal_resident": bitwise,
+            "sm_mhz_per_leg": {k: (float(np.median([m for m in v if m])) if any(v) else None)
+                               for k, v in mhz.items() if v},
             "note": ("SURVEY S8(d): (median gathered step - median resident step) / (L-1 gathered layers), "
-                     "steps interleaved one by one in this process (max over ranks); frac = that / resident "
-                     "layer time.  wait_ms_per_layer = the compute stream's wait for the slot before GEMM1 "
-                     "(inside the timed region) -- the part of the exposure that is not interference")}
+                     "steps interleaved one by one in this process, leg order rotated (max over ranks); frac = "
+                     "that / resident layer time; resident = the pooled steps of two resident contexts.  "
+                     "wait_ms_per_layer = the compute stream's wait for the slot before GEMM1 (inside the "
+                     "timed region) -- the part of the exposure that is not interference")}
+        if run_ctl:
+            m1, m2 = float(np.median(t_res)), float(np.median(t_ctl))
+            exposed["control"] = {
+                "step_ms_resident_1": m1, "step_ms_resident_2": m2,
+                "frac_of_layer": abs(m2 - m1) / (L - 1) / (med_r / L),
+                "note": "two identical resident contexts, normalised like frac_of_layer: the A/B's noise floor"}
+            del ctl
         del res
         torch.cuda.empty_cache()
 
