@@ -266,7 +266,10 @@ def main():
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
-    ap.add_argument("--xperm", action="store_true", help="materialise X_perm (unfused dispatch, FLAG_XPERM)")
+    ap.add_argument("--xperm", action="store_true", help="materialise X_perm (unfused dispatch, FLAG_XPERM; "
+                    "the FP8 default)")
+    ap.add_argument("--fused-dispatch", action="store_true",
+                    help="GEMM1 gathers the token rows (FLAG_FUSED_DISPATCH; the BF16 default)")
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
                     help="1-GPU emulation of the N-rank AsyncEP gather (copies of the N-1 peer shards into "
                          "the slot on the comm stream); measures exposed wait + interference")
@@ -340,7 +343,7 @@ def main():
     if args.graph and (world > 1 or args.emulate_gather or args.ep or args.offload):
         raise SystemExit("--graph: resident single-GPU stacks only (the gather's events cross steps)")
     flags = (0 if args.graph else A.FLAG_STAGE_TIMING) | (A.FLAG_SIMT_GEMM if args.simt else 0) | \
-        (A.FLAG_XPERM if args.xperm else 0)
+        (A.FLAG_XPERM if args.xperm else 0) | (A.FLAG_FUSED_DISPATCH if args.fused_dispatch else 0)
     graph_stream = torch.cuda.Stream(dev) if args.graph else None
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
     emu = args.emulate_gather if world == 1 else 0

@@ -30,6 +30,7 @@ FLAG_OFFLOAD = 0x20
 FLAG_NO_SWAP_TAILS = 0x40
 FLAG_SWAP_TAILS = 0x80
 FLAG_MX_ACT = 0x100
+FLAG_FUSED_DISPATCH = 0x200
 STAGES = ("router", "permute", "gather_wait", "gemm1_gateup_swiglu", "gemm2_down", "combine")
 
 

@@ -823,7 +823,11 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (and the identity / SIMT debug paths) materialise X_perm instead.
   const bool fp8 = cf.expert_dtype == ASYNCEP_FP8_E4M3;
   const bool identity = (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) != 0;
-  const bool gather_a = !(cf.flags & (ASYNCEP_FLAG_XPERM | ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM)) &&
+  // FP8 experts materialise the e4m3 X_perm by default (the quantisation pass writes the k rows of
+  // each token; GEMM1 then TMA-loads A: 9-10 % faster per step than the gathered A, S6)
+  const bool fp8_fused = cf.expert_dtype != ASYNCEP_FP8_E4M3 || (cf.flags & ASYNCEP_FLAG_FUSED_DISPATCH);
+  const bool gather_a = fp8_fused &&
+                        !(cf.flags & (ASYNCEP_FLAG_XPERM | ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM)) &&
                         ((uintptr_t)x % 16 == 0) && ((size_t)H * 2) % 16 == 0;
   const bool materialise = identity || (!gather_a && !fp8);
   aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);

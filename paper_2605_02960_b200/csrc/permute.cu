@@ -117,6 +117,26 @@ __global__ void __launch_bounds__(SCAN_THREADS) perm_scan_kernel(int32_t* __rest
   }
 }
 
+// The row copy of the dispatch: the warp's whole token row in registers (VPL 16-B vectors per lane,
+// all loads in flight at once), then its k destination rows written with 16-B stores.
+template <int VPL>
+__device__ __forceinline__ void copy_row_regs(const uint4* __restrict__ src, bf16* __restrict__ xperm,
+                                              const int32_t (&d)[kMaxTopK], int k, int H, int lane) {
+  uint4 val[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(val[i].x), "=r"(val[i].y), "=r"(val[i].z), "=r"(val[i].w)
+                 : "l"(src + lane + 32 * i));
+#pragma unroll
+  for (int j = 0; j < kMaxTopK; ++j)
+    if (j < k) {
+      uint4* dst = reinterpret_cast<uint4*>(xperm + (int64_t)d[j] * H) + lane;
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) dst[32 * i] = val[i];
+    }
+}
+
 __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restrict__ x,
                                                            const int32_t* __restrict__ ids,
                                                            const int32_t* __restrict__ blk_base,
@@ -189,6 +209,8 @@ __global__ void __launch_bounds__(256) perm_scatter_kernel(const bf16* __restric
     int32_t d[kMaxTopK];
 #pragma unroll
     for (int j = 0; j < kMaxTopK; ++j) d[j] = (j < k) ? dst[tl * k + j] : 0;
+    if (H == 4096) { copy_row_regs<16>(src, xperm, d, k, H, lane); continue; }
+    if (H == 2048) { copy_row_regs<8>(src, xperm, d, k, H, lane); continue; }
 #pragma unroll 4
     for (int v = lane; v < nv; v += 32) {
       uint4 val;
@@ -241,6 +263,54 @@ __global__ void __launch_bounds__(256) perm_quant_kernel(const bf16* __restrict_
       if (j < k) reinterpret_cast<uint2*>(xq + (int64_t)d[j] * H)[v] = o;
   }
   if (lane < k) xscale[d[lane]] = sc;
+}
+
+// perm_quant_kernel with the row in registers (H = 256 * VPL): one read of x, all VPL 16-B loads
+// of a lane in flight at once, 8-B e4m3 stores per destination row (256 contiguous bytes per warp).
+template <int VPL>
+__global__ void __launch_bounds__(256) perm_quant_reg_kernel(const bf16* __restrict__ x,
+                                                             const int32_t* __restrict__ dest, int64_t T, int k,
+                                                             uint8_t* __restrict__ xq, float* __restrict__ xscale) {
+  constexpr int H = 256 * VPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const uint4* src = reinterpret_cast<const uint4*>(x + t * H);
+  uint4 u[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i)
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(u[i].x), "=r"(u[i].y), "=r"(u[i].z), "=r"(u[i].w)
+                 : "l"(src + lane + 32 * i));
+  const int32_t dl = lane < k ? dest[t * k + lane] : 0;
+  uint32_t m = 0;  // max |x| over packed bf16 magnitudes (unsigned order = magnitude order)
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    m = __vmaxu2(m, u[i].x & 0x7fff7fffu);
+    m = __vmaxu2(m, u[i].y & 0x7fff7fffu);
+    m = __vmaxu2(m, u[i].z & 0x7fff7fffu);
+    m = __vmaxu2(m, u[i].w & 0x7fff7fffu);
+  }
+  float amax = fmaxf(bf16_lo(m), bf16_hi(m));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float inv = amax > 0.f ? 448.0f / amax : 0.f;
+  uint2 o[VPL];
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const uint32_t w[4] = {u[i].x, u[i].y, u[i].z, u[i].w};
+    o[i].x = (uint32_t)e4m3x2(bf16_lo(w[0]) * inv, bf16_hi(w[0]) * inv) |
+             ((uint32_t)e4m3x2(bf16_lo(w[1]) * inv, bf16_hi(w[1]) * inv) << 16);
+    o[i].y = (uint32_t)e4m3x2(bf16_lo(w[2]) * inv, bf16_hi(w[2]) * inv) |
+             ((uint32_t)e4m3x2(bf16_lo(w[3]) * inv, bf16_hi(w[3]) * inv) << 16);
+  }
+  for (int j = 0; j < k; ++j) {
+    const int32_t d = __shfl_sync(0xffffffffu, dl, j);
+    uint2* dst = reinterpret_cast<uint2*>(xq + (int64_t)d * H) + lane;
+#pragma unroll
+    for (int i = 0; i < VPL; ++i) dst[32 * i] = o[i];
+  }
+  if (lane < k) xscale[dl] = amax / 448.0f;
 }
 
 // Token-major form of perm_quant_kernel for the fused dispatch (x_q row t = token t): the same
@@ -309,8 +379,11 @@ void launch_perm_quant(const bf16* x, const int32_t* dest, int64_t T, int H, int
                        cudaStream_t s) {
   if (T <= 0) return;
   static const bool tok_kernel = getenv("ASYNCEP_QUANT_TOKENS") == nullptr || atoi(getenv("ASYNCEP_QUANT_TOKENS")) != 0;
-  if (!dest && tok_kernel) quant_tokens_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, T, H, xq, xscale);
-  else perm_quant_kernel<<<(unsigned)((T + 7) / 8), 256, 0, s>>>(x, dest, T, H, k, xq, xscale);
+  const unsigned grid = (unsigned)((T + 7) / 8);
+  if (!dest && tok_kernel) quant_tokens_kernel<<<grid, 256, 0, s>>>(x, T, H, xq, xscale);
+  else if (dest && H == 4096) perm_quant_reg_kernel<16><<<grid, 256, 0, s>>>(x, dest, T, k, xq, xscale);
+  else if (dest && H == 2048) perm_quant_reg_kernel<8><<<grid, 256, 0, s>>>(x, dest, T, k, xq, xscale);
+  else perm_quant_kernel<<<grid, 256, 0, s>>>(x, dest, T, H, k, xq, xscale);
 }
 
 void launch_act_quant(const bf16* act, uint32_t* act_amax, const int32_t* offsets, int E, int64_t R, int h,

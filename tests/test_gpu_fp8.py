@@ -33,7 +33,7 @@ def test_fp8_weights_bit_identical_cpu_gpu():
                            tb.cpu().view(torch.uint8) if tb.dtype == torch.uint8 else tb.cpu().view(torch.int32))
 
 
-@pytest.mark.parametrize("flags", [0, 16], ids=["fused_dispatch", "xperm"])
+@pytest.mark.parametrize("flags", [0x200, 0], ids=["fused_dispatch", "xperm_default"])
 @pytest.mark.parametrize("T", [300, 2048])
 def test_fp8_layer_parity(T, flags):
     wl = Workload(L=2, E=16, k=4, H=512, h=256, seed=21, fp8=True)
@@ -67,14 +67,16 @@ def test_fp8_qwen3_235b_shape_sampled():
                               act_quant=True))
 
 
+@pytest.mark.parametrize("H", [1024, 2048])
 @pytest.mark.parametrize("T", [1, 777, 4096])
-def test_fp8_fused_dispatch_bitwise(T):
-    """GEMM1 gathering e4m3 token rows itself (default: token-major x_q + per-token scale)
-    computes exactly what the materialised X_perm path (FLAG_XPERM) computes."""
-    wl = Workload(L=1, E=64, k=6, H=1024, h=512, seed=5, fp8=True)
+def test_fp8_fused_dispatch_bitwise(T, H):
+    """GEMM1 gathering e4m3 token rows itself (FLAG_FUSED_DISPATCH: token-major x_q + per-token
+    scale) computes exactly what the materialised X_perm path (the FP8 default) computes; H = 2048
+    runs the register-resident quantisation kernel."""
+    wl = Workload(L=1, E=64, k=6, H=H, h=512, seed=5, fp8=True)
     x = wl.tokens(T)
     outs = []
-    for flags in (0, 16):
+    for flags in (0x200, 0):
         st = wl.stack(max_tokens=4096, flags=flags)
         outs.append(run_layer(wl, st, 0, x)[0])
         del st

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 MX = 0x100
 
 
-@pytest.mark.parametrize("flags", [MX, MX | 16], ids=["fused_dispatch", "xperm"])
+@pytest.mark.parametrize("flags", [MX | 0x200, MX], ids=["fused_dispatch", "xperm_default"])
 @pytest.mark.parametrize("T", [300, 2048])
 def test_mx_layer_parity(T, flags):
     """H = 512: one 256-wide, one 224-wide and one clipped 32-wide N tile per row tile."""
@@ -51,7 +51,7 @@ def test_mx_fused_dispatch_bitwise(T):
     wl = Workload(L=1, E=64, k=6, H=1024, h=512, seed=5, fp8=True)
     x = wl.tokens(T)
     outs = []
-    for flags in (MX, MX | 16):
+    for flags in (MX | 0x200, MX):
         st = wl.stack(max_tokens=4096, flags=flags)
         outs.append(run_layer(wl, st, 0, x)[0])
         del st

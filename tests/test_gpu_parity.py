@@ -217,14 +217,16 @@ def test_config5_zipf_skewed_full_size_sampled():
     print(check_layer(f32(x)[idx], wr, g, u, d, wl.k, y[idx], ids[idx], w[idx], None))
 
 
-@pytest.mark.parametrize("swap", [False, True], ids=["padded_tails", "swap_tails"])
+@pytest.mark.parametrize("swap,H", [(False, 1024), (True, 1024), (False, 2048)],
+                         ids=["padded_tails", "swap_tails", "padded_tails_h2048"])
 @pytest.mark.parametrize("T", [1, 129, 5000])
-def test_fused_dispatch_bitwise(T, swap):
+def test_fused_dispatch_bitwise(T, swap, H):
     """GEMM1 gathering token rows of x itself (default: cp.async warps through src_tok)
     computes exactly what the materialised X_perm path (FLAG_XPERM) computes: same A bytes,
-    same MMAs; with the swap-AB tail tiles the gathered rows land in the B (N) operand instead."""
+    same MMAs; with the swap-AB tail tiles the gathered rows land in the B (N) operand instead;
+    H = 2048 runs the scatter's register-resident row copy."""
     from paper_2605_02960_b200 import asyncep as A
-    wl = Workload(L=1, E=64, k=8, H=1024, h=768, seed=9)
+    wl = Workload(L=1, E=64, k=8, H=H, h=768, seed=9)
     x = wl.tokens(T)
     outs = []
     sw = A.FLAG_SWAP_TAILS if swap else A.FLAG_NO_SWAP_TAILS
