@@ -70,6 +70,9 @@ def set_shape(name: str) -> None:
     GEMM2_FLOPS_TOK = 2 * K_ * H_ * h_
 
 
+B200_SMS = 148
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -79,23 +82,20 @@ def load_peaks():
 
 
 def tensor_peak(peaks: dict, src: str, run_mhz, fp8: bool):
-    """Clock-aware tensor peak for the dominant kernel: MEASURED_PEAKS' sustained cuBLAS bf16 rate
-    was taken at clocks_under_load.sm_mhz_median; the tensor pipe's rate is linear in the SM clock,
-    so the peak at this run's median clock is sustained x run_mhz / that clock, capped at the burst
-    figure (the most the part reached at all).  FP8: x 2 (nominal fp8:bf16 dense ratio)."""
+    """Tensor peak for the dominant kernel, which is timed inside a long step: MEASURED_PEAKS'
+    sustained cuBLAS bf16 rate (FP8: x 2, the nominal fp8:bf16 dense ratio).  The burst figure and
+    the nominal per-clock rate at this run's median SM clock (8,192 bf16 FLOP/clk/SM x SMs x clock)
+    are returned beside it for context (a power-capped run's clock moves the achievable rate)."""
     burst = peaks.get("bf16_tflops", 1590.0)
     sus = peaks.get("bf16_tflops_sustained", burst)
     sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
     mult = 2.0 if fp8 else 1.0
-    if run_mhz and sus_mhz:
-        peak = min(burst, sus * run_mhz / sus_mhz)
-        note = (f"{src} bf16_tflops_sustained {sus} at {sus_mhz} MHz scaled to this run's median {run_mhz} MHz, "
-                f"capped at the burst {burst}")
-    else:
-        peak, note = sus, f"{src} bf16_tflops_sustained (no clock record)"
+    note = f"{src} bf16_tflops_sustained {sus}" + (f" (median {sus_mhz} MHz under load)" if sus_mhz else "")
     if fp8:
         note += " x 2 (nominal fp8:bf16 dense ratio)"
-    return peak * mult, note, {"burst": burst * mult, "sustained": sus * mult}
+    nominal = 8192.0 * B200_SMS * run_mhz * 1e6 / 1e12 if run_mhz else None
+    return sus * mult, note, {"burst": burst * mult, "sustained": sus * mult,
+                              "nominal_at_run_clock": nominal * mult if nominal else None}
 
 
 class ClockSampler:
@@ -266,10 +266,9 @@ def main():
     ap.add_argument("--layers", type=int, default=L_)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
-    ap.add_argument("--xperm", action="store_true", help="materialise X_perm (unfused dispatch, FLAG_XPERM; "
-                    "the FP8 default)")
+    ap.add_argument("--xperm", action="store_true", help="materialise X_perm (FLAG_XPERM; the default)")
     ap.add_argument("--fused-dispatch", action="store_true",
-                    help="GEMM1 gathers the token rows (FLAG_FUSED_DISPATCH; the BF16 default)")
+                    help="GEMM1 gathers the token rows itself (FLAG_FUSED_DISPATCH)")
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
                     help="1-GPU emulation of the N-rank AsyncEP gather (copies of the N-1 peer shards into "
                          "the slot on the comm stream); measures exposed wait + interference")
@@ -738,8 +737,12 @@ def main():
                             if per_layer_ms.get("combine") else None),
             "combine_bytes_per_token": COMBINE_BYTES_TOK,
             "peak_gbs": peaks.get("hbm_gbs"),
+            "dispatch_gbs": (T * (H_ * 2 + K_ * H_ * (1 if args.fp8 else 2)) / (per_layer_ms["permute"] / 1e3) / 1e9
+                             if per_layer_ms.get("permute") and not args.fused_dispatch else None),
             "note": "combine reads k bf16 expert rows + the residual and writes y (81,920 B/token); the dispatch "
-                    "writes only the row maps (the row copy is fused into GEMM1's A load)"},
+                    "(permute stage: maps + row copy, or the FP8 quantisation into the k rows) reads x once and "
+                    "writes k rows per token (73,728 B/token BF16, 40,960 B/token FP8); with --fused-dispatch it "
+                    "writes only the row maps (GEMM1 gathers the rows)"},
         "attention": attn_info,
         "saturation_T": {"tokens_per_gpu": t_tok, "flops": t_flops, "N": n_for_T, "gamma": 1.2,
                          "flops_per_s": f_gemm, "ag_bytes_per_s": bw, "ag_bandwidth_source": bw_src,
@@ -755,6 +758,8 @@ def main():
                      "peak_source": peak_note,
                      "frac_of_burst": g1_tflops / peak_ref["burst"] if g1_tflops else None,
                      "frac_of_sustained": g1_tflops / peak_ref["sustained"] if g1_tflops else None,
+                     "frac_of_nominal_at_run_clock": (g1_tflops / peak_ref["nominal_at_run_clock"]
+                                                      if g1_tflops and peak_ref["nominal_at_run_clock"] else None),
                      "algorithmic_flops_per_launch": g1_flops, "ms_per_launch": g1_ms,
                      "traffic": traffic},
         "clocks": clk,

@@ -61,18 +61,19 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
 #define ASYNCEP_FLAG_SIMT_GEMM        0x2 /* CUDA-core grouped GEMM instead of tcgen05 (sanitizer runs) */
 #define ASYNCEP_FLAG_STAGE_TIMING     0x4 /* record CUDA events around each stage (asyncep_stage_times) */
 #define ASYNCEP_FLAG_SIMT_ROUTER      0x8 /* CUDA-core router logits instead of tcgen05                */
-#define ASYNCEP_FLAG_XPERM           0x10 /* materialise X_perm and TMA-load it (the default for FP8
-                                               experts; BF16 default: GEMM1 gathers the token rows
-                                               itself through src_tok, cp.async)                    */
+#define ASYNCEP_FLAG_XPERM           0x10 /* materialise X_perm and TMA-load it: the default (kept as
+                                               an explicit spelling; overrides FUSED_DISPATCH)      */
 #define ASYNCEP_FLAG_OFFLOAD         0x20 /* NEXT-2: expert_shard[l] may be NULL for offloaded layers  */
 #define ASYNCEP_FLAG_NO_SWAP_TAILS   0x40 /* compute every expert's last row tile as a padded 256-row
                                                tile (default: swap-AB tail tiles where they pay,
                                                FP8 gate/up GEMM; S6)                     */
 #define ASYNCEP_FLAG_SWAP_TAILS      0x80 /* swap-AB tail tiles (<= 240 rows) in both GEMMs and both
                                                dtypes (A/B and tests)                               */
-#define ASYNCEP_FLAG_FUSED_DISPATCH 0x200 /* the fused dispatch (GEMM1 gathers the token rows through
-                                               src_tok) also for FP8 experts, whose default is the
-                                               materialised X_perm (S6: 9-10 % faster)     */
+#define ASYNCEP_FLAG_FUSED_DISPATCH 0x200 /* the fused dispatch: GEMM1's cp.async warps gather the
+                                               token rows through src_tok and X_perm is never
+                                               written (default: the dispatch writes X_perm and
+                                               GEMM1 TMA-loads it; S6: FP8 10-12 %, BF16
+                                               0.3-3 % faster per step)                             */
 #define ASYNCEP_FLAG_MX_ACT         0x100 /* FP8 experts: the intermediate is quantised MX-style (e4m3,
                                                one E8M0 power-of-two scale per 32 columns, DESIGN.md
                                                R6b) inside the gate/up GEMM's epilogue and the down

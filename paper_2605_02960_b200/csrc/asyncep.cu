@@ -823,10 +823,11 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   // (and the identity / SIMT debug paths) materialise X_perm instead.
   const bool fp8 = cf.expert_dtype == ASYNCEP_FP8_E4M3;
   const bool identity = (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) != 0;
-  // FP8 experts materialise the e4m3 X_perm by default (the quantisation pass writes the k rows of
-  // each token; GEMM1 then TMA-loads A: 9-10 % faster per step than the gathered A, S6)
-  const bool fp8_fused = cf.expert_dtype != ASYNCEP_FP8_E4M3 || (cf.flags & ASYNCEP_FLAG_FUSED_DISPATCH);
-  const bool gather_a = fp8_fused &&
+  // The dispatch materialises X_perm by default (BF16 rows, or the e4m3 rows the quantisation pass
+  // writes for each of a token's k experts) and GEMM1 TMA-loads A: per step 10-12 % (FP8) and
+  // 0.3-3 % (BF16) faster than GEMM1 gathering the rows itself (FLAG_FUSED_DISPATCH; S6)
+  const bool fused = (cf.flags & ASYNCEP_FLAG_FUSED_DISPATCH) != 0;
+  const bool gather_a = fused &&
                         !(cf.flags & (ASYNCEP_FLAG_XPERM | ASYNCEP_FLAG_IDENTITY_EXPERTS | ASYNCEP_FLAG_SIMT_GEMM)) &&
                         ((uintptr_t)x % 16 == 0) && ((size_t)H * 2) % 16 == 0;
   const bool materialise = identity || (!gather_a && !fp8);

@@ -1,4 +1,4 @@
-"""Host-side logic of bench.py (no GPU): the clock-aware roofline peak and the N-rank launcher's
+"""Host-side logic of bench.py (no GPU): the roofline peak and the N-rank launcher's
 refusal when fewer GPUs than --gpus are visible."""
 import os
 import subprocess
@@ -14,19 +14,18 @@ import bench  # noqa: E402
 PEAKS = {"bf16_tflops": 1680.5, "bf16_tflops_sustained": 1448.3, "clocks_under_load": {"sm_mhz_median": 1395.0}}
 
 
-def test_tensor_peak_scales_with_the_run_clock():
+def test_tensor_peak_is_the_measured_sustained_rate():
     p, note, ref = bench.tensor_peak(PEAKS, "measured", 1237, False)
-    assert p == pytest.approx(1448.3 * 1237 / 1395.0, rel=1e-12)
-    assert ref == {"burst": 1680.5, "sustained": 1448.3} and "1237" in note
-    # at the sustained measurement's own clock the peak is the sustained figure
-    assert bench.tensor_peak(PEAKS, "measured", 1395, False)[0] == pytest.approx(1448.3)
-    # never above the burst figure, however high the clock
-    assert bench.tensor_peak(PEAKS, "measured", 1965, False)[0] == pytest.approx(1680.5)
+    assert p == pytest.approx(1448.3) and "1448.3" in note
+    assert ref["burst"] == 1680.5 and ref["sustained"] == 1448.3
+    # context: the nominal 8,192 FLOP/clk/SM x 148 SMs at the run's clock
+    assert ref["nominal_at_run_clock"] == pytest.approx(8192 * 148 * 1237e6 / 1e12)
     # FP8: x 2 (nominal fp8:bf16 dense ratio), references too
     p8, _, ref8 = bench.tensor_peak(PEAKS, "measured", 1237, True)
     assert p8 == pytest.approx(2 * p) and ref8["burst"] == pytest.approx(2 * 1680.5)
-    # no clock record: the sustained figure
-    assert bench.tensor_peak(PEAKS, "measured", None, False)[0] == pytest.approx(1448.3)
+    assert ref8["nominal_at_run_clock"] == pytest.approx(2 * ref["nominal_at_run_clock"])
+    # no clock record: no nominal figure
+    assert bench.tensor_peak(PEAKS, "measured", None, False)[2]["nominal_at_run_clock"] is None
 
 
 def test_self_launch_refuses_more_ranks_than_gpus():

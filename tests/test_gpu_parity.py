@@ -221,8 +221,8 @@ def test_config5_zipf_skewed_full_size_sampled():
                          ids=["padded_tails", "swap_tails", "padded_tails_h2048"])
 @pytest.mark.parametrize("T", [1, 129, 5000])
 def test_fused_dispatch_bitwise(T, swap, H):
-    """GEMM1 gathering token rows of x itself (default: cp.async warps through src_tok)
-    computes exactly what the materialised X_perm path (FLAG_XPERM) computes: same A bytes,
+    """GEMM1 gathering token rows of x itself (FLAG_FUSED_DISPATCH: cp.async warps through src_tok)
+    computes exactly what the materialised X_perm path (the default) computes: same A bytes,
     same MMAs; with the swap-AB tail tiles the gathered rows land in the B (N) operand instead;
     H = 2048 runs the scatter's register-resident row copy."""
     from paper_2605_02960_b200 import asyncep as A
@@ -230,7 +230,7 @@ def test_fused_dispatch_bitwise(T, swap, H):
     x = wl.tokens(T)
     outs = []
     sw = A.FLAG_SWAP_TAILS if swap else A.FLAG_NO_SWAP_TAILS
-    for flags in (sw, sw | A.FLAG_XPERM):
+    for flags in (sw | A.FLAG_FUSED_DISPATCH, sw):
         st = wl.stack(max_tokens=8192, flags=flags)
         outs.append(run_layer(wl, st, 0, x)[0])
         del st
