@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--flags-b", type=lambda v: int(v, 0), default=A.FLAG_NO_SWAP_TAILS)
     ap.add_argument("--pairs", type=int, default=10)
     ap.add_argument("--reverse-create", action="store_true", help="create context b before context a")
+    ap.add_argument("--emulate", type=int, default=1, help="N > 1: both stacks gathered, N ranks emulated")
+    ap.add_argument("--link-gbs", type=float, default=770.0, help="emulated link rate (with --emulate)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     T = args.tokens
@@ -41,8 +43,15 @@ def main():
     rf = lambda l: synth.router_weight(E, H, 0, l, device=dev)
     ef = lambda l, ex: gen(E, H, h, 0, l, device=dev, experts=ex)
     order = (("b", args.flags_b), ("a", args.flags_a)) if args.reverse_create else (("a", args.flags_a), ("b", args.flags_b))
-    st = {n: MoEStack(L, E, K, H, h, T, rf, ef, flags=A.FLAG_STAGE_TIMING | f, device=dev, fp8=args.fp8)
+    N = args.emulate
+    st = {n: MoEStack(L, E, K, H, h, T, rf, ef, flags=A.FLAG_STAGE_TIMING | f, device=dev, fp8=args.fp8,
+                      **({"world_size": N, "rank": 0} if N > 1 else {}))
           for n, f in order}
+    shards = {}
+    for n in st:  # N > 1: the N-rank gather emulated on this GPU (peer shards, paced copy kernel)
+        shards[n] = st[n].peer_shards() if N > 1 else None
+        if N > 1 and args.link_gbs > 0:
+            A.asyncep_set_link_emulation(st[n].ctx, args.link_gbs * 1e9)
     x = synth.tokens(T, H, 17, device=dev)
     out = {n: torch.empty_like(x) for n in st}
     cs = torch.cuda.current_stream()
@@ -51,7 +60,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(cs)
-        st[n].run(x, out=out[n])
+        st[n].run(x, out=out[n], local_shards=shards[n])
         e1.record(cs)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
@@ -72,7 +81,7 @@ def main():
         s, f = A.asyncep_stage_times(st[n].ctx)
         stages[n] = {k: v / max(f, 1) for k, v in s.items()}
     ma, mb = float(np.median(t["a"])), float(np.median(t["b"]))
-    print(json.dumps({"fp8": args.fp8, "tokens": T, "flags_a": args.flags_a, "flags_b": args.flags_b,
+    print(json.dumps({"fp8": args.fp8, "tokens": T, "emulate": N, "flags_a": args.flags_a, "flags_b": args.flags_b,
                       "step_ms_a": ma, "step_ms_b": mb, "speedup_a_over_b": mb / ma,
                       "tokens_per_s_a": T / (ma / 1e3), "tokens_per_s_b": T / (mb / 1e3),
                       "stage_ms_a": stages["a"], "stage_ms_b": stages["b"], "all_a": t["a"], "all_b": t["b"],
