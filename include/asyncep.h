@@ -249,6 +249,18 @@ ASYNCEP_API asyncep_status asyncep_gather_copy(void* dst, const void* src, size_
 ASYNCEP_API asyncep_status asyncep_set_link_emulation(asyncep_ctx* ctx, double bytes_per_s);
 
 /*
+ * Gated gather (every transport; §6.2: the grouped-GEMM time is what hides the gather).
+ * on != 0: asyncep_prefetch_layer(_local) validates and claims the slot but holds the gather on the
+ * host; the NEXT asyncep_moe_forward on this context enqueues it once its dispatch is enqueued, with
+ * the comm stream waiting for the compute stream to get there (an event), so the gather's HBM traffic
+ * overlaps the grouped GEMMs rather than the HBM-bound combine / router / dispatch.  The layer's own
+ * forward also releases it (before its wait for the slot).  on == 0 enqueues every held gather at
+ * once.  The startup probe (asyncep_probe_gather) is never held.  Errors: INVALID_ARG (ctx NULL), or
+ * those of the held prefetches when on == 0.
+ */
+ASYNCEP_API asyncep_status asyncep_set_gather_gate(asyncep_ctx* ctx, int32_t on);
+
+/*
  * The MoE FFN forward of layer `layer` on the compute stream.
  *  x         : [num_tokens, H] bf16 device, 16-B aligned rows.
  *  residual  : nullable [num_tokens, H] bf16 device; added to the output (reading R9).

@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
             "asyncep_calibrate_T": ([P, D, I64, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(D),
                                      ctypes.POINTER(D)], I32),
             "asyncep_set_link_emulation": ([P, D], I32),
+            "asyncep_set_gather_gate": ([P, I32], I32),
             "asyncep_set_peer_shards": ([P, P], I32),
             "asyncep_gather_copy": ([P, P, SZ, P], I32),
             "asyncep_enable_offload": ([P, P, P, I32, P], I32),
@@ -319,6 +320,11 @@ def asyncep_gather_copy(dst, src, nbytes: int, stream=None) -> None:
 
 def asyncep_set_link_emulation(ctx: Context, bytes_per_s: float) -> None:
     _check(lib().asyncep_set_link_emulation(ctx.handle, float(bytes_per_s)))
+
+
+def asyncep_set_gather_gate(ctx: Context, on: bool) -> None:
+    """Copy-kernel gathers move bytes only while a forward's grouped GEMMs run (asyncep.h)."""
+    _check(lib().asyncep_set_gather_gate(ctx.handle, int(bool(on))))
 
 
 def asyncep_moe_forward(ctx: Context, layer: int, x: torch.Tensor, residual=None, y=None,

@@ -280,6 +280,15 @@ struct asyncep_ctx {
   std::vector<std::pair<int32_t, std::pair<cudaEvent_t, cudaEvent_t>>> tl_gather;  // pending gathers
   int64_t launches = 0;
   double link_bps = 0.0;  // prefetch_layer_local pacing (0 = off)
+  // asyncep_set_gather_gate: prefetches are held on the host (pending) and enqueued by the next
+  // forward at its gate point -- after its dispatch -- with the comm stream waiting on gate_ev there
+  struct PendingGather {
+    int32_t layer;
+    std::vector<const void*> shards;  // empty: peer shards / NCCL
+  };
+  std::vector<PendingGather> pending;
+  cudaEvent_t gate_ev = nullptr;
+  bool gate_on = false, probing = false, flushing = false;
   std::vector<const void*> peer;  // P2P gather: [layer * N + rank] peer-mapped shard pointers (empty: NCCL)
   std::vector<aep::GemmMaps> ep_maps;  // EP contrast: maps over this rank's shard of each layer
   std::vector<char> ep_maps_ok;
@@ -527,6 +536,17 @@ static asyncep_status prefetch_common(asyncep_ctx* c, int32_t layer, const void*
     return fail(ASYNCEP_ERR_INVALID_ARG,
                 "slot %d still holds layer %d whose forward has not been issued (at most 2 layers in flight)", s,
                 c->slot_layer[s]);
+  // gated: held until the next forward's gate point, after its HBM-bound dispatch (the grouped GEMMs
+  // then hide the gather, instead of the combine / router / dispatch); the slot is
+  // claimed now, so the forward's checks see the layer as prefetched
+  if (c->gate_on && !c->probing && !c->flushing) {
+    asyncep_ctx::PendingGather p{layer, {}};
+    if (shards) p.shards.assign(shards, shards + c->cfg.world_size);
+    c->pending.push_back(std::move(p));
+    c->slot_layer[s] = layer;
+    c->slot_consumed[s] = false;
+    return ASYNCEP_OK;
+  }
   // WAR: the slot's previous occupant must have finished its GEMMs.
   CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
   const void* own = c->shard[layer];
@@ -718,7 +738,9 @@ asyncep_status asyncep_probe_gather(asyncep_ctx* c, int32_t layer, const void* c
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaStreamWaitEvent(c->ms, c->slot_free[s], 0));
   CUDA_TRY(cudaEventRecord(e0, c->ms));
+  c->probing = true;  // the probe's gather runs alone: never gated
   asyncep_status st = prefetch_common(c, layer, shards);
+  c->probing = false;
   if (st == ASYNCEP_OK) {
     CUDA_TRY(cudaEventRecord(e1, c->ms));
     CUDA_TRY(cudaEventSynchronize(e1));
@@ -740,6 +762,34 @@ asyncep_status asyncep_gather_copy(void* dst, const void* src, size_t bytes, voi
   if ((!dst || !src) && bytes) return fail(ASYNCEP_ERR_INVALID_ARG, "null pointer");
   if (!bytes) return ASYNCEP_OK;
   CUDA_TRY(gather_copy(dst, src, bytes, (cudaStream_t)stream));
+  return ASYNCEP_OK;
+}
+
+// Enqueue the held (gated) gathers; gated: the comm stream first waits for gate_stream (which may be
+// the legacy default stream, handle 0) to reach this point.
+static asyncep_status flush_pending(asyncep_ctx* c, bool gated, cudaStream_t gate_stream) {
+  if (c->pending.empty()) return ASYNCEP_OK;
+  if (gated) {
+    if (!c->gate_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->gate_ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(c->gate_ev, gate_stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->ms, c->gate_ev, 0));
+  }
+  std::vector<asyncep_ctx::PendingGather> todo;
+  todo.swap(c->pending);
+  c->flushing = true;
+  asyncep_status st = ASYNCEP_OK;
+  for (auto& p : todo) {
+    st = prefetch_common(c, p.layer, p.shards.empty() ? nullptr : p.shards.data());
+    if (st) break;
+  }
+  c->flushing = false;
+  return st;
+}
+
+asyncep_status asyncep_set_gather_gate(asyncep_ctx* c, int32_t on) {
+  if (!c) return fail(ASYNCEP_ERR_INVALID_ARG, "ctx is NULL");
+  c->gate_on = on != 0;
+  if (!c->gate_on) return flush_pending(c, false, nullptr);  // held gathers start now
   return ASYNCEP_OK;
 }
 
@@ -850,6 +900,11 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     c->launches += 1;
   }
   if (timing) CUDA_TRY(cudaEventRecord(ev[2], st));
+  // gated gathers (asyncep_set_gather_gate) held since their prefetch are enqueued here: after the
+  // dispatch, before the wait for this layer's slot (a held gather of this very layer included)
+  if (!c->pending.empty()) {
+    if (asyncep_status e = flush_pending(c, true, st)) return e;
+  }
   // wait for this layer's gathered experts (placed just before GEMM1 so router and
   // permute also overlap the gather tail)
   if (from_window) CUDA_TRY(cudaStreamWaitEvent(st, c->h2d_done[wi], 0));
@@ -1383,6 +1438,7 @@ asyncep_status asyncep_destroy(asyncep_ctx* c) {
     cudaEventDestroy(g.second.second);
   }
   if (c->epoch) cudaEventDestroy(c->epoch);
+  if (c->gate_ev) cudaEventDestroy(c->gate_ev);
   for (auto& e : c->h2d_done)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->win_free)

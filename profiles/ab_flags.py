@@ -36,6 +36,8 @@ def main():
     ap.add_argument("--reverse-create", action="store_true", help="create context b before context a")
     ap.add_argument("--emulate", type=int, default=1, help="N > 1: both stacks gathered, N ranks emulated")
     ap.add_argument("--link-gbs", type=float, default=770.0, help="emulated link rate (with --emulate)")
+    ap.add_argument("--gate", default="none", choices=["none", "a", "b", "both"],
+                    help="gated gather (asyncep_set_gather_gate) in context a / b / both (with --emulate)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     T = args.tokens
@@ -52,6 +54,8 @@ def main():
         shards[n] = st[n].peer_shards() if N > 1 else None
         if N > 1 and args.link_gbs > 0:
             A.asyncep_set_link_emulation(st[n].ctx, args.link_gbs * 1e9)
+        if N > 1 and args.gate in (n, "both"):
+            A.asyncep_set_gather_gate(st[n].ctx, True)
     x = synth.tokens(T, H, 17, device=dev)
     out = {n: torch.empty_like(x) for n in st}
     cs = torch.cuda.current_stream()
@@ -81,7 +85,7 @@ def main():
         s, f = A.asyncep_stage_times(st[n].ctx)
         stages[n] = {k: v / max(f, 1) for k, v in s.items()}
     ma, mb = float(np.median(t["a"])), float(np.median(t["b"]))
-    print(json.dumps({"fp8": args.fp8, "tokens": T, "emulate": N, "flags_a": args.flags_a, "flags_b": args.flags_b,
+    print(json.dumps({"fp8": args.fp8, "tokens": T, "emulate": N, "gate": args.gate, "flags_a": args.flags_a, "flags_b": args.flags_b,
                       "step_ms_a": ma, "step_ms_b": mb, "speedup_a_over_b": mb / ma,
                       "tokens_per_s_a": T / (ma / 1e3), "tokens_per_s_b": T / (mb / 1e3),
                       "stage_ms_a": stages["a"], "stage_ms_b": stages["b"], "all_a": t["a"], "all_b": t["b"],

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=32768)
     ap.add_argument("--N", type=int, default=8)
     ap.add_argument("--link-gbs", type=float, default=770.0)
+    ap.add_argument("--gate", action="store_true", help="gated gather (asyncep_set_gather_gate)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     gen = synth.expert_weights_fp8 if args.fp8 else synth.expert_weights
@@ -39,6 +40,8 @@ def main():
                   flags=A.FLAG_STAGE_TIMING, device=dev, fp8=args.fp8)
     shards = st.peer_shards()
     A.asyncep_set_link_emulation(st.ctx, args.link_gbs * 1e9)
+    if args.gate:
+        A.asyncep_set_gather_gate(st.ctx, True)
     x = synth.tokens(args.tokens, H, 17, device=dev)
     out = torch.empty_like(x)
     for _ in range(3):
@@ -57,7 +60,7 @@ def main():
         layers.append({"layer": l, "forward_start": f[0], "dispatch_done": f[1], "gemm1_start": f[2],
                        "forward_end": f[3], "gather_start": g[0] if g else None, "gather_end": g[1] if g else None,
                        "wait_ms": f[2] - f[1]})
-    print(json.dumps({"fp8": args.fp8, "tokens": args.tokens, "N": args.N, "link_gbs": args.link_gbs,
+    print(json.dumps({"fp8": args.fp8, "tokens": args.tokens, "N": args.N, "link_gbs": args.link_gbs, "gate": args.gate,
                       "step_ms": fwd[L - 1][3] - fwd[0][0], "layers": layers}), flush=True)
     scale = 100.0 / (fwd[L - 1][3] + 1e-9)
     for d in layers:

@@ -383,3 +383,31 @@ def test_stack_step_replays_as_cuda_graph(fp8):
             ref = wl.stack(max_tokens=T, compute_stream=cs).run(x_new).clone()
             cs.synchronize()
             assert torch.equal(_bits(got), _bits(ref)), seed
+
+
+@pytest.mark.parametrize("fp8", [False, True], ids=["bf16", "fp8"])
+def test_gated_gather_bitwise_and_no_hang(fp8):
+    """asyncep_set_gather_gate: a prefetched layer's gather starts only when the next forward has
+    finished its dispatch (the comm stream waits on a device word the compute stream writes); the
+    4-rank emulated stack still equals the resident one bitwise over repeated steps, and a prefetch
+    with no forward coming is released by turning the gate off."""
+    wl = Workload(L=3, E=16, k=4, H=512, h=256, seed=31, fp8=fp8)
+    T = 600
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    st = wl.stack(max_tokens=T, world_size=4, rank=1)
+    A.asyncep_set_link_emulation(st.ctx, 770e9)
+    A.asyncep_set_gather_gate(st.ctx, True)
+    sh = st.peer_shards()
+    for _ in range(3):
+        out = st.run(x, local_shards=sh).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(_bits(out), _bits(ref))
+    st.prefetch(1, sh)                       # no forward follows
+    A.asyncep_set_gather_gate(st.ctx, False)  # releases the waiting gather
+    torch.cuda.synchronize()
+    st.forward(1, x, y=torch.empty_like(x))  # the slot holds layer 1
+    A.asyncep_set_gather_gate(st.ctx, True)  # a new epoch works again
+    out = st.run(x, local_shards=sh).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(_bits(out), _bits(ref))
