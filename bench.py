@@ -267,6 +267,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--simt", action="store_true", help="CUDA-core GEMM (debug)")
     ap.add_argument("--xperm", action="store_true", help="materialise X_perm (FLAG_XPERM; the default)")
+    ap.add_argument("--gate", action="store_true",
+                    help="gated gather: each layer's gather starts after the previous forward's dispatch "
+                         "(asyncep_set_gather_gate)")
     ap.add_argument("--fused-dispatch", action="store_true",
                     help="GEMM1 gathers the token rows itself (FLAG_FUSED_DISPATCH)")
     ap.add_argument("--emulate-gather", type=int, default=0, metavar="N",
@@ -368,6 +371,8 @@ def main():
             A.asyncep_set_peer_shards(stack.ctx, None)
     if emu > 1 and args.link_gbs > 0:
         A.asyncep_set_link_emulation(stack.ctx, args.link_gbs * 1e9)
+    if args.gate and (world > 1 or emu > 1):
+        A.asyncep_set_gather_gate(stack.ctx, True)
     cu = None
     attn_flops_layer = 0.0
     if args.attn:
@@ -720,7 +725,7 @@ def main():
                                f"{T} tokens/GPU, {'FP8 e4m3 experts (bf16 router/activations)' if args.fp8 else 'BF16'}, "
                                "random-init weights" + (f", Zipf-skewed routing s={args.zipf} (R14)" if args.zipf else ""),
                    "tokens_per_gpu": T, "layers": L, "global_batch_tokens": T * world,
-                   "parallelism": par, "gather": gather_desc,
+                   "parallelism": par, "gather": gather_desc + (" (gated: starts after the dispatch)" if args.gate and gathered else ""),
                    "launch": ("one step captured as a CUDA graph, replayed per timed step (e2e runs eagerly)"
                               if args.graph else "eager stream launches"),
                    "l2": (f"inputs larger than L2 ({L * E_ * 3 * H_ * h_ * (1 if args.fp8 else 2) / 1e9:.1f} GB expert "
