@@ -65,8 +65,8 @@ typedef enum { ASYNCEP_BF16 = 0, ASYNCEP_FP8_E4M3 = 1 } asyncep_dtype;
                                                an explicit spelling; overrides FUSED_DISPATCH)      */
 #define ASYNCEP_FLAG_OFFLOAD         0x20 /* NEXT-2: expert_shard[l] may be NULL for offloaded layers  */
 #define ASYNCEP_FLAG_NO_SWAP_TAILS   0x40 /* compute every expert's last row tile as a padded 256-row
-                                               tile (default: swap-AB tail tiles where they pay,
-                                               FP8 gate/up GEMM; S6)                     */
+                                               tile (default: swap-AB tail tiles where they pay:
+                                               both BF16 GEMMs, the FP8 gate/up GEMM; S6) */
 #define ASYNCEP_FLAG_SWAP_TAILS      0x80 /* swap-AB tail tiles (<= 240 rows) in both GEMMs and both
                                                dtypes (A/B and tests)                               */
 #define ASYNCEP_FLAG_FUSED_DISPATCH 0x200 /* the fused dispatch: GEMM1's cp.async warps gather the

@@ -69,16 +69,17 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
 // Swap-AB tail tiles of the grouped GEMMs (gemm_tc.cu): an expert's last 256-row tile holding at
 // most this many rows runs with the weights as M and its tokens as N.  Same-process interleaved A/B
 // (profiles/ab_flags.py, profiles/r02/swap/ab_swap_*.jsonl): FP8 GEMM1 gains (stack +0.7 % at 32K,
-// +8 % at 16K, +23-25 % at 8K tokens/GPU); BF16 loses 0.5-1.7 % at 16-32K (a BF16 swap tile costs
-// more cycles than the padded tile it replaces, ncu r02/gemm1_ncu_full_16k_swap*.json) and the FP8
-// down GEMM (short K) loses 5-8 %.  Defaults: FP8 GEMM1 240 rows, the others off.
+// +8 % at 16K, +23-25 % at 8K tokens/GPU); the FP8 down GEMM (short K) loses 5-8 % (and 1-4 % per
+// step with the TMA-fed A, profiles/r02/swap_xperm/).  BF16 lost 0.5-1.7 % with the fused gather but
+// gains 1.3-1.6 % per step (GEMM1 -2 to -4 %) since the dispatch is materialised (swap_xperm/, both
+// A/B orders).  Defaults: 240 rows for both BF16 GEMMs and the FP8 GEMM1, the FP8 GEMM2 off.
 // ASYNCEP_SWAP_MAX_BF16 / ASYNCEP_SWAP_MAX_FP8 / ASYNCEP_SWAP_MAX_F8G2 override (0 = off).
 int env_rows(const char* name, int dflt) {
   const char* e = getenv(name);
   return (e && *e) ? atoi(e) : dflt;
 }
 int swap_max_rows(bool fp8, bool gemm2) {
-  static const int b = env_rows("ASYNCEP_SWAP_MAX_BF16", 0);
+  static const int b = env_rows("ASYNCEP_SWAP_MAX_BF16", 240);
   static const int f1 = env_rows("ASYNCEP_SWAP_MAX_FP8", 240);
   static const int f2 = env_rows("ASYNCEP_SWAP_MAX_F8G2", 0);
   return fp8 ? (gemm2 ? f2 : f1) : b;
