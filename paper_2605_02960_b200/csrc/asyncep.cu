@@ -869,9 +869,9 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (timing) CUDA_TRY(cudaEventRecord(ev[1], st));
   // (2) permute / dispatch
   aep::launch_perm_hist(ids, T, k, E, blk, st);
-  // Fused dispatch (default): GEMM1's cp.async gather warps read the token rows of x -- or of
-  // the token-major x_q -- through src_tok, so X_perm is never written.  ASYNCEP_FLAG_XPERM
-  // (and the identity / SIMT debug paths) materialise X_perm instead.
+  // Fused dispatch (optional, ASYNCEP_FLAG_FUSED_DISPATCH): GEMM1's cp.async gather warps read the
+  // token rows of x -- or of the token-major x_q -- through src_tok, so X_perm is never written.
+  // Otherwise (the default, and the identity / SIMT debug paths) X_perm is materialised.
   const bool fp8 = cf.expert_dtype == ASYNCEP_FP8_E4M3;
   const bool identity = (cf.flags & ASYNCEP_FLAG_IDENTITY_EXPERTS) != 0;
   // The dispatch materialises X_perm by default (BF16 rows, or the e4m3 rows the quantisation pass

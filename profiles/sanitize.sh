@@ -1,7 +1,12 @@
 #!/bin/bash
-mkdir -p gpurun_out
+# compute-sanitizer over small forwards (profiles/sanitize.py): the CUDA-core debug path under all
+# three tools, then the tcgen05 product path (BF16 / FP8 / fused dispatch / MX) under memcheck.
+O=${1:-gpurun_out}; mkdir -p $O
 for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python profiles/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
-  echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
-  tail -4 gpurun_out/sanitize_$tool.log
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python profiles/sanitize.py > $O/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?" >> $O/sanitize_$tool.log
+  tail -4 $O/sanitize_$tool.log
 done
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python profiles/sanitize.py --tc > $O/sanitize_memcheck_tc.log 2>&1
+echo "memcheck tc rc=$?" >> $O/sanitize_memcheck_tc.log
+tail -12 $O/sanitize_memcheck_tc.log
