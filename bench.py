@@ -81,21 +81,29 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
-def tensor_peak(peaks: dict, src: str, run_mhz, fp8: bool):
-    """Tensor peak for the dominant kernel, which is timed inside a long step: MEASURED_PEAKS'
-    sustained cuBLAS bf16 rate (FP8: x 2, the nominal fp8:bf16 dense ratio).  The burst figure and
-    the nominal per-clock rate at this run's median SM clock (8,192 bf16 FLOP/clk/SM x SMs x clock)
-    are returned beside it for context (a power-capped run's clock moves the achievable rate)."""
+def tensor_peak(peaks: dict, src: str, clk: dict, fp8: bool):
+    """Tensor peak for the dominant kernel (FP8: x 2, the nominal fp8:bf16 dense ratio), chosen
+    from this run's own clock record: a run that hit the power cap (or ran well below the maximum
+    SM clock) is a kernel inside a long step -> MEASURED_PEAKS' sustained cuBLAS rate; a run that
+    stayed at (>= 95 % of) the maximum clock with no throttle reason -> the burst rate.  Burst,
+    sustained and the nominal per-clock rate at the run's median SM clock (8,192 bf16 FLOP/clk/SM x
+    SMs x clock) are all returned for context."""
     burst = peaks.get("bf16_tflops", 1590.0)
     sus = peaks.get("bf16_tflops_sustained", burst)
     sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+    run_mhz, max_mhz = clk.get("sm_mhz"), clk.get("sm_max_mhz")
+    capped = bool(clk.get("reasons")) or not (run_mhz and max_mhz and run_mhz >= 0.95 * max_mhz)
     mult = 2.0 if fp8 else 1.0
-    note = f"{src} bf16_tflops_sustained {sus}" + (f" (median {sus_mhz} MHz under load)" if sus_mhz else "")
+    if capped:
+        peak, note = sus, f"{src} bf16_tflops_sustained {sus}" + (
+            f" (median {sus_mhz} MHz under load)" if sus_mhz else "") + " -- run power-capped / below max clock"
+    else:
+        peak, note = burst, f"{src} bf16_tflops {burst} (burst) -- run at max clock, no throttle reason"
     if fp8:
         note += " x 2 (nominal fp8:bf16 dense ratio)"
     nominal = 8192.0 * B200_SMS * run_mhz * 1e6 / 1e12 if run_mhz else None
-    return sus * mult, note, {"burst": burst * mult, "sustained": sus * mult,
-                              "nominal_at_run_clock": nominal * mult if nominal else None}
+    return peak * mult, note, {"burst": burst * mult, "sustained": sus * mult,
+                               "nominal_at_run_clock": nominal * mult if nominal else None}
 
 
 class ClockSampler:
@@ -586,7 +594,7 @@ def main():
     g1_ms = stages["gemm1_gateup_swiglu"] / max(nfwd, 1)
     g1_flops = GEMM1_FLOPS_TOK * T
     g1_tflops = g1_flops / (g1_ms / 1e3) / 1e12 if g1_ms > 0 else 0.0  # 0: no stage events (--ep)
-    peak_tf, peak_note, peak_ref = tensor_peak(peaks, peak_src, clk.get("sm_mhz"), args.fp8)
+    peak_tf, peak_note, peak_ref = tensor_peak(peaks, peak_src, clk, args.fp8)
     spec = SPEC_BF16 * (2.0 if args.fp8 else 1.0)
     traffic = ncu_traffic(args.fp8)
     per_layer_ms = {k: v / max(nfwd, 1) for k, v in stages.items()}
