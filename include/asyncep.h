@@ -20,7 +20,8 @@
  *    TMA descriptors.  The NCCL communicator is BORROWED (never destroyed).
  *  - All compute entry points enqueue work and return; no host synchronisation.
  *  - Every call returns an asyncep_status; asyncep_last_error() returns a thread-local
- *    message for the last failure.  Degenerate inputs (num_tokens == 0) are no-ops.
+ *    message for the last failure.  Degenerate inputs (num_tokens == 0) compute nothing
+ *    (the gather schedule's bookkeeping still runs, see asyncep_moe_forward).
  *  - Not thread-safe per context; one context per GPU per process.
  *  - Data types: bf16 = IEEE bfloat16 (2 B); e4m3 = OCP FP8 E4M3FN (1 B); fp32.
  */
@@ -269,7 +270,10 @@ ASYNCEP_API asyncep_status asyncep_set_gather_gate(asyncep_ctx* ctx, int32_t on)
  *  expert_counts_out [E] int32 : nullable device outputs (router decisions, in the
  *                  canonical order: descending logit, ties -> lower expert id).
  * Gathered layers require a prior asyncep_prefetch_layer(layer) (else NOT_PREFETCHED).
- * num_tokens == 0 is a successful no-op; num_tokens > max_tokens -> WORKSPACE.
+ * num_tokens == 0 computes nothing (x / y may be NULL) but keeps the schedule: a gathered layer must
+ * still have been prefetched, a held (gated) gather is started, and the slot is released in stream
+ * order after its gather, as a DP rank with an empty batch still takes part in every AllGather.
+ * num_tokens > max_tokens -> WORKSPACE.
  */
 ASYNCEP_API asyncep_status asyncep_moe_forward(asyncep_ctx* ctx, int32_t layer, const void* x,
                                    int64_t num_tokens, const void* residual, void* y,
@@ -302,7 +306,9 @@ ASYNCEP_API size_t asyncep_ep_workspace_size(const asyncep_config* cfg, int64_t 
  * to size the variable AllToAlls, as an EP layer must).  Uses the context's NCCL communicator
  * (ncclSend/ncclRecv groups on the compute stream; a device copy when world_size == 1 and no
  * communicator is given) and this rank's shard of `layer`.  x, residual, y as in
- * asyncep_moe_forward.  ERR_WORKSPACE if more than max_recv_rows rows arrive.
+ * asyncep_moe_forward.  ERR_WORKSPACE if more than max_recv_rows rows arrive.  num_tokens == 0
+ * at world_size > 1 still joins both AllToAlls (no rows sent; rows received for this rank's
+ * experts are computed and returned).
  */
 ASYNCEP_API asyncep_status asyncep_ep_forward(asyncep_ctx* ctx, int32_t layer, const void* x, int64_t num_tokens,
                                               const void* residual, void* y, void* ep_workspace,

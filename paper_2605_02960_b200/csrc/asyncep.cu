@@ -808,13 +808,12 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
   if (T < 0) return fail(ASYNCEP_ERR_INVALID_ARG, "num_tokens < 0");
   if (T > cf.max_tokens) return fail(ASYNCEP_ERR_WORKSPACE, "num_tokens %lld > max_tokens %lld", (long long)T,
                                      (long long)cf.max_tokens);
-  if (T == 0) return ASYNCEP_OK;
-  if (!x || !y) return fail(ASYNCEP_ERR_INVALID_ARG, "x / y is NULL");
+  if (T > 0 && (!x || !y)) return fail(ASYNCEP_ERR_INVALID_ARG, "x / y is NULL");
   NvtxRange nv("asyncep_moe_forward L%d", layer);
   if (asyncep_status e = check_nccl_async(c)) return e;
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "x / y / residual must be 16-B aligned");
-  if (x == y) return fail(ASYNCEP_ERR_INVALID_ARG, "y must not alias x");
+  if (T > 0 && x == y) return fail(ASYNCEP_ERR_INVALID_ARG, "y must not alias x");
   const bool from_window = c->offload && cf.world_size == 1 && layer > 0;  // NEXT-2, N == 1
   const bool res = !from_window && layer_resident(c, layer);
   const int s = layer % 2;
@@ -823,6 +822,25 @@ asyncep_status asyncep_moe_forward(asyncep_ctx* c, int32_t layer, const void* x,
     return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not staged (asyncep_stage_layer)", layer);
   if (!res && !from_window && (c->slot_layer[s] != layer || c->slot_consumed[s]))
     return fail(ASYNCEP_ERR_NOT_PREFETCHED, "layer %d was not prefetched", layer);
+  if (T == 0) {
+    // No tokens on this rank (a DP rank with an empty batch still takes part in every gather): no
+    // compute, but the schedule's bookkeeping stays -- held gathers start, and the slot / window
+    // buffer is released in stream order after its gather, so the next prefetch into it proceeds.
+    cudaStream_t st0 = c->cs;
+    if (!c->pending.empty()) {
+      if (asyncep_status e = flush_pending(c, true, st0)) return e;
+    }
+    if (from_window) {
+      CUDA_TRY(cudaStreamWaitEvent(st0, c->h2d_done[wi], 0));
+      CUDA_TRY(cudaEventRecord(c->win_free[wi], st0));
+      c->win_consumed[wi] = true;
+    } else if (!res) {
+      CUDA_TRY(cudaStreamWaitEvent(st0, c->ag_done[s], 0));
+      CUDA_TRY(cudaEventRecord(c->slot_free[s], st0));
+      c->slot_consumed[s] = true;
+    }
+    return ASYNCEP_OK;
+  }
 
   const int E = cf.num_experts, k = cf.top_k, H = cf.hidden, h = cf.ffn;
   cudaStream_t st = c->cs;
@@ -1051,8 +1069,10 @@ asyncep_status asyncep_ep_forward(asyncep_ctx* c, int32_t layer, const void* x, 
   if (layer < 0 || layer >= cf.num_layers) return fail(ASYNCEP_ERR_INVALID_ARG, "layer out of range");
   if (cf.expert_dtype != ASYNCEP_BF16) return fail(ASYNCEP_ERR_UNSUPPORTED, "EP contrast layer is BF16 only");
   if (T < 0 || T > cf.max_tokens) return fail(ASYNCEP_ERR_WORKSPACE, "num_tokens out of range");
-  if (T == 0) return ASYNCEP_OK;
-  if (!x || !y || !ep_ws || max_recv_rows <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "null argument");
+  // T == 0 at N == 1: nothing to do; at N > 1 the rank still joins both AllToAlls (it sends no rows
+  // but computes the rows other ranks send to its experts)
+  if (T == 0 && cf.world_size == 1) return ASYNCEP_OK;
+  if ((T > 0 && (!x || !y)) || !ep_ws || max_recv_rows <= 0) return fail(ASYNCEP_ERR_INVALID_ARG, "null argument");
   if (((uintptr_t)x | (uintptr_t)y | (uintptr_t)residual | (uintptr_t)ep_ws) & 15)
     return fail(ASYNCEP_ERR_INVALID_ARG, "pointers must be 16-B aligned");
   NvtxRange nv("asyncep_ep_forward L%d", layer);
@@ -1088,14 +1108,18 @@ asyncep_status asyncep_ep_forward(asyncep_ctx* c, int32_t layer, const void* x, 
   int* sched = (int*)(ws + c->L.sched);
   const int nblk = (int)((T + aep::kPermTokensPerBlock - 1) / aep::kPermTokensPerBlock);
   CUDA_TRY(cudaMemsetAsync(sched, 0, 16, st));
-  // (1) router + (2) local permute, as in the AsyncEP forward
-  if (!aep::launch_router_tc(c->router_maps[layer], (const bf16*)x, T, H, E, k, cf.norm_topk, ids, w, c->num_sms,
-                             st, sched))
-    return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router x map)");
-  aep::launch_perm_hist(ids, T, k, E, blk, st);
-  aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
-  aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok, xperm, st);
-  c->launches += 4;
+  if (T > 0) {
+    // (1) router + (2) local permute, as in the AsyncEP forward
+    if (!aep::launch_router_tc(c->router_maps[layer], (const bf16*)x, T, H, E, k, cf.norm_topk, ids, w, c->num_sms,
+                               st, sched))
+      return fail(ASYNCEP_ERR_CUDA, "cuTensorMapEncodeTiled failed (router x map)");
+    aep::launch_perm_hist(ids, T, k, E, blk, st);
+    aep::launch_perm_scan(blk, nblk, E, offsets, tile_start, counts, (unsigned int*)(ws + c->L.done), src_tok, st);
+    aep::launch_perm_scatter((const bf16*)x, ids, blk, offsets, T, H, k, E, dest, src_tok, xperm, st);
+    c->launches += 4;
+  } else {
+    CUDA_TRY(cudaMemsetAsync(counts, 0, (size_t)E * 4, st));  // sends no rows
+  }
   // (a) exchange the per-expert counts (E/N to every rank), read them back: host sync
   int32_t* d_rc = (int32_t*)(ew + EL.rcounts);
   if (N > 1) {
@@ -1163,8 +1187,10 @@ asyncep_status asyncep_ep_forward(asyncep_ctx* c, int32_t layer, const void* x, 
   xs = exchange(recv, ro, rr, xperm, so, sr);
   if (xs) return xs;
   // (e) weighted combine (+ residual)
-  aep::launch_combine(xperm, dest, w, (const bf16*)residual, (bf16*)y, T, H, k, st);
-  c->launches += 1;
+  if (T > 0) {
+    aep::launch_combine(xperm, dest, w, (const bf16*)residual, (bf16*)y, T, H, k, st);
+    c->launches += 1;
+  }
   CUDA_TRY(cudaGetLastError());
   return ASYNCEP_OK;
 }

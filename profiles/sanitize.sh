@@ -1,4 +1,6 @@
 #!/bin/bash
+# (Round 2: compute-sanitizer is closed on the GPU pool -- profiles/r02/sanitize/; tests/test_gpu_guard.py
+# checks the product path for out-of-bounds writes with guard bands instead.)
 # compute-sanitizer over small forwards (profiles/sanitize.py): the CUDA-core debug path under all
 # three tools, then the tcgen05 product path (BF16 / FP8 / fused dispatch / MX) under memcheck.
 O=${1:-gpurun_out}; mkdir -p $O

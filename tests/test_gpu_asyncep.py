@@ -411,3 +411,30 @@ def test_gated_gather_bitwise_and_no_hang(fp8):
     out = st.run(x, local_shards=sh).clone()
     torch.cuda.synchronize()
     assert torch.equal(_bits(out), _bits(ref))
+
+
+@pytest.mark.parametrize("gate", [False, True], ids=["ungated", "gated"])
+def test_empty_batch_keeps_the_gather_schedule(gate):
+    """A DP rank with no tokens this step still takes part in every gather (the other ranks' NCCL
+    AllGathers need it): asyncep_moe_forward with num_tokens == 0 computes nothing but releases the
+    layer's slot in stream order (and starts a held, gated gather), so the next prefetch into that
+    slot proceeds.  Steps with 0 tokens between real steps leave the real steps bitwise equal to the
+    resident stack."""
+    wl = Workload(L=4, E=16, k=4, H=256, h=256, seed=33)
+    T = 300
+    x = wl.tokens(T)
+    ref = wl.stack(max_tokens=T).run(x).clone()
+    st = wl.stack(max_tokens=T, world_size=2, rank=0)
+    if gate:
+        A.asyncep_set_gather_gate(st.ctx, True)
+    sh = st.peer_shards()
+    empty = x[:0]
+    for _ in range(2):
+        e = st.run(empty, local_shards=sh)
+        assert e.shape == (0, wl.H)
+        out = st.run(x, local_shards=sh).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(_bits(out), _bits(ref))
+    # the empty forward still enforces the schedule: a gathered layer that was not prefetched
+    with pytest.raises(A.AsyncEPError):
+        st.forward(3, empty, y=empty)

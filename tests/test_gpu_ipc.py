@@ -56,6 +56,19 @@ def _rank(rank, world, port, q, transport="kernel"):
         ref = wl.stack(max_tokens=T).run(x).clone()
         torch.cuda.synchronize()
         ok = all(torch.equal(o.view(torch.int16), ref.view(torch.int16)) for o in outs)
+        if nccl:
+            # rank 1 has an empty batch: it still joins every AllGather (and both AllToAlls of the
+            # EP contrast layer, computing rank 0's rows for its experts); rank 0's output is unchanged
+            xin = x if rank == 0 else x[:0]
+            o2 = st.run(xin).clone()
+            ep_ref = wl.stack(max_tokens=T).run_ep(x).clone()  # N = 1: equals the AsyncEP stack
+            o3 = st.run_ep(xin).clone()
+            torch.cuda.synchronize()
+            if rank == 0:
+                ok = ok and torch.equal(o2.view(torch.int16), ref.view(torch.int16))
+                ok = ok and torch.equal(o3.view(torch.int16), ep_ref.view(torch.int16))
+            else:
+                ok = ok and o2.shape[0] == 0 and o3.shape[0] == 0
         dist.barrier()  # keep this rank's shards mapped until the peer is done
         q.put((rank, ok, ""))
     except Exception as e:  # report instead of hanging the parent

@@ -134,10 +134,11 @@ def test_schedule_invariants():
         shard_range(100, 8, 0)
 
 
-def _ep_rank(rank, world, port, q):
+def _ep_rank(rank, world, port, q, empty=False):
     """Each rank routes its own tokens (oracle router), exchanges per-expert counts with a
     real gloo all_to_all, and plans the DP x EP exchange with the library's asyncep_ep_plan.
-    The plans must agree pairwise: what r sends to d is what d expects from r."""
+    The plans must agree pairwise: what r sends to d is what d expects from r.  empty: the last
+    rank has no tokens this step (it sends nothing but still receives rows for its experts)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -148,6 +149,8 @@ def _ep_rank(rank, world, port, q):
         wr = synth.router_weight(E_, 64, 0, 0, zipf_s=1.0).float().numpy()
         ids = oracle.router(x, wr, 4)["ids"]
         counts = np.bincount(ids.ravel(), minlength=E_).astype(np.int32)
+        if empty and rank == world - 1:
+            counts[:] = 0
         recv = torch.empty(E_, dtype=torch.int32)
         dist.all_to_all_single(recv, torch.from_numpy(counts), [per] * world, [per] * world)
         cfg = A.make_config(1, E_, 4, 64, 128, world_size=world, rank=rank, max_tokens=300)
@@ -155,17 +158,21 @@ def _ep_rank(rank, world, port, q):
         sr = torch.from_numpy(plan["send_rows"])
         rr = torch.empty(world, dtype=torch.int64)
         dist.all_to_all_single(rr, sr, [1] * world, [1] * world)  # what each source plans to send me
-        q.put((rank, bool(np.array_equal(rr.numpy(), plan["recv_rows"])), int(counts.sum())))
+        ok = bool(np.array_equal(rr.numpy(), plan["recv_rows"]))
+        if empty and rank == world - 1:
+            ok = ok and int(plan["send_rows"].sum()) == 0 and int(plan["recv_total"]) > 0
+        q.put((rank, ok, int(counts.sum())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_ep_exchange_plan_over_gloo(world):
+@pytest.mark.parametrize("world,empty", [(2, False), (4, False), (2, True), (4, True)],
+                         ids=["w2", "w4", "w2_empty_rank", "w4_empty_rank"])
+def test_ep_exchange_plan_over_gloo(world, empty):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ep_rank, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_ep_rank, args=(r, world, port, q, empty)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -174,4 +181,4 @@ def test_ep_exchange_plan_over_gloo(world):
         assert p.exitcode == 0
     for rank, ok, n in res:
         assert ok, f"rank {rank}: receive plan disagrees with the senders' plans"
-        assert n == 300 * 4
+        assert n == (0 if empty and rank == world - 1 else 300 * 4)
