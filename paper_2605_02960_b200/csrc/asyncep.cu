@@ -59,13 +59,7 @@ cudaError_t gather_copy(void* dst, const void* src, size_t n, cudaStream_t st, u
                         int mode = ASYNCEP_GATHER_COPY_KERNEL, int ctas = 0) {
   if (mode == ASYNCEP_GATHER_COPY_KERNEL && ((uintptr_t)dst % 16 == 0) && ((uintptr_t)src % 16 == 0) && n % 16 == 0) {
     static const int dflt = default_copy_ctas();
-    // ASYNCEP_GATHER_EXCL=<KB>: exclusive copy CTAs (1024 threads, KB of shared memory each, so they
-    // never share an SM with a GEMM CTA; pair with ASYNCEP_RESERVE_SMS and ASYNCEP_GATHER_CTAS)
-    static const int excl = [] {
-      const char* e = getenv("ASYNCEP_GATHER_EXCL");
-      return (e && *e && atoi(e) > 0) ? atoi(e) * 1024 : 0;
-    }();
-    aep::launch_gather_copy(dst, src, n, ctas > 0 ? ctas : dflt, st, min_ns, excl);
+    aep::launch_gather_copy(dst, src, n, ctas > 0 ? ctas : dflt, st, min_ns);
     return cudaGetLastError();
   }
   if (min_ns) aep::launch_spin_ns(min_ns, st);  // copy engine: link time, then the copy

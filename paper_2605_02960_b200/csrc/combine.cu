@@ -83,17 +83,13 @@ __global__ void spin_ns_kernel(uint64_t ns) {
 // so a chunk takes max(copy, link) time, and ns_per_round > 0: every CTA paces itself -- round r of its strided share
 // may start only ns_per_round * r after the kernel started -- so the copy streams smoothly at the
 // emulated link rate over the whole chunk, like a remote read, instead of bursting at HBM speed.
-// Exclusive mode (launch_gather_copy with smem_bytes > 0): 1024-thread CTAs that request enough
-// shared memory not to fit beside a GEMM CTA, so they run only on the SMs the grouped GEMMs leave
-// free (ASYNCEP_RESERVE_SMS) instead of sharing every SM's L1 / shared-memory data path with them.
 constexpr int kCopyUnroll = 8;
-template <int NT>
-__global__ void __launch_bounds__(NT) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
-                                                         size_t n16, uint64_t ns_per_round, uint64_t min_ns) {
+__global__ void __launch_bounds__(128) gather_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src,
+                                                          size_t n16, uint64_t ns_per_round, uint64_t min_ns) {
   uint64_t t0 = 0;
   if (ns_per_round || min_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  const size_t stride = (size_t)gridDim.x * NT;
-  size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * 128;
+  size_t i = (size_t)blockIdx.x * 128 + threadIdx.x;
   uint64_t round = 0;
   for (; i + (kCopyUnroll - 1) * stride < n16; i += kCopyUnroll * stride) {
     if (ns_per_round) {
@@ -124,27 +120,15 @@ __global__ void __launch_bounds__(NT) gather_copy_kernel(uint4* __restrict__ dst
 
 void launch_spin_ns(uint64_t ns, cudaStream_t s) { spin_ns_kernel<<<1, 1, 0, s>>>(ns); }
 
-void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns,
-                        int smem_bytes) {
+void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns) {
   if (!bytes) return;
   const size_t n16 = bytes / 16;
-  const int nt = smem_bytes > 0 ? 1024 : 128;
-  // pacing: the chunk must take min_ns; a CTA's share is split into rounds of nt x kCopyUnroll x 16 B
-  const size_t per_round = (size_t)ctas * nt * kCopyUnroll;
+  // pacing: the chunk must take min_ns; a CTA's share is split into rounds of 128 x kCopyUnroll x 16 B
+  const size_t per_round = (size_t)ctas * 128 * kCopyUnroll;
   const uint64_t rounds = (n16 + per_round - 1) / per_round;
   const uint64_t ns_per_round = (min_ns && rounds) ? min_ns / rounds : 0;
-  if (smem_bytes > 0) {
-    static int set = 0;
-    if (set != smem_bytes) {
-      cudaFuncSetAttribute(gather_copy_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-      set = smem_bytes;
-    }
-    gather_copy_kernel<1024><<<ctas, 1024, smem_bytes, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src),
-                                                            n16, ns_per_round, min_ns);
-  } else {
-    gather_copy_kernel<128><<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
-                                                 ns_per_round, min_ns);
-  }
+  gather_copy_kernel<<<ctas, 128, 0, s>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), n16,
+                                         ns_per_round, min_ns);
 }
 
 void launch_combine(const bf16* yperm, const int32_t* dest, const float* w, const bf16* residual, bf16* y,

@@ -145,8 +145,7 @@ void launch_pack_fp8(const uint8_t* gate, const uint8_t* up, const uint8_t* down
 // One thread spinning on %globaltimer for `ns` nanoseconds (link-bandwidth emulation).
 // co-resident SM copy (gather transport); bytes % 16 == 0, 16-B aligned pointers
 // min_ns > 0: the copy takes at least min_ns (1-GPU link emulation, overlapping copy and link time)
-void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns = 0,
-                        int smem_bytes = 0);
+void launch_gather_copy(void* dst, const void* src, size_t bytes, int ctas, cudaStream_t s, uint64_t min_ns = 0);
 void launch_spin_ns(uint64_t ns, cudaStream_t s);
 
 // ---- NEXT-3 attention layer (attn.cu) ----
