@@ -491,22 +491,38 @@ def main():
     for _ in range(args.warmup):
         _run(x, out)
     barrier()
-    A.asyncep_reset_stage_times(stack.ctx)
-    launches0 = A.asyncep_kernel_launches(stack.ctx)
-    clocks = ClockSampler(dev_idx).start()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(cs)
-    for _ in range(args.steps):
-        torch.cuda.nvtx.range_push("step")
-        _run(x, out)
-        torch.cuda.nvtx.range_pop()
-    e1.record(cs)
-    barrier()
-    clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    launches = A.asyncep_kernel_launches(stack.ctx) - launches0
+    # The timed region.  A run whose clock record shows a hardware / thermal slowdown is rejected
+    # and re-measured once (the task's timing rule); sw_power_cap is kept and noted.
+    bad_reasons = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "hw_power_brake_slowdown"}
+    rejected = None
+    for attempt in range(2):
+        A.asyncep_reset_stage_times(stack.ctx)
+        launches0 = A.asyncep_kernel_launches(stack.ctx)
+        clocks = ClockSampler(dev_idx).start()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(cs)
+        for _ in range(args.steps):
+            torch.cuda.nvtx.range_push("step")
+            _run(x, out)
+            torch.cuda.nvtx.range_pop()
+        e1.record(cs)
+        barrier()
+        clk = clocks.stop()
+        ms = e0.elapsed_time(e1)
+        launches = A.asyncep_kernel_launches(stack.ctx) - launches0
+        bad = sorted(set(clk.get("reasons") or []) & bad_reasons)
+        if world > 1:  # every rank takes the same decision
+            t = torch.tensor([1 if bad else 0], device=dev if backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bad = bad or (["on another rank"] if int(t.item()) else [])
+        if not bad or attempt == 1:
+            break
+        rejected = {"ms": ms, "reasons": bad, "sm_mhz": clk.get("sm_mhz")}
+        print(f"bench.py: timed region saw {bad}; re-measuring once", file=sys.stderr)
+    if rejected:
+        clk["remeasured_after"] = rejected
     # NEXT-1 (App. B.4): T from the last timed step as the profile pass -- t_c = the
     # resident layer 0, t_e = the slowest gathered layer, C_dummy = f_tok x tokens (in the library)
     calib = None  # (N = 1 without offload: nothing is transferred, Eq. 3 has no t_EP to calibrate)
