@@ -19,9 +19,9 @@ def _bits(t):
     return t.contiguous().view(torch.int16)
 
 
-@pytest.mark.parametrize("N", [2, 4, 8])
-def test_sharded_stack_bitwise_equals_resident(N):
-    wl = Workload(L=5, E=16, k=4, H=256, h=256, seed=11)
+@pytest.mark.parametrize("N,fp8", [(2, False), (4, False), (8, False), (8, True)])
+def test_sharded_stack_bitwise_equals_resident(N, fp8):
+    wl = Workload(L=5, E=16, k=4, H=256, h=256, seed=11, fp8=fp8)
     T = 1500
     x = wl.tokens(T)
     ref = wl.stack(max_tokens=T).run(x).clone()
@@ -229,13 +229,14 @@ def test_ep_contrast_layer_matches_asyncep_forward():
     assert torch.equal(_bits(out), _bits(ref))
 
 
-@pytest.mark.parametrize("N,w", [(1, 1), (1, 2), (2, 2), (4, 3)])
-def test_offload_window_bitwise_equals_resident(N, w):
+@pytest.mark.parametrize("N,w,fp8", [(1, 1, False), (1, 2, False), (2, 2, False), (4, 3, False), (1, 2, True),
+                                     (4, 3, True)])
+def test_offload_window_bitwise_equals_resident(N, w, fp8):
     """NEXT-2 hybrid offload: shards in pinned host memory, a w-deep device
     window filled over PCIe on a third stream, then gathered (N > 1, emulated locally) or
     computed directly (N == 1).  Two passes reuse every window buffer; the output must equal
-    the resident stack bit for bit."""
-    wl = Workload(L=5, E=16, k=4, H=256, h=256, seed=19)
+    the resident stack bit for bit (FP8 blobs too: codes and scales travel as bytes)."""
+    wl = Workload(L=5, E=16, k=4, H=256, h=256, seed=19, fp8=fp8)
     T = 640
     x = wl.tokens(T)
     ref = wl.stack(max_tokens=T).run(x).clone()
